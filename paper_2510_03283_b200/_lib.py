@@ -1,0 +1,93 @@
+"""ctypes binding of libmace_b200.so (the C-ABI declared in include/mace_b200.h).
+
+There is deliberately no fallback: if the shared library is missing or no sm_100 device is present,
+``Lib()`` / ``Ctx()`` raise. The product path never routes through torch math or the oracle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libmace_b200.so"
+
+
+class MaceError(RuntimeError):
+    pass
+
+
+class MaceGemmArgs(C.Structure):
+    _fields_ = [
+        ("a", C.c_void_p), ("lda", C.c_int), ("a_mn_major", C.c_int),
+        ("b", C.c_void_p), ("ldb", C.c_int), ("b_mn_major", C.c_int),
+        ("M", C.c_int), ("N", C.c_int), ("K", C.c_int),
+        ("out", C.c_void_p), ("ldo", C.c_int), ("mode", C.c_int),
+        ("bias", C.c_void_p), ("alpha", C.c_float), ("split_k", C.c_int),
+        ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+    ]
+
+
+# (name, argtypes) for every symbol include/mace_b200.h declares; checked by tests/test_abi.py
+SIGNATURES: dict[str, tuple[type, list]] = {
+    "mace_version": (C.c_int, []),
+    "mace_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "mace_ctx_destroy": (C.c_int, [C.c_void_p]),
+    "mace_last_error": (C.c_char_p, [C.c_void_p]),
+    "mace_launch_count": (C.c_longlong, [C.c_void_p]),
+    "mace_gemm_bf16": (C.c_int, [C.c_void_p, C.POINTER(MaceGemmArgs), C.c_void_p]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> C.CDLL:
+    """Load the in-tree library once; raise loudly if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise MaceError(
+                    f"{LIB_PATH} is missing: run `python -m paper_2510_03283_b200.build` "
+                    "(the CUDA path has no CPU fallback)"
+                )
+            L = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+        return _lib
+
+
+class Ctx:
+    """One mace_ctx (per engine / thread). Owns nothing but the handle."""
+
+    def __init__(self, device: int = 0):
+        self.L = lib()
+        h = C.c_void_p()
+        rc = self.L.mace_ctx_create(device, C.byref(h))
+        if rc != 0:
+            raise MaceError(f"mace_ctx_create(device={device}) failed with status {rc} (needs an sm_100 GPU)")
+        self.h = h
+
+    def check(self, rc: int, what: str) -> None:
+        if rc != 0:
+            msg = self.L.mace_last_error(self.h).decode(errors="replace")
+            raise MaceError(f"{what} failed ({rc}): {msg}")
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.mace_launch_count(self.h))
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.L.mace_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

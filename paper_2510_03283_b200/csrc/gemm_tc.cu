@@ -1,0 +1,374 @@
+// bf16 tcgen05 GEMM for sm_100a: C[M,N] = alpha * A[M,K] . B[N,K]^T  (+bias, +=C, split-K)
+//
+// Replaces the cost-model stand-in for the packed QKV / O / MLP / lm_head projections of the
+// hybrid iteration (reference: engine.py:588-600 charges prefill/decode/FT latency from
+// cost_model.get_workload, cost_model.py:92-106) and their backward on fine-tune rows.
+//
+// Design (B200-first):
+//  * persistent, one CTA per SM, static tile schedule (tile = blockIdx.x + i * gridDim.x)
+//  * warp 0: TMA producer (cp.async.bulk.tensor, 128B swizzle) over a kStages smem ring
+//  * warp 1: single-thread tcgen05.mma issuer (M=128, N=BN, K=16 per instruction)
+//  * warp 2: TMEM allocator (2 accumulator buffers -> epilogue of tile i overlaps MMA of i+1)
+//  * warps 4..7: epilogue, tcgen05.ld 32x32b -> registers -> fused bias / residual / convert
+//  * operands may be K-major (row-major [rows, K]) or MN-major (row-major [K, rows]); the MN-major
+//    form is what the fine-tune backward needs (dX = dY.W and dW = dY^T.X) without transposes.
+#include "common.cuh"
+#include "mace_internal.h"
+
+namespace mace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16 along K
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kABytes = kBM * kBK * 2;  // 16 KB
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct GemmParams {
+  int M, N, K;
+  int num_m, num_n, splits, kb_total, kb_per_split;
+  GemmEpilogue ep;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const GemmParams p) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + S * Cfg::kABytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int num_tiles = p.num_m * p.num_n * p.splits;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m_blk = t % p.num_m;
+        const int n_blk = (t / p.num_m) % p.num_n;
+        const int split = t / (p.num_m * p.num_n);
+        const int kb0 = split * p.kb_per_split;
+        const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+          uint8_t* sa = smem_a + stage * Cfg::kABytes;
+          uint8_t* sb = smem_b + stage * Cfg::kBBytes;
+          if (!A_MN) {
+            tma_load_2d(sa, &map_a, &full_bar[stage], kb * kBK, m_blk * kBM);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j)
+              tma_load_2d(sa + j * (64 * kBK * 2), &map_a, &full_bar[stage], m_blk * kBM + j * 64, kb * kBK);
+          }
+          if (!B_MN) {
+            tma_load_2d(sb, &map_b, &full_bar[stage], kb * kBK, n_blk * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sb + j * (64 * kBK * 2), &map_b, &full_bar[stage], n_blk * BN + j * 64, kb * kBK);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer (single thread)
+      constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int split = t / (p.num_m * p.num_n);
+        const int kb0 = split * p.kb_per_split;
+        const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::kABytes);
+          const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            // K-major: advance 16 elems = 32 B inside the swizzle atom; SBO = 8 rows * 128 B.
+            // MN-major: advance 16 K-rows = 2048 B; LBO = one 64-wide MN block (64 rows * 128 B).
+            const uint64_t ad = A_MN ? smem_desc_sw128(a_addr + k * 2048, 64 * kBK * 2, 1024)
+                                     : smem_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
+                                     : smem_desc_sw128(b_addr + k * 32, 16, 1024);
+            umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue (128 threads <-> 128 TMEM lanes)
+    const uint32_t quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const GemmEpilogue& ep = p.ep;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m_blk = t % p.num_m;
+      const int n_blk = (t / p.num_m) % p.num_n;
+      const int split = t / (p.num_m * p.num_n);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = m_blk * kBM + quarter * 32 + lane;
+      const bool row_ok = row < p.M;
+      const bool add_bias = ep.bias != nullptr && split == 0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + acc * BN + c0, r);
+        tmem_ld_wait();
+        const int col0 = n_blk * BN + c0;
+        if (!row_ok || col0 >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
+        if (add_bias) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < p.N) v[j] += __bfloat162float(ep.bias[col0 + j]);
+        }
+        const bool full = (col0 + 32 <= p.N) && ((ep.ldo & 7) == 0);
+        if (ep.mode == EPI_BF16) {
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ep.out) + (size_t)row * ep.ldo + col0;
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint4 w = make_uint4(pack_bf16(v[j], v[j + 1]), pack_bf16(v[j + 2], v[j + 3]),
+                                   pack_bf16(v[j + 4], v[j + 5]), pack_bf16(v[j + 6], v[j + 7]));
+              *reinterpret_cast<uint4*>(out + j) = w;
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) out[j] = __float2bfloat16(v[j]);
+          }
+        } else if (ep.mode == EPI_F32) {
+          float* out = reinterpret_cast<float*>(ep.out) + (size_t)row * ep.ldo + col0;
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) out[j] = v[j];
+          }
+        } else if (ep.mode == EPI_F32_ADD) {
+          // out += v (exclusive owner of the tile: plain read-modify-write)
+          float* out = reinterpret_cast<float*>(ep.out) + (size_t)row * ep.ldo + col0;
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 o = *reinterpret_cast<float4*>(out + j);
+              o.x += v[j]; o.y += v[j + 1]; o.z += v[j + 2]; o.w += v[j + 3];
+              *reinterpret_cast<float4*>(out + j) = o;
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) out[j] += v[j];
+          }
+        } else {  // EPI_F32_ATOMIC: split-K partials / shared accumulation
+          float* out = reinterpret_cast<float*>(ep.out) + (size_t)row * ep.ldo + col0;
+          for (int j = 0; j < 32 && col0 + j < p.N; ++j) atomicAdd(out + j, v[j]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+// split-K finalize: ws fp32 [M,N] -> bf16 out (bias already added by split 0)
+__global__ void gemm_finalize_bf16(const float* __restrict__ ws, int M, int N, __nv_bfloat16* __restrict__ out,
+                                   int ldo) {
+  const size_t total = (size_t)M * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / N, c = i % N;
+    out[r * ldo + c] = __float2bfloat16(ws[i]);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static int make_map(MaceCtx* ctx, CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                    uint32_t box_inner, uint32_t box_outer) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = ctx->encode_tiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -1;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch_gemm(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStream_t stream, const GemmEpilogue& ep) {
+  using Cfg = GemmCfg<BN>;
+  CUtensorMap ma, mb;
+  // A logical [M,K]; K-major storage [M, lda>=K], MN-major storage [K, lda>=M]
+  int rc = A_MN ? make_map(ctx, &ma, g->a, g->M, g->K, g->lda, 64, kBK) : make_map(ctx, &ma, g->a, g->K, g->M, g->lda, kBK, kBM);
+  if (rc) return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm: tensor map A encode failed");
+  rc = B_MN ? make_map(ctx, &mb, g->b, g->N, g->K, g->ldb, 64, kBK) : make_map(ctx, &mb, g->b, g->K, g->N, g->ldb, kBK, BN);
+  if (rc) return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm: tensor map B encode failed");
+  GemmParams p;
+  p.M = g->M;
+  p.N = g->N;
+  p.K = g->K;
+  p.num_m = (g->M + kBM - 1) / kBM;
+  p.num_n = (g->N + BN - 1) / BN;
+  p.kb_total = (g->K + kBK - 1) / kBK;
+  p.kb_per_split = (p.kb_total + splits - 1) / splits;
+  p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  p.ep = ep;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;  // per-instantiation; attribute is process-wide and idempotent
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    attr_set = true;
+  }
+  const int tiles = p.num_m * p.num_n * p.splits;
+  const int grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
+  kern<<<grid, 256, Cfg::kSmemBytes, stream>>>(ma, mb, p);
+  ctx->launches++;
+  return 0;
+}
+
+template <int BN>
+static int dispatch_major(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStream_t s, const GemmEpilogue& ep) {
+  if (!g->a_mn_major && !g->b_mn_major) return launch_gemm<BN, false, false>(ctx, g, splits, s, ep);
+  if (!g->a_mn_major && g->b_mn_major) return launch_gemm<BN, false, true>(ctx, g, splits, s, ep);
+  if (g->a_mn_major && !g->b_mn_major) return launch_gemm<BN, true, false>(ctx, g, splits, s, ep);
+  return launch_gemm<BN, true, true>(ctx, g, splits, s, ep);
+}
+
+}  // namespace mace
+
+using namespace mace;
+
+extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* stream_) {
+  MaceCtx* ctx = ctx_;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  if (!ctx || !g) return MACE_ERR_ARG;
+  if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 0;  // empty ragged batch: nothing to do
+  if ((g->lda & 7) || (g->ldb & 7) || ((uintptr_t)g->a & 15) || ((uintptr_t)g->b & 15))
+    return mace_fail(ctx, MACE_ERR_ARG, "gemm: operands need 16-byte aligned rows (ld % 8 == 0)");
+  if (g->mode < EPI_BF16 || g->mode > EPI_F32_ATOMIC) return mace_fail(ctx, MACE_ERR_ARG, "gemm: bad epilogue mode");
+
+  // tile shape / split-K heuristic: fill the 148 SMs
+  const int num_m = (g->M + kBM - 1) / kBM;
+  const int kb_total = (g->K + kBK - 1) / kBK;
+  int bn = 256;
+  if ((long)num_m * ((g->N + 255) / 256) < ctx->num_sms) bn = 128;
+  if (bn == 128 && (long)num_m * ((g->N + 127) / 128) < ctx->num_sms / 2) bn = 64;
+  const long tiles = (long)num_m * ((g->N + bn - 1) / bn);
+  int splits = g->split_k > 0 ? g->split_k : 1;
+  if (g->split_k <= 0 && tiles < ctx->num_sms) {
+    splits = (int)(ctx->num_sms / tiles);
+    int max_split = kb_total / 4;  // keep >= 4 k-blocks per split
+    if (splits > max_split) splits = max_split;
+    if (splits < 1) splits = 1;
+  }
+  GemmEpilogue ep;
+  ep.out = g->out;
+  ep.ldo = g->ldo;
+  ep.bias = reinterpret_cast<const __nv_bfloat16*>(g->bias);
+  ep.alpha = g->alpha == 0.f ? 1.f : g->alpha;
+  ep.mode = g->mode;
+  bool need_finalize = false;
+  if (splits > 1) {
+    if (g->mode == EPI_F32_ADD || g->mode == EPI_F32_ATOMIC) {
+      ep.mode = EPI_F32_ATOMIC;  // partial sums accumulate straight into the destination
+    } else if (g->mode == EPI_F32) {
+      // zero the rows of the destination then accumulate
+      cudaMemset2DAsync(g->out, (size_t)g->ldo * 4, 0, (size_t)g->N * 4, g->M, stream);
+      ep.mode = EPI_F32_ATOMIC;
+    } else {  // bf16 output: fp32 workspace + finalize
+      if (!g->workspace || g->workspace_bytes < (size_t)g->M * g->N * 4) {
+        splits = 1;
+      } else {
+        cudaMemsetAsync(g->workspace, 0, (size_t)g->M * g->N * 4, stream);
+        ep.out = g->workspace;
+        ep.ldo = g->N;
+        ep.mode = EPI_F32_ATOMIC;
+        need_finalize = true;
+      }
+    }
+  }
+  int rc;
+  if (bn == 256)
+    rc = dispatch_major<256>(ctx, g, splits, stream, ep);
+  else if (bn == 128)
+    rc = dispatch_major<128>(ctx, g, splits, stream, ep);
+  else
+    rc = dispatch_major<64>(ctx, g, splits, stream, ep);
+  if (rc) return rc;
+  if (need_finalize) {
+    gemm_finalize_bf16<<<ctx->num_sms * 4, 256, 0, stream>>>(reinterpret_cast<const float*>(g->workspace), g->M, g->N,
+                                                             reinterpret_cast<__nv_bfloat16*>(g->out), g->ldo);
+    ctx->launches++;
+  }
+  return mace_check_launch(ctx, "gemm");
+}

@@ -1,0 +1,38 @@
+// Internal (non-ABI) declarations shared by the .cu translation units of libmace_b200.so.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/mace_b200.h"
+
+namespace mace {
+
+enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ADD = 2, EPI_F32_ATOMIC = 3 };
+
+struct GemmEpilogue {
+  void* out;
+  int ldo;
+  int mode;
+  const __nv_bfloat16* bias;
+  float alpha;
+};
+
+struct MaceCtx {
+  int device = 0;
+  int num_sms = 148;
+  long long launches = 0;
+  std::string last_error;
+  PFN_cuTensorMapEncodeTiled_v12000 encode_tiled = nullptr;
+};
+
+int mace_fail(MaceCtx* ctx, int code, const std::string& msg);
+int mace_check_launch(MaceCtx* ctx, const char* what);
+
+}  // namespace mace
+
+// opaque ABI handle is the internal struct
+struct mace_ctx : public mace::MaceCtx {};

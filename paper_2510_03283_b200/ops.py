@@ -1,0 +1,73 @@
+"""Thin torch-tensor front end over the C-ABI (device pointers + the current CUDA stream).
+
+torch is plumbing here (device memory, streams); every op below is one or more launches of the
+hand-written sm_100a kernels in csrc/. Shapes are validated on the host before the launch.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import Ctx, MaceGemmArgs
+
+EPI = {"bf16": 0, "f32": 1, "f32_add": 2, "f32_atomic": 3}
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def gemm(
+    ctx: Ctx,
+    a: torch.Tensor,
+    b: torch.Tensor,
+    out: torch.Tensor | None = None,
+    *,
+    mode: str = "bf16",
+    bias: torch.Tensor | None = None,
+    a_mn: bool = False,
+    b_mn: bool = False,
+    alpha: float = 1.0,
+    split_k: int = 0,
+    workspace: torch.Tensor | None = None,
+    stream: torch.cuda.Stream | None = None,
+) -> torch.Tensor:
+    """out[M,N] (op)= alpha * A[M,K] . B[N,K]^T.
+
+    ``a`` is [M,K] (K-major) or, with ``a_mn``, [K,M]; ``b`` is [N,K] or, with ``b_mn``, [K,N].
+    Leading dims may be padded (row stride used as ld) but the inner dim must be contiguous.
+    """
+    assert a.dtype == torch.bfloat16 and b.dtype == torch.bfloat16
+    assert a.stride(1) == 1 and b.stride(1) == 1
+    if a_mn:
+        K, M = a.shape
+    else:
+        M, K = a.shape
+    if b_mn:
+        Kb, N = b.shape
+    else:
+        N, Kb = b.shape
+    assert Kb == K, f"K mismatch {K} vs {Kb}"
+    if out is None:
+        assert mode in ("bf16", "f32")
+        out = torch.empty(M, N, device=a.device, dtype=torch.bfloat16 if mode == "bf16" else torch.float32)
+    assert out.shape[0] >= M and out.shape[1] >= N and out.stride(1) == 1
+    assert out.dtype == (torch.bfloat16 if mode == "bf16" else torch.float32)
+    if bias is not None:
+        assert bias.dtype == torch.bfloat16 and bias.numel() == N
+    g = MaceGemmArgs(
+        a=_ptr(a), lda=a.stride(0), a_mn_major=int(a_mn),
+        b=_ptr(b), ldb=b.stride(0), b_mn_major=int(b_mn),
+        M=M, N=N, K=K,
+        out=_ptr(out), ldo=out.stride(0), mode=EPI[mode],
+        bias=_ptr(bias), alpha=float(alpha), split_k=int(split_k),
+        workspace=_ptr(workspace), workspace_bytes=0 if workspace is None else workspace.numel() * workspace.element_size(),
+    )
+    ctx.check(ctx.L.mace_gemm_bf16(ctx.h, C.byref(g), _stream(stream)), "mace_gemm_bf16")
+    return out

@@ -1,0 +1,74 @@
+"""tcgen05 GEMM vs a plain torch fp32 reference of the same op (bf16 inputs, fp32 accumulate)."""
+import pytest
+import torch
+
+from paper_2510_03283_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    (128, 128, 64),
+    (256, 512, 256),
+    (1, 2048, 2048),      # one decode row
+    (7, 384, 96),         # ragged tails in every dim (K % 64 != 0)
+    (300, 1000, 520),
+    (1024, 2048, 1024),
+    (4096, 4096, 512),    # >148 tiles -> persistent loop + double-buffered TMEM
+]
+
+
+def _ref(a, b, a_mn, b_mn):
+    A = (a.t() if a_mn else a).float()
+    B = (b.t() if b_mn else b).float()
+    return A @ B.t()
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+def test_gemm_layouts(ctx, M, N, K, a_mn, b_mn):
+    torch.manual_seed(M * 7 + N + K)
+    dev = "cuda"
+    a = torch.randn((K, M) if a_mn else (M, K), device=dev).bfloat16()
+    b = torch.randn((K, N) if b_mn else (N, K), device=dev).bfloat16()
+    # MN-major operands need 16-byte aligned rows: pad the leading dim
+    if a_mn and M % 8:
+        a = torch.nn.functional.pad(a, (0, 8 - M % 8))[:, :M]
+    if b_mn and N % 8:
+        b = torch.nn.functional.pad(b, (0, 8 - N % 8))[:, :N]
+    if not a_mn and K % 8:
+        pytest.skip("K-major rows need K % 8 == 0")
+    out = ops.gemm(ctx, a, b, mode="f32", a_mn=a_mn, b_mn=b_mn)
+    ref = _ref(a, b, a_mn, b_mn)
+    torch.cuda.synchronize()
+    err = (out - ref).abs().max().item()
+    tol = 1e-3 * K ** 0.5 + 1e-2
+    assert err <= tol, f"max err {err} > {tol}"
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 256, 128), (500, 768, 768), (2, 50257, 768)])
+def test_gemm_epilogues(ctx, M, N, K):
+    torch.manual_seed(0)
+    a = torch.randn(M, K, device="cuda").bfloat16()
+    b = torch.randn(N, K, device="cuda").bfloat16()
+    bias = torch.randn(N, device="cuda").bfloat16()
+    ref = a.float() @ b.float().t()
+    y = ops.gemm(ctx, a, b, mode="bf16", bias=bias)
+    assert torch.allclose(y.float(), (ref + bias.float()), atol=0.1, rtol=1e-2)
+    acc = torch.randn(M, N, device="cuda")
+    acc0 = acc.clone()
+    ops.gemm(ctx, a, b, acc, mode="f32_add", alpha=0.5)
+    assert torch.allclose(acc, acc0 + 0.5 * ref, atol=2e-2, rtol=1e-3)
+    acc1 = acc0.clone()
+    ops.gemm(ctx, a, b, acc1, mode="f32_atomic", split_k=2)
+    assert torch.allclose(acc1, acc0 + ref, atol=2e-2, rtol=1e-3)
+
+
+def test_gemm_splitk_bf16_workspace(ctx):
+    torch.manual_seed(1)
+    M, N, K = 64, 512, 4096
+    a = torch.randn(M, K, device="cuda").bfloat16()
+    b = torch.randn(N, K, device="cuda").bfloat16()
+    ws = torch.empty(M * N, device="cuda")
+    y = ops.gemm(ctx, a, b, mode="bf16", split_k=8, workspace=ws)
+    ref = a.float() @ b.float().t()
+    assert torch.allclose(y.float(), ref, atol=0.5, rtol=1e-2)
