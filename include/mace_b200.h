@@ -73,6 +73,69 @@ typedef struct MaceGemmArgs {
 } MaceGemmArgs;
 int mace_gemm_bf16(mace_ctx* ctx, const MaceGemmArgs* args, void* stream);
 
+
+/* ---------------------------------------------------------------- tick row tables
+ * One hybrid tick = one ragged batch of rows: [prefill rows | decode rows | fine-tune rows].
+ * Row order inside each group follows Engine._execute (engine.py:578-584): prefills in trie-DFS
+ * order, decodes by id, fine-tunes by id. A "sequence" is a contiguous run of rows:
+ *   kind 0 PREFILL : rows = uncached prompt suffix [n_pv - q_len, n_pv), KV in prompt pages
+ *   kind 1 DECODE  : 1 row, KV = prompt[:n_pv] + per-head decode window [dec_first[h], dec_end)
+ *   kind 2 FT      : rows = [prompt | response], dense causal KV read from the qkv rows          */
+#define MACE_PAGE_TOKENS 16
+typedef struct MaceSeq {
+  int kind, q_start, q_len, slot; /* slot: KV-table slot of the request (paged kinds) */
+  int n_pv;                       /* prompt tokens visible to this sequence            */
+  int kv_len;                     /* FT / prefill: total causal KV length               */
+  int out_row, pad;               /* decode: row in the logits batch                    */
+} MaceSeq;
+
+/* Device-resident KV page tables (persist across ticks).  Pools are head-major pages:
+ *   pool[layer][page][MACE_PAGE_TOKENS][head_dim] bf16, one pool for K and one for V.
+ * Prompt pages are allocated in groups of n_kv_heads (head page = group*Hkv + h) by the host page
+ * manager (trie-owned, refcounted; PrefixTrie semantics cache.py:67-241).  Decode pages are per head,
+ * popped from / pushed to a device free stack (mace_kv_decode_alloc / mace_kv_trim).            */
+typedef struct MaceKvLayout {
+  const int* ptab; int max_prompt_pages;   /* [slots][max_prompt_pages] prompt group ids */
+  int* dtab; int max_dec_pages;            /* [slots][Hkv][max_dec_pages] decode ring    */
+  int* dec_base;                           /* [slots][Hkv] decode slot held by dtab[..][0] row 0 */
+  int* dec_first;                          /* [slots][Hkv] first retained decode slot    */
+  int* dec_end;                            /* [slots] decode slots created               */
+  int* free_stack; int* free_top; int stack_cap; /* device free list of decode head pages */
+  int n_kv_heads; int pad;
+} MaceKvLayout;
+
+/* ---------------------------------------------------------------- row kernels */
+int mace_embed(mace_ctx* ctx, const int* tokens, const int* pos, const void* emb, const void* pos_emb, int T, int d,
+               float* x, void* stream);
+int mace_norm(mace_ctx* ctx, const float* x, int ldx, const int* rows, int n_rows, int d, const void* w,
+              const void* b, int layernorm, float eps, void* out, int ldo, float* rstd_out, void* stream);
+int mace_rope_kv(mace_ctx* ctx, void* qkv, int T, int Hq, int Hkv, int hd, const int* row_pos, const int* row_seq,
+                 const int* row_kvi, const MaceSeq* seqs, const float* cos_t, const float* sin_t, int apply_rope,
+                 const MaceKvLayout* kv, void* k_pool, void* v_pool, void* stream);
+int mace_act(mace_ctx* ctx, const void* u, int T, int F, int swiglu, void* out, void* stream);
+int mace_argmax(mace_ctx* ctx, const float* logits, int n, int V, int ld, int* out, void* stream);
+
+/* ---------------------------------------------------------------- (1) ragged paged attention fwd
+ * Prefill and fine-tune sequences run as tcgen05 tiles (128 query rows x one query head; S = QK^T
+ * and O = PV on the tensor cores, K/V pages TMA-staged, online softmax in registers); decode
+ * sequences run as bandwidth-bound (sequence, kv-head) items streaming K/V pages with
+ * cp.async.bulk.  Work lists are built per tick by the host:
+ *   tc_items  int4 [n_tc]  = (seq, q_head, q_block, 0)
+ *   dec_items int2 [n_dec] = (seq, kv_head)                                                       */
+typedef struct MaceAttnArgs {
+  void* qkv; int T; int Hq; int Hkv; int hd; /* packed [T, (Hq+2Hkv)*hd] bf16 after RoPE */
+  const MaceSeq* seqs;
+  const int* tc_items; int n_tc;
+  const int* dec_items; int n_dec;
+  MaceKvLayout kv;
+  const void* k_pool; const void* v_pool; long long pool_pages; /* this layer */
+  void* out;          /* [T, Hq*hd] bf16 */
+  float* lse;         /* [T, Hq] natural-log LSE (tc rows) or NULL */
+  float* head_norm;   /* [T, Hq] ||o_{t,h}||_2 of decode rows or NULL */
+  float scale;        /* softmax scale, 0 -> 1/sqrt(hd) */
+} MaceAttnArgs;
+int mace_attn_fwd(mace_ctx* ctx, const MaceAttnArgs* args, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,294 @@
+"""CPU ORACLE (test infrastructure only) for the model arithmetic of MACE's hybrid iteration.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may import this module. It is
+the checker, never the thing measured or shipped; the product path (paper_2510_03283_b200) never
+imports it.
+
+PARITY STATUS: the reference (macesim) is a simulator with no logits, tokens, gradients or weights
+(SURVEY.md §0.3, §8(c)), so the model arithmetic here is *parity unpinned* against the reference
+itself. It is a plain fp32 PyTorch restatement of standard definitions, pinned where the reference
+has arithmetic:
+  * DPO scalar stage  = macesim.alignment.dpo_loss (alignment.py:39-47), pinned by golden vectors
+    generated from the reference (tests/golden/dpo_golden.json, tests/golden/make_golden.py).
+  * tick / row order  = Engine._execute (engine.py:573-676): prefills in trie-DFS order, decodes
+    and fine-tunes by id (engine.py:578-584).
+  * KV semantics      = cache.py:67-273 + engine.py:496-529: prompt KV is never pruned; decode slots
+    are trimmed oldest-first per KV head to the reference's kept[h] counts.
+  * pi_ref frozen at init; AdamW = torch.optim.AdamW's update order.
+Builder-defined (no reference exists, documented in DESIGN.md): the decoder shapes, synthetic
+chosen/rejected token content, the selected-parameter rule (top-k layers + final norm), AdamW
+hyper-parameters, and the decode token convention (prefill writes the prompt KV and emits no token,
+engine.py:474 / test_engine.py:33-36; decode step k consumes x_k at position P-2+k with
+x_1 = prompt[-1], x_k = y_{k-1}).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+import torch.nn.functional as F
+
+
+# ----------------------------------------------------------------------------- scalar DPO stage
+def dpo_loss_scalar(margin: float, beta: float) -> float:
+    """-log sigmoid(beta*m), the reference's stable form (alignment.py:39-47)."""
+    if beta <= 0:
+        raise ValueError("beta must be > 0")
+    x = -beta * margin
+    if x > 0:
+        return x + math.log1p(math.exp(-x))
+    return math.log1p(math.exp(x))
+
+
+# ----------------------------------------------------------------------------- building blocks
+def rms_norm(x, w, eps):
+    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * w
+
+
+def layer_norm(x, w, b, eps):
+    mu = x.mean(-1, keepdim=True)
+    var = (x - mu).pow(2).mean(-1, keepdim=True)
+    return (x - mu) * torch.rsqrt(var + eps) * w + b
+
+
+def gelu_tanh(x):
+    return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x * x * x)))
+
+
+def rope(x, pos, theta):
+    """x [n, H, hd]; rotate-half convention (Llama); pos int64 [n]."""
+    hd = x.shape[-1]
+    inv = theta ** (-torch.arange(0, hd // 2, dtype=torch.float64) * 2.0 / hd)
+    ang = pos.to(torch.float64)[:, None] * inv[None, :]
+    cos = torch.cos(ang).to(x.dtype)[:, None, :]
+    sin = torch.sin(ang).to(x.dtype)[:, None, :]
+    x1, x2 = x[..., : hd // 2], x[..., hd // 2:]
+    return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
+
+
+@dataclass
+class _Seq:
+    prompt: list[int]
+    k_prompt: list = field(default_factory=list)   # per layer [P, Hkv, hd]
+    v_prompt: list = field(default_factory=list)
+    k_dec: list = field(default_factory=list)      # per layer list of [Hkv, hd]
+    v_dec: list = field(default_factory=list)
+
+
+class OracleModel:
+    """fp32 CPU decoder: Llama (RMSNorm/RoPE/GQA/SwiGLU) or GPT-2 (LayerNorm/learned pos/GELU/bias)."""
+
+    def __init__(self, cfg, weights: dict[str, torch.Tensor]):
+        self.cfg = cfg
+        self.w = {k: v.detach().float().clone() for k, v in weights.items()}
+
+    # -- one decoder layer over rows x [n, d]; kv_ctx(l, k_new, v_new) -> (K [m,Hkv,hd], V, mask [n,Hkv?,m])
+    def _norm(self, x, name, params):
+        c = self.cfg
+        if c.family == "llama":
+            return rms_norm(x, params[name + ".w"], c.norm_eps)
+        return layer_norm(x, params[name + ".w"], params[name + ".b"], c.norm_eps)
+
+    def _lin(self, x, name, params):
+        y = x @ params[name + ".w"].t()
+        if self.cfg.has_bias:
+            y = y + params[name + ".b"]
+        return y
+
+    def embed(self, tokens, pos, params=None):
+        params = params or self.w
+        x = params["embed"][torch.as_tensor(tokens, dtype=torch.long)]
+        if self.cfg.family == "gpt2":
+            x = x + params["pos_embed"][torch.as_tensor(pos, dtype=torch.long)]
+        return x
+
+    def layer(self, l, x, pos, attend, params=None):
+        """attend(l, q[n,Hq,hd], k[n,Hkv,hd], v) -> o [n, Hq, hd]"""
+        c = self.cfg
+        params = params or self.w
+        p = f"layers.{l}."
+        h = self._norm(x, p + "attn_norm", params)
+        qkv = self._lin(h, p + "qkv", params)
+        Hq, Hk, hd = c.n_heads, c.n_kv_heads, c.head_dim
+        q = qkv[:, : Hq * hd].reshape(-1, Hq, hd)
+        k = qkv[:, Hq * hd: (Hq + Hk) * hd].reshape(-1, Hk, hd)
+        v = qkv[:, (Hq + Hk) * hd:].reshape(-1, Hk, hd)
+        if c.family == "llama":
+            pos_t = torch.as_tensor(pos, dtype=torch.long)
+            q = rope(q, pos_t, c.rope_theta)
+            k = rope(k, pos_t, c.rope_theta)
+        o = attend(l, q, k, v)
+        x = x + self._lin(o.reshape(-1, Hq * hd), p + "o", params)
+        h = self._norm(x, p + "mlp_norm", params)
+        u = self._lin(h, p + "up", params)
+        if c.family == "llama":
+            a = F.silu(u[:, : c.ffn]) * u[:, c.ffn:]
+        else:
+            a = gelu_tanh(u)
+        return x + self._lin(a, p + "down", params)
+
+    def final(self, x, params=None):
+        params = params or self.w
+        return self._norm(x, "final_norm", params) @ params["embed"].t()
+
+    def attention(self, q, K, V, mask):
+        """q [n,Hq,hd], K/V [m,Hkv,hd] or per-head lists, mask bool [n, Hkv, m] (True = attend)."""
+        c = self.cfg
+        g = c.group
+        Kx = K.repeat_interleave(g, dim=1)  # [m, Hq, hd]
+        Vx = V.repeat_interleave(g, dim=1)
+        s = torch.einsum("nhd,mhd->nhm", q, Kx) / math.sqrt(c.head_dim)
+        mk = mask.repeat_interleave(g, dim=1)
+        s = s.masked_fill(~mk, float("-inf"))
+        p = torch.softmax(s, dim=-1)
+        return torch.einsum("nhm,mhd->nhd", p, Vx)
+
+    # -- full causal sequence (prefill, fine-tune); returns hidden [n, d] and per-layer (k, v)
+    def forward_seq(self, tokens, pos0=0, params=None, collect_kv=False):
+        n = len(tokens)
+        pos = list(range(pos0, pos0 + n))
+        x = self.embed(tokens, pos, params)
+        causal = torch.tril(torch.ones(n, n, dtype=torch.bool))
+        kvs = []
+
+        def attend(l, q, k, v):
+            if collect_kv:
+                kvs.append((k.detach().clone(), v.detach().clone()))
+            mask = causal[:, None, :].expand(n, self.cfg.n_kv_heads, n)
+            return self.attention(q, k, v, mask)
+
+        for l in range(self.cfg.n_layers):
+            x = self.layer(l, x, pos, attend, params)
+        return x, kvs
+
+    def seq_logprob(self, prompt, response, params=None):
+        """Sum of log p(response | prompt) under ``params``; response token i predicted at P+i-1."""
+        toks = list(prompt) + list(response)
+        h, _ = self.forward_seq(toks, params=params)
+        P = len(prompt)
+        logits = self.final(h[P - 1: P - 1 + len(response)], params)
+        lp = torch.log_softmax(logits, dim=-1)
+        tgt = torch.as_tensor(response, dtype=torch.long)
+        return lp.gather(1, tgt[:, None]).sum()
+
+
+class OracleExecutor:
+    """Request-level restatement of the GPU hybrid step (prefill / decode / DPO fine-tune)."""
+
+    def __init__(self, cfg, weights, tcfg, selected_names):
+        self.cfg = cfg
+        self.tcfg = tcfg
+        self.model = OracleModel(cfg, weights)
+        self.selected = list(selected_names)
+        self.ref_params = {n: self.model.w[n].clone() for n in self.selected}  # pi_ref frozen at init
+        self.master = {n: self.model.w[n].clone() for n in self.selected}
+        self.m = {n: torch.zeros_like(self.master[n]) for n in self.selected}
+        self.v = {n: torch.zeros_like(self.master[n]) for n in self.selected}
+        self.step = 0
+        self.seqs: dict[int, _Seq] = {}
+        self.ref_lp_cache: dict[int, tuple[float, float]] = {}
+
+    # ---------------------------------------------------------------- inference rows
+    def prefill(self, rid: int, prompt: list[int]) -> None:
+        """Engine._exec_prefill (engine.py:444-480): prompt KV for all P tokens, no token emitted."""
+        _, kvs = self.model.forward_seq(prompt, collect_kv=True)
+        s = _Seq(prompt=list(prompt))
+        s.k_prompt = [k for k, _ in kvs]
+        s.v_prompt = [v for _, v in kvs]
+        s.k_dec = [[] for _ in range(self.cfg.n_layers)]
+        s.v_dec = [[] for _ in range(self.cfg.n_layers)]
+        self.seqs[rid] = s
+
+    def decode(self, rid: int, x_token: int, kept_pre: list[int] | None) -> torch.Tensor:
+        """Engine._exec_decode (engine.py:482-532) step k: returns logits [V] for y_k.
+
+        Window for KV head h = prompt[:P-1] (never pruned) + the last kept_pre[h] decode slots + the
+        new slot k. ``kept_pre`` None means no pruning (all decode slots).
+        """
+        s = self.seqs[rid]
+        c = self.cfg
+        P = len(s.prompt)
+        k_idx = len(s.k_dec[0]) + 1          # this is decode slot k (1-based)
+        pos = P - 2 + k_idx
+        x = self.model.embed([x_token], [pos])
+
+        def attend(l, q, k, v):
+            s.k_dec[l].append(k[0].clone())
+            s.v_dec[l].append(v[0].clone())
+            Kp = s.k_prompt[l][: P - 1]
+            Vp = s.v_prompt[l][: P - 1]
+            Kd = torch.stack(s.k_dec[l])   # [k, Hkv, hd]
+            Vd = torch.stack(s.v_dec[l])
+            K = torch.cat([Kp, Kd])
+            V = torch.cat([Vp, Vd])
+            m = K.shape[0]
+            mask = torch.zeros(1, c.n_kv_heads, m, dtype=torch.bool)
+            mask[:, :, : P - 1] = True
+            for h in range(c.n_kv_heads):
+                keep = (k_idx - 1) if kept_pre is None else min(kept_pre[h], k_idx - 1)
+                lo = (P - 1) + (k_idx - 1 - keep)
+                mask[0, h, lo:] = True
+            return self.model.attention(q, K, V, mask)
+
+        for l in range(c.n_layers):
+            x = self.model.layer(l, x, [pos], attend)
+        return self.model.final(x)[0]
+
+    def release(self, rid: int) -> None:
+        self.seqs.pop(rid, None)
+
+    # ---------------------------------------------------------------- fine-tune rows
+    def dpo_step(self, pairs: list[tuple[int, list[int], list[int], list[int]]]):
+        """One optimizer step on mean_i softplus(-beta * m_i) over the tick's FT pairs.
+
+        pairs: (rid, prompt, chosen, rejected). m_i = (lp_c - ref_c) - (lp_r - ref_r) with ref log-probs
+        under the frozen pi_ref, computed once per pair (alignment.py:39-47 for the scalar stage).
+        Returns per-pair (loss, margin) and the gradients of the selected parameters.
+        """
+        beta = self.tcfg.dpo_beta
+        params = dict(self.model.w)
+        for n in self.selected:
+            params[n] = self.model.w[n].clone().requires_grad_(True)
+        ref = dict(self.model.w)
+        ref.update(self.ref_params)
+        losses, margins, total = [], [], 0.0
+        for rid, prompt, chosen, rejected in pairs:
+            if rid not in self.ref_lp_cache:
+                with torch.no_grad():
+                    self.ref_lp_cache[rid] = (
+                        float(self.model.seq_logprob(prompt, chosen, ref)),
+                        float(self.model.seq_logprob(prompt, rejected, ref)),
+                    )
+            rc, rr = self.ref_lp_cache[rid]
+            lc = self.model.seq_logprob(prompt, chosen, params)
+            lr_ = self.model.seq_logprob(prompt, rejected, params)
+            m = (lc - rc) - (lr_ - rr)
+            loss = F.softplus(-beta * m)
+            total = total + loss / len(pairs)
+            losses.append(float(loss))
+            margins.append(float(m))
+        total.backward()
+        grads = {n: params[n].grad.detach().clone() for n in self.selected}
+        return losses, margins, grads
+
+    def adamw(self, grads: dict[str, torch.Tensor]) -> None:
+        """torch.optim.AdamW update order on fp32 masters; working weights = bf16(master)."""
+        t = self.tcfg
+        self.step += 1
+        bc1 = 1.0 - t.beta1 ** self.step
+        bc2 = 1.0 - t.beta2 ** self.step
+        for n in self.selected:
+            adamw_reference(self.master[n], self.m[n], self.v[n], grads[n], t.lr, t.beta1, t.beta2, t.eps,
+                            t.weight_decay, bc1, bc2)
+            self.model.w[n] = self.master[n].to(torch.bfloat16).float()
+
+
+def adamw_reference(p, m, v, g, lr, b1, b2, eps, wd, bc1, bc2):
+    """In-place fp32 AdamW restatement (torch.optim.AdamW single-tensor order)."""
+    p.mul_(1.0 - lr * wd)
+    m.lerp_(g, 1.0 - b1)
+    v.mul_(b2).addcmul_(g, g, value=1.0 - b2)
+    step_size = lr / bc1
+    denom = (v.sqrt() / math.sqrt(bc2)).add_(eps)
+    p.addcdiv_(m, denom, value=-step_size)

@@ -28,6 +28,34 @@ class MaceGemmArgs(C.Structure):
     ]
 
 
+class MaceKvLayout(C.Structure):
+    _fields_ = [
+        ("ptab", C.c_void_p), ("max_prompt_pages", C.c_int),
+        ("dtab", C.c_void_p), ("max_dec_pages", C.c_int),
+        ("dec_base", C.c_void_p), ("dec_first", C.c_void_p), ("dec_end", C.c_void_p),
+        ("free_stack", C.c_void_p), ("free_top", C.c_void_p), ("stack_cap", C.c_int),
+        ("n_kv_heads", C.c_int), ("pad", C.c_int),
+    ]
+
+
+class MaceAttnArgs(C.Structure):
+    _fields_ = [
+        ("qkv", C.c_void_p), ("T", C.c_int), ("Hq", C.c_int), ("Hkv", C.c_int), ("hd", C.c_int),
+        ("seqs", C.c_void_p),
+        ("tc_items", C.c_void_p), ("n_tc", C.c_int),
+        ("dec_items", C.c_void_p), ("n_dec", C.c_int),
+        ("kv", MaceKvLayout),
+        ("k_pool", C.c_void_p), ("v_pool", C.c_void_p), ("pool_pages", C.c_longlong),
+        ("out", C.c_void_p), ("lse", C.c_void_p), ("head_norm", C.c_void_p),
+        ("scale", C.c_float),
+    ]
+
+
+# MaceSeq is 8 x int32 (see include/mace_b200.h); built as numpy/torch int32 [S, 8] arrays
+SEQ_FIELDS = ("kind", "q_start", "q_len", "slot", "n_pv", "kv_len", "out_row", "pad")
+
+_vp, _i, _f, _ip = C.c_void_p, C.c_int, C.c_float, C.c_void_p
+
 # (name, argtypes) for every symbol include/mace_b200.h declares; checked by tests/test_abi.py
 SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_version": (C.c_int, []),
@@ -36,6 +64,13 @@ SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_last_error": (C.c_char_p, [C.c_void_p]),
     "mace_launch_count": (C.c_longlong, [C.c_void_p]),
     "mace_gemm_bf16": (C.c_int, [C.c_void_p, C.POINTER(MaceGemmArgs), C.c_void_p]),
+    "mace_embed": (C.c_int, [_vp, _ip, _ip, _vp, _vp, _i, _i, _vp, _vp]),
+    "mace_norm": (C.c_int, [_vp, _vp, _i, _ip, _i, _i, _vp, _vp, _i, _f, _vp, _i, _vp, _vp]),
+    "mace_rope_kv": (C.c_int, [_vp, _vp, _i, _i, _i, _i, _ip, _ip, _ip, _vp, _vp, _vp, _i,
+                               C.POINTER(MaceKvLayout), _vp, _vp, _vp]),
+    "mace_act": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp]),
+    "mace_argmax": (C.c_int, [_vp, _vp, _i, _i, _i, _ip, _vp]),
+    "mace_attn_fwd": (C.c_int, [_vp, C.POINTER(MaceAttnArgs), _vp]),
 }
 
 _lib = None

@@ -1,0 +1,110 @@
+"""Decoder shapes for the BASELINE.json configs (SURVEY.md §8(d) "Model shapes").
+
+The reference (macesim) has no model at all: its cost model (cost_model.py:25-73) stands in for one.
+These presets are the real architectures the hybrid iteration executes; weights are seeded random
+init (no checkpoints offline), bf16 on device.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    name: str
+    family: str            # "llama" (RMSNorm, RoPE, GQA, SwiGLU) or "gpt2" (LayerNorm, learned pos, GELU, biases)
+    n_layers: int
+    d_model: int
+    n_heads: int           # query heads
+    n_kv_heads: int        # = CacheConfig.num_heads (per-head KV windows, engine.py:44)
+    head_dim: int
+    ffn: int
+    vocab: int
+    max_pos: int = 8192
+    rope_theta: float = 10000.0
+    norm_eps: float = 1e-5
+    tied: bool = True
+    init_std: float = 0.02
+    embed_std: float = 0.1     # larger than GPT-2's 0.02 so random-init greedy decode has clear top-1 gaps
+
+    @property
+    def qkv_dim(self) -> int:
+        return (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
+
+    @property
+    def group(self) -> int:
+        return self.n_heads // self.n_kv_heads
+
+    @property
+    def has_bias(self) -> bool:
+        return self.family == "gpt2"
+
+    @property
+    def up_dim(self) -> int:
+        return 2 * self.ffn if self.family == "llama" else self.ffn
+
+    def kv_bytes_per_token(self) -> int:
+        return 2 * self.n_layers * self.n_kv_heads * self.head_dim * 2
+
+    def body_params(self) -> int:
+        d = self.d_model
+        per = self.qkv_dim * d + self.n_heads * self.head_dim * d + self.up_dim * d + self.ffn * d
+        return self.n_layers * per
+
+    def param_shapes(self) -> dict[str, tuple[int, ...]]:
+        d = self.d_model
+        s: dict[str, tuple[int, ...]] = {"embed": (self.vocab, d)}
+        if self.family == "gpt2":
+            s["pos_embed"] = (self.max_pos, d)
+        for i in range(self.n_layers):
+            p = f"layers.{i}."
+            s[p + "attn_norm.w"] = (d,)
+            s[p + "qkv.w"] = (self.qkv_dim, d)
+            s[p + "o.w"] = (d, self.n_heads * self.head_dim)
+            s[p + "mlp_norm.w"] = (d,)
+            s[p + "up.w"] = (self.up_dim, d)
+            s[p + "down.w"] = (d, self.ffn)
+            if self.family == "gpt2":
+                for n, dim in (("attn_norm.b", d), ("qkv.b", self.qkv_dim), ("o.b", d), ("mlp_norm.b", d),
+                               ("up.b", self.ffn), ("down.b", d)):
+                    s[p + n] = (dim,)
+        s["final_norm.w"] = (d,)
+        if self.family == "gpt2":
+            s["final_norm.b"] = (d,)
+        return s
+
+
+PRESETS: dict[str, ModelConfig] = {
+    # C1: tiny default decoder: L4 d256 Hq=Hkv=8 hd32 ffn1024, vocab 50000 = workload.py:129
+    "tiny": ModelConfig("tiny", "llama", 4, 256, 8, 8, 32, 1024, 50000, max_pos=4096),
+    # C2: GPT-2 small, 1024 positions
+    "gpt2": ModelConfig("gpt2", "gpt2", 12, 768, 12, 12, 64, 3072, 50257, max_pos=1024),
+    # C3: Llama-3.2-1B
+    "llama1b": ModelConfig("llama1b", "llama", 16, 2048, 32, 8, 64, 8192, 128256, max_pos=8192, rope_theta=500000.0),
+    # C4/C5: Llama-3-8B (untied lm_head in the real model; tied here to keep one vocab matrix)
+    "llama8b": ModelConfig("llama8b", "llama", 32, 4096, 32, 8, 128, 14336, 128256, max_pos=8192, rope_theta=500000.0),
+}
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """Builder-defined fine-tune settings (the reference has only ft_gain, alignment.py:69)."""
+
+    n_selected_layers: int = 2        # top-k layers (+ final norm) receive the masked AdamW update
+    lr: float = 1e-5
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+    dpo_beta: float = 1.0             # = AlignmentEnv.beta default (alignment.py:99)
+
+    def selected_layers(self, cfg: ModelConfig) -> list[int]:
+        return list(range(cfg.n_layers - self.n_selected_layers, cfg.n_layers))
+
+
+def selected_param_names(cfg: ModelConfig, tcfg: TrainConfig) -> list[str]:
+    names = []
+    for i in tcfg.selected_layers(cfg):
+        names += [n for n in cfg.param_shapes() if n.startswith(f"layers.{i}.")]
+    names += [n for n in cfg.param_shapes() if n.startswith("final_norm.")]
+    return names

@@ -1,0 +1,289 @@
+// Row-wise fused kernels of the hybrid step (HBM-bound; one warp per row, 16-byte vector access).
+//   embed          tokens -> fp32 residual stream (+ learned positions for GPT-2)
+//   norm           fp32 residual -> bf16 RMSNorm/LayerNorm output, optional row gather
+//   rope_kv        RoPE on q/k (Llama) in the packed qkv rows + scatter of k/v rows into the
+//                  head-major paged KV pools (prefill rows -> prompt pages, decode rows -> the
+//                  per-head decode ring), replacing the MB bookkeeping of engine.py:469-471,512-514
+//   act            SwiGLU / GELU(tanh)
+//   argmax         greedy token per decode row (ties -> lowest id, = torch.argmax)
+#include "common.cuh"
+#include "mace_internal.h"
+
+namespace mace {
+
+// ------------------------------------------------------------------ embed
+__global__ void embed_kernel(const int* __restrict__ tokens, const int* __restrict__ pos,
+                             const __nv_bfloat16* __restrict__ emb, const __nv_bfloat16* __restrict__ pos_emb, int T,
+                             int d, float* __restrict__ x) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (row >= T) return;
+  const int lane = threadIdx.x & 31;
+  const __nv_bfloat16* e = emb + (size_t)tokens[row] * d;
+  const __nv_bfloat16* pe = pos_emb ? pos_emb + (size_t)pos[row] * d : nullptr;
+  float* xr = x + (size_t)row * d;
+  for (int c = lane * 8; c < d; c += 256) {
+    uint4 u = *reinterpret_cast<const uint4*>(e + c);
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(h[j]);
+    if (pe) {
+      uint4 up = *reinterpret_cast<const uint4*>(pe + c);
+      const __nv_bfloat16* hp = reinterpret_cast<const __nv_bfloat16*>(&up);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += __bfloat162float(hp[j]);
+    }
+    *reinterpret_cast<float4*>(xr + c) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(xr + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+// ------------------------------------------------------------------ norm (fp32 in -> bf16 out)
+// out[i] = norm(x[rows ? rows[i] : i]); LayerNorm when bias != nullptr semantics chosen by `layernorm`.
+template <int kPerLane>
+__global__ void norm_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ rows, int n_rows, int d,
+                            const __nv_bfloat16* __restrict__ w, const __nv_bfloat16* __restrict__ b, int layernorm,
+                            float eps, __nv_bfloat16* __restrict__ out, int ldo, float* __restrict__ rstd_out) {
+  const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (i >= n_rows) return;
+  const int lane = threadIdx.x & 31;
+  const int src = rows ? rows[i] : i;
+  const float* xr = x + (size_t)src * ldx;
+  float v[kPerLane];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < kPerLane / 4; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    float4 f = c < d ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    v[4 * k] = f.x; v[4 * k + 1] = f.y; v[4 * k + 2] = f.z; v[4 * k + 3] = f.w;
+    s += f.x + f.y + f.z + f.w;
+  }
+  float mean = 0.f;
+  if (layernorm) {
+    mean = warp_sum(s) / d;
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kPerLane / 4; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    if (c < d) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float t = v[4 * k + j] - mean;
+        ss += t * t;
+      }
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(ss) / d + eps);
+  if (rstd_out && lane == 0) rstd_out[i] = rstd;
+  __nv_bfloat16* o = out + (size_t)i * ldo;
+#pragma unroll
+  for (int k = 0; k < kPerLane / 4; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    if (c < d) {
+      float y[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        y[j] = (v[4 * k + j] - mean) * rstd * __bfloat162float(w[c + j]);
+        if (layernorm) y[j] += __bfloat162float(b[c + j]);
+      }
+      uint2 pk = make_uint2(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]));
+      *reinterpret_cast<uint2*>(o + c) = pk;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ RoPE + paged KV write
+// qkv row layout: [q heads | k heads | v heads] x hd (bf16). cos/sin tables [max_pos, hd/2] fp32.
+// Row kinds come from the tick's sequence table (MaceSeq). Paged destinations:
+//   prefill row (kind 0), prompt index t: head page = ptab[slot][t/16] * Hkv + h, row t % 16
+//   decode row  (kind 1), decode slot j:  head page = dtab[slot][h][(j - dec_base)/16],  row j % 16
+//   fine-tune row (kind 2): attention reads K/V straight from the qkv rows (no write)
+__global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int T, int Hq, int Hkv, int hd,
+                               const int* __restrict__ row_pos, const int* __restrict__ row_seq,
+                               const int* __restrict__ row_kvi, const MaceSeq* __restrict__ seqs,
+                               const float* __restrict__ cos_t, const float* __restrict__ sin_t, int apply_rope,
+                               const MaceKvLayout kv, __nv_bfloat16* __restrict__ k_pool,
+                               __nv_bfloat16* __restrict__ v_pool) {
+  const int row = blockIdx.x;
+  if (row >= T) return;
+  const int W = (Hq + 2 * Hkv) * hd;
+  __nv_bfloat16* r = qkv + (size_t)row * W;
+  const int pos = row_pos[row];
+  const int half = hd / 2;
+  if (apply_rope) {
+    // rotate-half on every (q and k) head; one thread per (head, i < hd/2)
+    const int nh = Hq + Hkv;
+    for (int idx = threadIdx.x; idx < nh * half; idx += blockDim.x) {
+      const int h = idx / half, i = idx % half;
+      __nv_bfloat16* base = r + h * hd;
+      const float c = cos_t[(size_t)pos * half + i], s = sin_t[(size_t)pos * half + i];
+      const float x1 = __bfloat162float(base[i]), x2 = __bfloat162float(base[i + half]);
+      base[i] = __float2bfloat16(x1 * c - x2 * s);
+      base[i + half] = __float2bfloat16(x2 * c + x1 * s);
+    }
+    __syncthreads();
+  }
+  const MaceSeq sq = seqs[row_seq[row]];
+  if (sq.kind == 2 || k_pool == nullptr) return;
+  const int t = row_kvi[row];
+  for (int idx = threadIdx.x; idx < Hkv * (hd / 8); idx += blockDim.x) {
+    const int h = idx / (hd / 8), c = (idx % (hd / 8)) * 8;
+    int page;
+    if (sq.kind == 0) {
+      page = kv.ptab[(size_t)sq.slot * kv.max_prompt_pages + t / kPageTokens] * Hkv + h;
+    } else {
+      const int base = kv.dec_base[sq.slot * Hkv + h];
+      page = kv.dtab[((size_t)sq.slot * Hkv + h) * kv.max_dec_pages + (t - base) / kPageTokens];
+    }
+    const size_t off = ((size_t)page * kPageTokens + (t % kPageTokens)) * hd + c;
+    *reinterpret_cast<uint4*>(k_pool + off) = *reinterpret_cast<const uint4*>(r + (Hq + h) * hd + c);
+    *reinterpret_cast<uint4*>(v_pool + off) = *reinterpret_cast<const uint4*>(r + (Hq + Hkv + h) * hd + c);
+  }
+}
+
+// ------------------------------------------------------------------ activations
+// llama: up row = [gate(F) | up(F)] -> silu(gate) * up ; gpt2: gelu_tanh(up)
+__global__ void act_kernel(const __nv_bfloat16* __restrict__ u, int T, int F, int swiglu,
+                           __nv_bfloat16* __restrict__ out) {
+  const size_t total = (size_t)T * F / 8;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = (i * 8) / F, c = (i * 8) % F;
+    const int W = swiglu ? 2 * F : F;
+    uint4 a = *reinterpret_cast<const uint4*>(u + row * W + c);
+    const __nv_bfloat16* ah = reinterpret_cast<const __nv_bfloat16*>(&a);
+    float y[8];
+    if (swiglu) {
+      uint4 b = *reinterpret_cast<const uint4*>(u + row * W + F + c);
+      const __nv_bfloat16* bh = reinterpret_cast<const __nv_bfloat16*>(&b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float g = __bfloat162float(ah[j]);
+        y[j] = g / (1.f + __expf(-g)) * __bfloat162float(bh[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float x = __bfloat162float(ah[j]);
+        y[j] = 0.5f * x * (1.f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+      }
+    }
+    *reinterpret_cast<uint4*>(out + row * F + c) =
+        make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+  }
+}
+
+// ------------------------------------------------------------------ argmax over fp32 logits rows
+__global__ void argmax_kernel(const float* __restrict__ logits, int V, int ld, int* __restrict__ out) {
+  const float* r = logits + (size_t)blockIdx.x * ld;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    const float v = r[c];
+    if (v > best) {
+      best = v;
+      idx = c;
+    }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ob > best || (ob == best && oi < idx)) {
+      best = ob;
+      idx = oi;
+    }
+  }
+  const int w = threadIdx.x / 32;
+  if ((threadIdx.x & 31) == 0) {
+    sb[w] = best;
+    si[w] = idx;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x / 32;
+    best = (threadIdx.x < nw) ? sb[threadIdx.x] : -INFINITY;
+    idx = (threadIdx.x < nw) ? si[threadIdx.x] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ob > best || (ob == best && oi < idx)) {
+        best = ob;
+        idx = oi;
+      }
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = idx;
+  }
+}
+
+}  // namespace mace
+
+using namespace mace;
+
+extern "C" int mace_embed(mace_ctx* ctx, const int* tokens, const int* pos, const void* emb, const void* pos_emb, int T,
+                          int d, float* x, void* stream) {
+  if (T <= 0) return 0;
+  if (d % 256) return mace_fail(ctx, MACE_ERR_ARG, "embed: d must be a multiple of 256");
+  embed_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>(tokens, pos, (const __nv_bfloat16*)emb,
+                                                                 (const __nv_bfloat16*)pos_emb, T, d, x);
+  ctx->launches++;
+  return mace_check_launch(ctx, "embed");
+}
+
+extern "C" int mace_norm(mace_ctx* ctx, const float* x, int ldx, const int* rows, int n_rows, int d, const void* w,
+                         const void* b, int layernorm, float eps, void* out, int ldo, float* rstd_out, void* stream) {
+  if (n_rows <= 0) return 0;
+  if (d % 128) return mace_fail(ctx, MACE_ERR_ARG, "norm: d must be a multiple of 128");
+  const int per_lane = (d + 31) / 32;
+  dim3 grid((n_rows + 7) / 8);
+  auto* W = (const __nv_bfloat16*)w;
+  auto* B = (const __nv_bfloat16*)b;
+  auto* O = (__nv_bfloat16*)out;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (per_lane <= 8)
+    norm_kernel<8><<<grid, 256, 0, s>>>(x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
+  else if (per_lane <= 24)
+    norm_kernel<24><<<grid, 256, 0, s>>>(x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
+  else if (per_lane <= 64)
+    norm_kernel<64><<<grid, 256, 0, s>>>(x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
+  else if (per_lane <= 128)
+    norm_kernel<128><<<grid, 256, 0, s>>>(x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
+  else
+    return mace_fail(ctx, MACE_ERR_ARG, "norm: d too large");
+  ctx->launches++;
+  return mace_check_launch(ctx, "norm");
+}
+
+extern "C" int mace_rope_kv(mace_ctx* ctx, void* qkv, int T, int Hq, int Hkv, int hd, const int* row_pos,
+                            const int* row_seq, const int* row_kvi, const MaceSeq* seqs, const float* cos_t,
+                            const float* sin_t, int apply_rope, const MaceKvLayout* kv, void* k_pool, void* v_pool,
+                            void* stream) {
+  if (T <= 0) return 0;
+  if (hd % 8) return mace_fail(ctx, MACE_ERR_ARG, "rope_kv: hd % 8");
+  rope_kv_kernel<<<T, 128, 0, (cudaStream_t)stream>>>((__nv_bfloat16*)qkv, T, Hq, Hkv, hd, row_pos, row_seq, row_kvi,
+                                                      seqs, cos_t, sin_t, apply_rope, *kv, (__nv_bfloat16*)k_pool,
+                                                      (__nv_bfloat16*)v_pool);
+  ctx->launches++;
+  return mace_check_launch(ctx, "rope_kv");
+}
+
+extern "C" int mace_act(mace_ctx* ctx, const void* u, int T, int F, int swiglu, void* out, void* stream) {
+  if (T <= 0) return 0;
+  if (F % 8) return mace_fail(ctx, MACE_ERR_ARG, "act: F % 8");
+  const size_t work = (size_t)T * F / 8;
+  int grid = (int)((work + 255) / 256);
+  if (grid > ctx->num_sms * 16) grid = ctx->num_sms * 16;
+  act_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)u, T, F, swiglu, (__nv_bfloat16*)out);
+  ctx->launches++;
+  return mace_check_launch(ctx, "act");
+}
+
+extern "C" int mace_argmax(mace_ctx* ctx, const float* logits, int n, int V, int ld, int* out, void* stream) {
+  if (n <= 0) return 0;
+  argmax_kernel<<<n, 1024, 0, (cudaStream_t)stream>>>(logits, V, ld, out);
+  ctx->launches++;
+  return mace_check_launch(ctx, "argmax");
+}

@@ -71,3 +71,38 @@ def gemm(
     )
     ctx.check(ctx.L.mace_gemm_bf16(ctx.h, C.byref(g), _stream(stream)), "mace_gemm_bf16")
     return out
+
+
+def attn_fwd(
+    ctx: Ctx,
+    qkv: torch.Tensor,
+    Hq: int,
+    Hkv: int,
+    hd: int,
+    seqs: torch.Tensor,
+    tc_items: torch.Tensor | None,
+    dec_items: torch.Tensor | None,
+    kv_layout,
+    k_pool: torch.Tensor | None,
+    v_pool: torch.Tensor | None,
+    out: torch.Tensor,
+    lse: torch.Tensor | None = None,
+    head_norm: torch.Tensor | None = None,
+    stream: torch.cuda.Stream | None = None,
+) -> torch.Tensor:
+    """Ragged paged attention of one tick (prefill + FT tiles on tcgen05, decode rows streamed)."""
+    from ._lib import MaceAttnArgs
+
+    T = qkv.shape[0]
+    assert qkv.dtype == torch.bfloat16 and qkv.shape[1] == (Hq + 2 * Hkv) * hd and qkv.is_contiguous()
+    assert seqs.dtype == torch.int32 and seqs.shape[1] == 8
+    a = MaceAttnArgs(
+        qkv=qkv.data_ptr(), T=T, Hq=Hq, Hkv=Hkv, hd=hd, seqs=seqs.data_ptr(),
+        tc_items=_ptr(tc_items), n_tc=0 if tc_items is None else tc_items.shape[0],
+        dec_items=_ptr(dec_items), n_dec=0 if dec_items is None else dec_items.shape[0],
+        kv=kv_layout,
+        k_pool=_ptr(k_pool), v_pool=_ptr(v_pool), pool_pages=0 if k_pool is None else k_pool.shape[0],
+        out=out.data_ptr(), lse=_ptr(lse), head_norm=_ptr(head_norm), scale=0.0,
+    )
+    ctx.check(ctx.L.mace_attn_fwd(ctx.h, C.byref(a), _stream(stream)), "mace_attn_fwd")
+    return out

@@ -1,0 +1,34 @@
+"""Seeded random-init weights at the real architecture shapes (no checkpoints exist offline).
+
+Generated on the CPU with a torch.Generator so the device run and the CPU oracle see identical
+bf16 values for a given seed.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .config import ModelConfig
+
+
+def init_weights(cfg: ModelConfig, seed: int = 0, device: str | torch.device = "cpu") -> dict[str, torch.Tensor]:
+    """bf16 weights; CPU generation is the parity-test path, device generation is for the big presets."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    out: dict[str, torch.Tensor] = {}
+    resid_std = cfg.init_std / math.sqrt(2 * cfg.n_layers)
+    for name, shape in cfg.param_shapes().items():
+        if name == "embed":
+            t = torch.randn(shape, generator=g, device=device) * cfg.embed_std
+        elif name == "pos_embed":
+            t = torch.randn(shape, generator=g, device=device) * 0.01
+        elif name.endswith("norm.w"):
+            t = 1.0 + 0.05 * torch.randn(shape, generator=g, device=device)
+        elif name.endswith(".b"):
+            t = 0.02 * torch.randn(shape, generator=g, device=device)
+        elif name.endswith("o.w") or name.endswith("down.w"):
+            t = torch.randn(shape, generator=g, device=device) * resid_std
+        else:
+            t = torch.randn(shape, generator=g, device=device) * cfg.init_std
+        out[name] = t.to(torch.bfloat16)
+    return out
