@@ -105,8 +105,9 @@ typedef struct MaceKvLayout {
 } MaceKvLayout;
 
 /* ---------------------------------------------------------------- row kernels */
-int mace_embed(mace_ctx* ctx, const int* tokens, const int* pos, const void* emb, const void* pos_emb, int T, int d,
-               float* x, void* stream);
+/* tokens[i] < 0 reads last_token[-tokens[i]-1] (the slot's previous greedy token, kept on device) */
+int mace_embed(mace_ctx* ctx, const int* tokens, const int* pos, const int* last_token, const void* emb,
+               const void* pos_emb, int T, int d, float* x, void* stream);
 int mace_norm(mace_ctx* ctx, const float* x, int ldx, const int* rows, int n_rows, int d, const void* w,
               const void* b, int layernorm, float eps, void* out, int ldo, float* rstd_out, void* stream);
 int mace_rope_kv(mace_ctx* ctx, void* qkv, int T, int Hq, int Hkv, int hd, const int* row_pos, const int* row_seq,
@@ -135,6 +136,46 @@ typedef struct MaceAttnArgs {
   float scale;        /* softmax scale, 0 -> 1/sqrt(hd) */
 } MaceAttnArgs;
 int mace_attn_fwd(mace_ctx* ctx, const MaceAttnArgs* args, void* stream);
+
+/* ---------------------------------------------------------------- (3) fused DPO + masked AdamW
+ * logits fp32 [R, ld] for the response-predicting rows of the tick's FT sequences; targets [R];
+ * pair_rows [n_pairs][4] = (chosen_row0, n_chosen, rejected_row0, n_rejected); row_ps[R] = 2*pair+side.
+ * ref_lp [n_pairs][2] (NULL: only the policy log-probs lp_out are produced, e.g. for the pi_ref pass).
+ * Outputs: loss/margin [n_pairs] (loss = softplus(-beta m), alignment.py:39-47), coef [n_pairs][2]
+ * and, if dlogits != NULL, dlogits bf16 [R, ldd] = d(mean loss)/d logits.                          */
+int mace_dpo_fused(mace_ctx* ctx, const float* logits, int R, int V, int ld, const int* targets, const int* pair_rows,
+                   int n_pairs, const int* row_ps, const float* ref_lp, float beta, float* row_lse, float* row_lp,
+                   float* lp_out, float* loss, float* margin, float* coef, void* dlogits, int ldd, void* stream);
+/* masked AdamW over the selected-parameter segments: flat fp32 master/m/v/grad [n]; segment s covers
+ * [seg_offsets[s], seg_offsets[s+1]) and its bf16 working copy is seg_weights[s] (device array of
+ * device pointers). torch.optim.AdamW update order; step is 1-based.                               */
+int mace_adamw_masked(mace_ctx* ctx, float* master, float* m, float* v, const float* grad, long long n,
+                      const long long* seg_offsets, void* const* seg_weights, int n_seg, float lr, float beta1,
+                      float beta2, float eps, float weight_decay, int step, void* stream);
+
+/* ---------------------------------------------------------------- FT-row backward pieces */
+int mace_norm_bwd(mace_ctx* ctx, const float* x, int ldx, const int* xrows, const float* dy, int lddy, int n, int d,
+                  const void* w, int layernorm, float eps, float* dx, int lddx, const int* dxrows, float* dw, float* db,
+                  float* workspace, size_t workspace_bytes, void* stream);
+int mace_colsum_bf16(mace_ctx* ctx, const void* y, int n, int N, int ld, float* out, float* workspace,
+                     size_t workspace_bytes, void* stream);
+int mace_act_bwd(mace_ctx* ctx, const void* u, const void* da, int n, int F, int swiglu, void* du, void* stream);
+int mace_rope_bwd(mace_ctx* ctx, float* dqkv, int n, int Hq, int Hkv, int hd, const int* pos, const float* cos_t,
+                  const float* sin_t, void* stream);
+int mace_f32_to_bf16(mace_ctx* ctx, const float* x, long long n, void* y, void* stream);
+int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, const void* dout, const float* lse, int n_rows, int Hq,
+                  int Hkv, int hd, const MaceSeq* seqs, const int* items, int n_items, int row_offset, float* Dbuf,
+                  float* dqkv, void* stream);
+
+/* ---------------------------------------------------------------- (4) KV pages */
+int mace_kv_decode_alloc(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, int n, void* stream);
+int mace_kv_trim(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, const int* kept, int n, void* stream);
+int mace_kv_release(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, int n, void* stream);
+int mace_kv_page_copy(mace_ctx* ctx, const int* copies, int n, int n_kv_heads, int hd, long long pages_per_layer,
+                      int n_layers, void* k_pools, void* v_pools, void* stream);
+int mace_kv_set_prompt_tables(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, const int* tables, int n,
+                              int ncols, void* stream);
+int mace_scatter_tokens(mace_ctx* ctx, const int* src, const int* slots, int n, int* last_token, void* stream);
 
 #ifdef __cplusplus
 }

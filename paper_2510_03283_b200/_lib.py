@@ -64,13 +64,29 @@ SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_last_error": (C.c_char_p, [C.c_void_p]),
     "mace_launch_count": (C.c_longlong, [C.c_void_p]),
     "mace_gemm_bf16": (C.c_int, [C.c_void_p, C.POINTER(MaceGemmArgs), C.c_void_p]),
-    "mace_embed": (C.c_int, [_vp, _ip, _ip, _vp, _vp, _i, _i, _vp, _vp]),
+    "mace_embed": (C.c_int, [_vp, _ip, _ip, _ip, _vp, _vp, _i, _i, _vp, _vp]),
     "mace_norm": (C.c_int, [_vp, _vp, _i, _ip, _i, _i, _vp, _vp, _i, _f, _vp, _i, _vp, _vp]),
     "mace_rope_kv": (C.c_int, [_vp, _vp, _i, _i, _i, _i, _ip, _ip, _ip, _vp, _vp, _vp, _i,
                                C.POINTER(MaceKvLayout), _vp, _vp, _vp]),
     "mace_act": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp]),
     "mace_argmax": (C.c_int, [_vp, _vp, _i, _i, _i, _ip, _vp]),
     "mace_attn_fwd": (C.c_int, [_vp, C.POINTER(MaceAttnArgs), _vp]),
+    "mace_dpo_fused": (C.c_int, [_vp, _vp, _i, _i, _i, _ip, _ip, _i, _ip, _vp, _f, _vp, _vp, _vp, _vp, _vp, _vp,
+                                 _vp, _i, _vp]),
+    "mace_adamw_masked": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_longlong, _vp, _vp, _i, _f, _f, _f, _f, _f, _i, _vp]),
+    "mace_norm_bwd": (C.c_int, [_vp, _vp, _i, _ip, _vp, _i, _i, _i, _vp, _i, _f, _vp, _i, _ip, _vp, _vp, _vp,
+                                C.c_size_t, _vp]),
+    "mace_colsum_bf16": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp, C.c_size_t, _vp]),
+    "mace_act_bwd": (C.c_int, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp]),
+    "mace_rope_bwd": (C.c_int, [_vp, _vp, _i, _i, _i, _i, _ip, _vp, _vp, _vp]),
+    "mace_f32_to_bf16": (C.c_int, [_vp, _vp, C.c_longlong, _vp, _vp]),
+    "mace_attn_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _ip, _i, _i, _vp, _vp, _vp]),
+    "mace_kv_decode_alloc": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _i, _vp]),
+    "mace_kv_trim": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _ip, _i, _vp]),
+    "mace_kv_release": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _i, _vp]),
+    "mace_kv_page_copy": (C.c_int, [_vp, _ip, _i, _i, _i, C.c_longlong, _i, _vp, _vp, _vp]),
+    "mace_kv_set_prompt_tables": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _ip, _i, _i, _vp]),
+    "mace_scatter_tokens": (C.c_int, [_vp, _ip, _ip, _i, _ip, _vp]),
 }
 
 _lib = None

@@ -1,0 +1,431 @@
+// Backward kernels for the fine-tune rows of the hybrid batch: only FT rows, only
+// the selected layers and above (the reference's "alignment-sensitive" update, PAPER.md:108-109 /
+// alignment.py:168-172 stand-in). GEMM-shaped backward work (dX = dY.W, dW = dY^T.X) runs on the
+// tcgen05 GEMM with MN-major operands; these are the row-wise and attention pieces.
+//   norm_bwd    RMSNorm/LayerNorm: dx (+= into the residual grad, optional row scatter), dw/db partials
+//   col_reduce  deterministic column sums of per-block partials (dw, db, bias grads)
+//   act_bwd     SwiGLU / GELU(tanh)
+//   rope_bwd    inverse rotation of dq/dk
+//   attn_bwd    dense causal attention backward for FT sequences (dQ via fp32 atomics, dK/dV owned)
+#include "common.cuh"
+#include "mace_internal.h"
+
+namespace mace {
+
+// ------------------------------------------------------------------ norm backward
+// rows i < n: x = xbuf[xrows ? xrows[i] : i], dy = dy[i]; dx written to dx[dxrows ? dxrows[i] : i] (+=).
+// Per-block partials of dw (and db) go to part[blockIdx.x][0..d) and part[blockIdx.x][d..2d).
+template <int kPerLane>
+__global__ void norm_bwd_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ xrows,
+                                const float* __restrict__ dy, int lddy, int n, int d, const __nv_bfloat16* __restrict__ w,
+                                int layernorm, float eps, float* __restrict__ dx, int lddx, const int* __restrict__ dxrows,
+                                float* __restrict__ part, int rows_per_block) {
+  extern __shared__ float sh[];  // [2][d] block partials
+  for (int c = threadIdx.x; c < 2 * d; c += blockDim.x) sh[c] = 0.f;
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
+  const int r_begin = blockIdx.x * rows_per_block, r_end = min(n, r_begin + rows_per_block);
+  float dwa[kPerLane], dba[kPerLane];  // per-warp partials, merged in fixed warp order (deterministic)
+#pragma unroll
+  for (int k = 0; k < kPerLane; ++k) dwa[k] = dba[k] = 0.f;
+  for (int i = r_begin + warp; i < r_end; i += nw) {
+    const float* xr = x + (size_t)(xrows ? xrows[i] : i) * ldx;
+    const float* gr = dy + (size_t)i * lddy;
+    float xv[kPerLane], gv[kPerLane];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const int c = k * 32 + lane;
+      xv[k] = c < d ? xr[c] : 0.f;
+      gv[k] = c < d ? gr[c] : 0.f;
+      s += xv[k];
+    }
+    const float mean = layernorm ? warp_sum(s) / d : 0.f;
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const int c = k * 32 + lane;
+      if (c < d) {
+        xv[k] -= mean;
+        ss += xv[k] * xv[k];
+      }
+    }
+    const float rstd = rsqrtf(warp_sum(ss) / d + eps);
+    float sum_g = 0.f, sum_gx = 0.f;
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const int c = k * 32 + lane;
+      if (c < d) {
+        const float gw = gv[k] * __bfloat162float(w[c]);
+        sum_g += gw;
+        sum_gx += gw * xv[k] * rstd;
+      }
+    }
+    sum_g = warp_sum(sum_g) / d;
+    sum_gx = warp_sum(sum_gx) / d;
+    float* dr = dx + (size_t)(dxrows ? dxrows[i] : i) * lddx;
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const int c = k * 32 + lane;
+      if (c < d) {
+        const float xh = xv[k] * rstd;
+        const float gw = gv[k] * __bfloat162float(w[c]);
+        const float g = layernorm ? rstd * (gw - sum_g - xh * sum_gx) : rstd * (gw - xh * sum_gx);
+        dr[c] += g;
+        dwa[k] += gv[k] * xh;
+        dba[k] += gv[k];
+      }
+    }
+  }
+  for (int wv = 0; wv < nw; ++wv) {
+    if (warp == wv) {
+#pragma unroll
+      for (int k = 0; k < kPerLane; ++k) {
+        const int c = k * 32 + lane;
+        if (c < d) {
+          sh[c] += dwa[k];
+          sh[d + c] += dba[k];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int c = threadIdx.x; c < 2 * d; c += blockDim.x) part[(size_t)blockIdx.x * 2 * d + c] = sh[c];
+}
+
+// out[c] += sum_b part[b * ld + c]   (fixed order over b)
+__global__ void col_reduce_kernel(const float* __restrict__ part, int nb, int ld, int ncols, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  float s = 0.f;
+  for (int b = 0; b < nb; ++b) s += part[(size_t)b * ld + c];
+  out[c] += s;
+}
+
+// column sums of a bf16 matrix (bias grads), partial per row-chunk then col_reduce
+__global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ y, int n, int N, int ld, int rows_per_block,
+                                   float* __restrict__ part) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  const int r0 = blockIdx.y * rows_per_block, r1 = min(n, r0 + rows_per_block);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += __bfloat162float(y[(size_t)r * ld + c]);
+  part[(size_t)blockIdx.y * N + c] = s;
+}
+
+// ------------------------------------------------------------------ activation backward
+__global__ void act_bwd_kernel(const __nv_bfloat16* __restrict__ u, const __nv_bfloat16* __restrict__ da, int n, int F,
+                               int swiglu, __nv_bfloat16* __restrict__ du) {
+  const size_t total = (size_t)n * F;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / F, c = i % F;
+    const float g = __bfloat162float(da[i]);
+    if (swiglu) {
+      const float a = __bfloat162float(u[r * 2 * F + c]);
+      const float b = __bfloat162float(u[r * 2 * F + F + c]);
+      const float sg = 1.f / (1.f + __expf(-a));
+      du[r * 2 * F + c] = __float2bfloat16(g * b * sg * (1.f + a * (1.f - sg)));
+      du[r * 2 * F + F + c] = __float2bfloat16(g * a * sg);
+    } else {
+      const float x = __bfloat162float(u[i]);
+      const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+      const float inner = k0 * (x + k1 * x * x * x);
+      const float th = tanhf(inner);
+      const float dgelu = 0.5f * (1.f + th) + 0.5f * x * (1.f - th * th) * k0 * (1.f + 3.f * k1 * x * x);
+      du[i] = __float2bfloat16(g * dgelu);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ RoPE backward on dq / dk (fp32 rows)
+__global__ void rope_bwd_kernel(float* __restrict__ dqkv, int n, int Hq, int Hkv, int hd, const int* __restrict__ pos,
+                                const float* __restrict__ cos_t, const float* __restrict__ sin_t) {
+  const int r = blockIdx.x;
+  if (r >= n) return;
+  const int W = (Hq + 2 * Hkv) * hd, half = hd / 2;
+  float* row = dqkv + (size_t)r * W;
+  const int p = pos[r];
+  for (int idx = threadIdx.x; idx < (Hq + Hkv) * half; idx += blockDim.x) {
+    const int h = idx / half, i = idx % half;
+    float* b = row + h * hd;
+    const float c = cos_t[(size_t)p * half + i], s = sin_t[(size_t)p * half + i];
+    const float g1 = b[i], g2 = b[i + half];
+    b[i] = g1 * c + g2 * s;
+    b[i + half] = -g1 * s + g2 * c;
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ x, long long n, __nv_bfloat16* __restrict__ y) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16(x[i]);
+}
+
+// ------------------------------------------------------------------ attention backward (dense FT sequences)
+// D[r, hq] = sum_d dO[r, hq, d] * O[r, hq, d]
+__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout, int n,
+                                     int Hq, int hd, float* __restrict__ Dout) {
+  const int idx = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (idx >= n * Hq) return;
+  const __nv_bfloat16* a = o + (size_t)idx * hd;
+  const __nv_bfloat16* b = dout + (size_t)idx * hd;
+  float s = 0.f;
+  for (int c = lane; c < hd; c += 32) s += __bfloat162float(a[c]) * __bfloat162float(b[c]);
+  s = warp_sum(s);
+  if (lane == 0) Dout[idx] = s;
+}
+
+// block = (seq, kv head h, key block jb of 64). Loops over the G query heads of the group and the
+// query chunks at or after the key block (causal). K/V block fp32 in smem.
+template <int HD>
+__global__ void __launch_bounds__(256) attn_bwd_kernel(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ dout,
+                                                       const float* __restrict__ lse, const float* __restrict__ Dv,
+                                                       const MaceSeq* __restrict__ seqs, const int4* __restrict__ items,
+                                                       int Hq, int Hkv, float scale, float* __restrict__ dqkv,
+                                                       int row_offset) {
+  constexpr int B = 64;
+  constexpr int LDH = HD + 1;
+  extern __shared__ float sm[];
+  float* Ks = sm;                 // [B][LDH]
+  float* Vs = Ks + B * LDH;       // [B][LDH]
+  float* Qs = Vs + B * LDH;       // [B][LDH]
+  float* dOs = Qs + B * LDH;      // [B][LDH]
+  float* Ps = dOs + B * LDH;      // [B][B+1]  P[q][k]
+  float* dSs = Ps + B * (B + 1);  // [B][B+1]
+  float* ls = dSs + B * (B + 1);  // [B] lse
+  float* Ds = ls + B;             // [B]
+
+  const int4 it = items[blockIdx.x];
+  const MaceSeq sq = seqs[it.x];
+  const int h = it.y, jb = it.z;
+  const int G = Hq / Hkv;
+  const int W = (Hq + 2 * Hkv) * HD;
+  const int n = sq.q_len;
+  const int base = sq.q_start - row_offset;  // local row of token 0 in the FT activation block
+  const int k0 = jb * B;
+  const int tid = threadIdx.x;
+  const int ty = tid / 16, tx = tid % 16;  // 16x16 threads, 4x4 micro tiles
+
+  for (int i = tid; i < B * HD; i += 256) {
+    const int r = i / HD, c = i % HD;
+    const bool ok = k0 + r < n;
+    const __nv_bfloat16* row = qkv + (size_t)(base + k0 + r) * W;
+    Ks[r * LDH + c] = ok ? __bfloat162float(row[(Hq + h) * HD + c]) : 0.f;
+    Vs[r * LDH + c] = ok ? __bfloat162float(row[(Hq + Hkv + h) * HD + c]) : 0.f;
+  }
+  // dK / dV accumulators: thread owns key rows ty*4..+3, dims tx*(HD/16)..
+  constexpr int DC = HD / 16;
+  float dK[4][DC], dV[4][DC];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < DC; ++b) dK[a][b] = dV[a][b] = 0.f;
+
+  for (int g = 0; g < G; ++g) {
+    const int hq = h * G + g;
+    for (int q0 = k0; q0 < n; q0 += B) {  // causal: query chunks at or after the key block
+      __syncthreads();
+      for (int i = tid; i < B * HD; i += 256) {
+        const int r = i / HD, c = i % HD;
+        const bool ok = q0 + r < n;
+        Qs[r * LDH + c] = ok ? __bfloat162float(qkv[(size_t)(base + q0 + r) * W + hq * HD + c]) : 0.f;
+        dOs[r * LDH + c] = ok ? __bfloat162float(dout[(size_t)(base + q0 + r) * Hq * HD + hq * HD + c]) : 0.f;
+      }
+      for (int i = tid; i < B; i += 256) {
+        const bool ok = q0 + i < n;
+        ls[i] = ok ? lse[(size_t)(base + q0 + i) * Hq + hq] : 0.f;
+        Ds[i] = ok ? Dv[(size_t)(base + q0 + i) * Hq + hq] : 0.f;
+      }
+      __syncthreads();
+      // S = Q K^T, dP = dO V^T : thread computes q rows ty*4.., key cols tx*4..
+      float s[4][4], dp[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) s[a][b] = dp[a][b] = 0.f;
+      for (int d = 0; d < HD; ++d) {
+        float qa[4], ka[4], oa[4], va[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          qa[a] = Qs[(ty * 4 + a) * LDH + d];
+          oa[a] = dOs[(ty * 4 + a) * LDH + d];
+          ka[a] = Ks[(tx * 4 + a) * LDH + d];
+          va[a] = Vs[(tx * 4 + a) * LDH + d];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            s[a][b] = fmaf(qa[a], ka[b], s[a][b]);
+            dp[a][b] = fmaf(oa[a], va[b], dp[a][b]);
+          }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int qi = ty * 4 + a, qg = q0 + qi;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int kj = tx * 4 + b, kg = k0 + kj;
+          float p = 0.f;
+          if (qg < n && kg < n && kg <= qg) p = __expf(s[a][b] * scale - ls[qi]);
+          Ps[qi * (B + 1) + kj] = p;
+          dSs[qi * (B + 1) + kj] = p * (dp[a][b] - Ds[qi]);
+        }
+      }
+      __syncthreads();
+      // dV += P^T dO ; dK += dS^T Q * scale   (thread: key rows ty*4.., dims tx*DC..)
+      for (int qi = 0; qi < B; ++qi) {
+        float pa[4], sa[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          pa[a] = Ps[qi * (B + 1) + ty * 4 + a];
+          sa[a] = dSs[qi * (B + 1) + ty * 4 + a];
+        }
+#pragma unroll
+        for (int b = 0; b < DC; ++b) {
+          const float o_ = dOs[qi * LDH + tx * DC + b];
+          const float q_ = Qs[qi * LDH + tx * DC + b];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            dV[a][b] = fmaf(pa[a], o_, dV[a][b]);
+            dK[a][b] = fmaf(sa[a], q_, dK[a][b]);
+          }
+        }
+      }
+      // dQ += dS K * scale  (thread: q rows ty*4.., dims tx*DC..) -> atomics (G x key blocks contribute)
+      float dq[4][DC];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < DC; ++b) dq[a][b] = 0.f;
+      for (int kj = 0; kj < B; ++kj) {
+        float sa[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) sa[a] = dSs[(ty * 4 + a) * (B + 1) + kj];
+#pragma unroll
+        for (int b = 0; b < DC; ++b) {
+          const float k_ = Ks[kj * LDH + tx * DC + b];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) dq[a][b] = fmaf(sa[a], k_, dq[a][b]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int qg = q0 + ty * 4 + a;
+        if (qg < n) {
+#pragma unroll
+          for (int b = 0; b < DC; ++b) atomicAdd(&dqkv[(size_t)(base + qg) * W + hq * HD + tx * DC + b], dq[a][b] * scale);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int kg = k0 + ty * 4 + a;
+    if (kg < n) {
+#pragma unroll
+      for (int b = 0; b < DC; ++b) {
+        dqkv[(size_t)(base + kg) * W + (Hq + h) * HD + tx * DC + b] = dK[a][b] * scale;
+        dqkv[(size_t)(base + kg) * W + (Hq + Hkv + h) * HD + tx * DC + b] = dV[a][b];
+      }
+    }
+  }
+}
+
+}  // namespace mace
+
+using namespace mace;
+
+extern "C" int mace_norm_bwd(mace_ctx* ctx, const float* x, int ldx, const int* xrows, const float* dy, int lddy, int n,
+                             int d, const void* w, int layernorm, float eps, float* dx, int lddx, const int* dxrows,
+                             float* dw, float* db, float* workspace, size_t workspace_bytes, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int rows_per_block = 32;
+  const int nb = (n + rows_per_block - 1) / rows_per_block;
+  if (workspace_bytes < (size_t)nb * 2 * d * 4) return mace_fail(ctx, MACE_ERR_ARG, "norm_bwd: workspace too small");
+  const int per_lane = (d + 31) / 32;
+  const size_t sh = 2 * d * sizeof(float);
+  auto* W = (const __nv_bfloat16*)w;
+#define MACE_NB(K) norm_bwd_kernel<K><<<nb, 256, sh, s>>>(x, ldx, xrows, dy, lddy, n, d, W, layernorm, eps, dx, lddx, dxrows, workspace, rows_per_block)
+  if (per_lane <= 8) MACE_NB(8);
+  else if (per_lane <= 24) MACE_NB(24);
+  else if (per_lane <= 64) MACE_NB(64);
+  else if (per_lane <= 128) MACE_NB(128);
+  else return mace_fail(ctx, MACE_ERR_ARG, "norm_bwd: d too large");
+#undef MACE_NB
+  col_reduce_kernel<<<(d + 255) / 256, 256, 0, s>>>(workspace, nb, 2 * d, d, dw);
+  ctx->launches += 2;
+  if (layernorm && db) {
+    col_reduce_kernel<<<(d + 255) / 256, 256, 0, s>>>(workspace + d, nb, 2 * d, d, db);
+    ctx->launches++;
+  }
+  return mace_check_launch(ctx, "norm_bwd");
+}
+
+extern "C" int mace_colsum_bf16(mace_ctx* ctx, const void* y, int n, int N, int ld, float* out, float* workspace,
+                                size_t workspace_bytes, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int rpb = 64;
+  const int nb = (n + rpb - 1) / rpb;
+  if (workspace_bytes < (size_t)nb * N * 4) return mace_fail(ctx, MACE_ERR_ARG, "colsum: workspace too small");
+  colsum_bf16_kernel<<<dim3((N + 255) / 256, nb), 256, 0, s>>>((const __nv_bfloat16*)y, n, N, ld, rpb, workspace);
+  col_reduce_kernel<<<(N + 255) / 256, 256, 0, s>>>(workspace, nb, N, N, out);
+  ctx->launches += 2;
+  return mace_check_launch(ctx, "colsum");
+}
+
+extern "C" int mace_act_bwd(mace_ctx* ctx, const void* u, const void* da, int n, int F, int swiglu, void* du,
+                            void* stream) {
+  if (n <= 0) return 0;
+  int grid = (int)(((size_t)n * F + 255) / 256);
+  if (grid > ctx->num_sms * 16) grid = ctx->num_sms * 16;
+  act_bwd_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)u, (const __nv_bfloat16*)da, n, F, swiglu,
+                                                         (__nv_bfloat16*)du);
+  ctx->launches++;
+  return mace_check_launch(ctx, "act_bwd");
+}
+
+extern "C" int mace_rope_bwd(mace_ctx* ctx, float* dqkv, int n, int Hq, int Hkv, int hd, const int* pos,
+                             const float* cos_t, const float* sin_t, void* stream) {
+  if (n <= 0) return 0;
+  rope_bwd_kernel<<<n, 128, 0, (cudaStream_t)stream>>>(dqkv, n, Hq, Hkv, hd, pos, cos_t, sin_t);
+  ctx->launches++;
+  return mace_check_launch(ctx, "rope_bwd");
+}
+
+extern "C" int mace_f32_to_bf16(mace_ctx* ctx, const float* x, long long n, void* y, void* stream) {
+  if (n <= 0) return 0;
+  long long grid = (n + 255) / 256;
+  if (grid > ctx->num_sms * 16) grid = ctx->num_sms * 16;
+  f32_to_bf16_kernel<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(x, n, (__nv_bfloat16*)y);
+  ctx->launches++;
+  return mace_check_launch(ctx, "f32_to_bf16");
+}
+
+// items int4 [n_items] = (seq, kv_head, key_block, 0); rows of qkv/dout/lse/dqkv are local to the FT
+// block starting at global row `row_offset`. dqkv must be zeroed by the caller (dq accumulates).
+extern "C" int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, const void* dout, const float* lse, int n_rows,
+                             int Hq, int Hkv, int hd, const MaceSeq* seqs, const int* items, int n_items, int row_offset,
+                             float* Dbuf, float* dqkv, void* stream) {
+  if (n_items <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  attn_bwd_prep_kernel<<<(n_rows * Hq + 7) / 8, 256, 0, s>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, n_rows,
+                                                             Hq, hd, Dbuf);
+  const float scale = 1.f / sqrtf((float)hd);
+  auto go = [&](auto kern, int HD) {
+    const size_t sh = (4 * 64 * (HD + 1) + 2 * 64 * 65 + 128) * sizeof(float);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+    kern<<<n_items, 256, sh, s>>>((const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse, Dbuf, seqs,
+                                  reinterpret_cast<const int4*>(items), Hq, Hkv, scale, dqkv, row_offset);
+  };
+  switch (hd) {
+    case 32: go(attn_bwd_kernel<32>, 32); break;
+    case 64: go(attn_bwd_kernel<64>, 64); break;
+    case 128: go(attn_bwd_kernel<128>, 128); break;
+    default: return mace_fail(ctx, MACE_ERR_UNSUPPORTED, "attn_bwd: head_dim");
+  }
+  ctx->launches += 2;
+  return mace_check_launch(ctx, "attn_bwd");
+}

@@ -12,13 +12,17 @@
 namespace mace {
 
 // ------------------------------------------------------------------ embed
+// tokens[row] < 0 means "the token this request's slot produced last tick": last_token[-tok-1]
+// (decode input feedback stays on the device; no host round trip per tick)
 __global__ void embed_kernel(const int* __restrict__ tokens, const int* __restrict__ pos,
-                             const __nv_bfloat16* __restrict__ emb, const __nv_bfloat16* __restrict__ pos_emb, int T,
-                             int d, float* __restrict__ x) {
+                             const int* __restrict__ last_token, const __nv_bfloat16* __restrict__ emb,
+                             const __nv_bfloat16* __restrict__ pos_emb, int T, int d, float* __restrict__ x) {
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (row >= T) return;
   const int lane = threadIdx.x & 31;
-  const __nv_bfloat16* e = emb + (size_t)tokens[row] * d;
+  int tok = tokens[row];
+  if (tok < 0) tok = last_token[-tok - 1];
+  const __nv_bfloat16* e = emb + (size_t)tok * d;
   const __nv_bfloat16* pe = pos_emb ? pos_emb + (size_t)pos[row] * d : nullptr;
   float* xr = x + (size_t)row * d;
   for (int c = lane * 8; c < d; c += 256) {
@@ -223,11 +227,11 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int ld, i
 
 using namespace mace;
 
-extern "C" int mace_embed(mace_ctx* ctx, const int* tokens, const int* pos, const void* emb, const void* pos_emb, int T,
-                          int d, float* x, void* stream) {
+extern "C" int mace_embed(mace_ctx* ctx, const int* tokens, const int* pos, const int* last_token, const void* emb,
+                          const void* pos_emb, int T, int d, float* x, void* stream) {
   if (T <= 0) return 0;
   if (d % 256) return mace_fail(ctx, MACE_ERR_ARG, "embed: d must be a multiple of 256");
-  embed_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>(tokens, pos, (const __nv_bfloat16*)emb,
+  embed_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>(tokens, pos, last_token, (const __nv_bfloat16*)emb,
                                                                  (const __nv_bfloat16*)pos_emb, T, d, x);
   ctx->launches++;
   return mace_check_launch(ctx, "embed");

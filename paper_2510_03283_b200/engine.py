@@ -1,0 +1,305 @@
+"""GpuEngine: the drop-in for the reference's hybrid iteration.
+
+The reference exposes no plugin registry; its override point is ``Engine._execute(plan)``
+(/root/reference/pkg/src/macesim/engine.py:573-676), called once per tick with the packed bin of
+Alg. 1 (scheduler.py:133-188). ``GpuEngine`` subclasses the UNMODIFIED reference Engine:
+
+  1. it snapshots the bin's pre-tick state and builds ONE ragged batch in the reference's row order
+     (prefills in trie-DFS order, decodes by id, fine-tunes by id; engine.py:578-584);
+  2. it launches the hybrid step on the B200 (HybridModel.step, all math in libmace_b200.so);
+  3. it calls ``super()._execute(plan)`` so every bookkeeping effect (TTFT/TBT, KV MB, head stats,
+     prune, ft_step, check_end, retire/requeue, timeline) is the reference's own code;
+  4. it mirrors the reference's post-tick KV decisions onto the device (per-head prune trims,
+     retirements -> page release; trie evictions via GpuPrefixTrie).
+
+Clock modes:
+  "P"  parity: the reference cost model drives the clock -> scheduler decisions are bit-identical
+       to an unmodified reference run; the GPU executes the same bins for real.
+  "M"  measured: the tick duration is the measured device time of the hybrid step (the reference's
+       own instrument precedent, engine.py:602-604), via CostProfile.bin_latency (cost_model.py:64-69).
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from .batch import KIND_DECODE, KIND_FT, KIND_PREFILL, PAGE, FtPair, TickBatch
+from .config import ModelConfig, TrainConfig
+from .kvmanager import GpuPrefixTrie, GroupPool, plan_prefill_pages
+from .model import HybridModel
+from .refpath import ensure_macesim
+
+ensure_macesim()
+from macesim.cache import dfs_order  # noqa: E402
+from macesim.cost_model import CostProfile  # noqa: E402
+from macesim.engine import Engine  # noqa: E402
+from macesim.workload import WorkloadType  # noqa: E402
+
+
+def synthetic_pair_tokens(seed: int, rid: int, n_c: int, n_r: int, vocab: int) -> tuple[list[int], list[int]]:
+    """Builder-defined chosen/rejected content (mace-trace-v1 carries lengths only, workload.py:205,265)."""
+    c = np.random.default_rng([seed, 307, rid]).integers(0, vocab, n_c).tolist()
+    r = np.random.default_rng([seed, 308, rid]).integers(0, vocab, n_r).tolist()
+    return c, r
+
+
+class _MeasuredProfile(CostProfile):
+    """CostProfile whose bin latency is the measured device time of the current tick (mode M).
+
+    CostProfile.bin_latency (cost_model.py:64-69) is the single point where the reference forms a
+    tick's duration (engine.py:605-611), so replacing it is the whole measured-clock hook."""
+
+    def bin_latency(self, max_member_lat: float, n_members: int) -> float:
+        return self._clock[0]
+
+
+def measured_profile(profile: CostProfile) -> _MeasuredProfile:
+    fields = {k: getattr(profile, k) for k in profile.__dataclass_fields__}
+    fields["iter_overhead"] = 0.0
+    p = _MeasuredProfile(**fields)
+    object.__setattr__(p, "_clock", [0.0])
+    return p
+
+
+class GpuEngine(Engine):
+    def __init__(self, trace, profile, sched_cfg, priority_params, cache_cfg, env, engine_cfg, metrics_horizon=None,
+                 *, model: HybridModel, mode: str = "P", seed: int | None = None, record: bool = False):
+        if mode not in ("P", "M"):
+            raise ValueError("mode must be 'P' (parity clock) or 'M' (measured clock)")
+        if mode == "M":
+            profile = measured_profile(profile)
+            engine_cfg = replace(engine_cfg, scheduler_overhead_ms=0.0)
+        super().__init__(trace, profile, sched_cfg, priority_params, cache_cfg, env, engine_cfg, metrics_horizon)
+        if model.cfg.n_kv_heads != cache_cfg.num_heads:
+            raise ValueError("CacheConfig.num_heads must equal the model's KV heads (per-head KV windows)")
+        self.model = model
+        self.mcfg: ModelConfig = model.cfg
+        self.mode = mode
+        self.seed = engine_cfg.seed if seed is None else seed
+        self.pool = GroupPool(model.prompt_groups)
+        if self.trie is not None:
+            self.trie = GpuPrefixTrie(profile.decode_kv_mem_per_token, self.pool)
+        self.free_slots = list(range(model.max_slots - 1, -1, -1))
+        self.slot_of: dict[int, int] = {}
+        self.table_of: dict[int, list[int]] = {}
+        self.ref_lp: dict[int, tuple[float, float]] = {}
+        self._pending_ref: list = []
+        self.record = record
+        self.records: list[dict] = []
+        self.tick_tokens: list[int] = []
+        self.tick_device_ms: list[float] = []
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        self._planned_shared: dict[int, int] = {}
+        self._dec_out: list = []
+
+    # ------------------------------------------------------------------ helpers
+    def _slot(self, rid: int) -> int:
+        if rid not in self.slot_of:
+            if not self.free_slots:
+                raise RuntimeError("out of KV slots (raise HybridModel max_slots)")
+            self.slot_of[rid] = self.free_slots.pop()
+        return self.slot_of[rid]
+
+    def _resolve_ref(self) -> None:
+        for host, ev, rids in self._pending_ref:
+            ev.synchronize()
+            arr = host.numpy()
+            for i, rid in enumerate(rids):
+                self.ref_lp[rid] = (float(arr[i, 0]), float(arr[i, 1]))
+        self._pending_ref.clear()
+
+    # ------------------------------------------------------------------ batch building
+    def build_batch(self, prefills, decodes, fts) -> TickBatch:
+        c = self.mcfg
+        toks, pos, rseq, rkvi = [], [], [], []
+        seqs, tc_items, dec_items = [], [], []
+        dec_slots, dec_rows = [], []
+        ptab_slots, ptab_rows, copies = [], [], []
+        n_pre = n_dec = n_ft = 0
+        pending_cached: set[int] = set()
+        self._planned_shared = {}
+
+        def add_tc(si, q_len):
+            for hq in range(c.n_heads):
+                for qb in range((q_len + 127) // 128):
+                    tc_items.append((si, hq, qb, 0))
+
+        for req in prefills:
+            rs = self.state[req.id]
+            slot = self._slot(req.id)
+            P = len(req.prompt_tokens)
+            shared, table, cps = plan_prefill_pages(self.trie, self.pool, rs.leaf, P, pending_cached)
+            self._planned_shared[req.id] = shared
+            self.table_of[req.id] = table
+            ptab_slots.append(slot)
+            ptab_rows.append(table)
+            copies += [(s_, d_, n_, 0) for s_, d_, n_ in cps]
+            q = P - shared
+            if q <= 0:
+                continue
+            si = len(seqs)
+            seqs.append((KIND_PREFILL, len(toks), q, slot, P, P, -1, 0))
+            add_tc(si, q)
+            toks += req.prompt_tokens[shared:]
+            pos += list(range(shared, P))
+            rseq += [si] * q
+            rkvi += list(range(shared, P))
+            n_pre += q
+        for j, req in enumerate(decodes):
+            slot = self.slot_of[req.id]
+            P = len(req.prompt_tokens)
+            k0 = req.decode_pos
+            si = len(seqs)
+            seqs.append((KIND_DECODE, len(toks), 1, slot, P - 1, 0, j, 0))
+            dec_items += [(si, h) for h in range(c.n_kv_heads)]
+            dec_slots.append(slot)
+            dec_rows.append(len(toks))
+            toks.append(req.prompt_tokens[-1] if k0 == 0 else -(slot + 1))
+            pos.append(P - 1 + k0)
+            rseq.append(si)
+            rkvi.append(k0)
+            n_dec += 1
+        ft0 = len(toks)
+        pairs: list[FtPair] = []
+        logit_rows, targets, pair_rows, row_ps = [], [], [], []
+        ft_seqs, ft_tc, ft_rseq, bwd = [], [], [], []
+        if fts:
+            self._resolve_ref()
+        for p_i, req in enumerate(fts):
+            P = len(req.prompt_tokens)
+            room = max(1, c.max_pos - P)
+            n_c = min(req.pair.tokens_chosen, room)
+            n_r = min(req.pair.tokens_rejected, room)
+            ch, rj = synthetic_pair_tokens(self.seed, req.id, n_c, n_r, c.vocab)
+            pairs.append(FtPair(req.id, req.prompt_tokens, ch, rj, self.ref_lp.get(req.id)))
+            pr = []
+            for side, resp in enumerate((ch, rj)):
+                n = P + len(resp)
+                si = len(seqs)
+                q0 = len(toks)
+                seqs.append((KIND_FT, q0, n, -1, 0, n, -1, 0))
+                add_tc(si, n)
+                fs = len(ft_seqs)
+                ft_seqs.append((KIND_FT, q0 - ft0, n, -1, 0, n, -1, 0))
+                for hq in range(c.n_heads):
+                    for qb in range((n + 127) // 128):
+                        ft_tc.append((fs, hq, qb, 0))
+                bwd += [(fs, h, kb, 0) for h in range(c.n_kv_heads) for kb in range((n + 63) // 64)]
+                toks += list(req.prompt_tokens) + list(resp)
+                pos += list(range(n))
+                rseq += [si] * n
+                rkvi += [-1] * n
+                ft_rseq += [fs] * n
+                pr += [len(logit_rows), len(resp)]
+                for i, y in enumerate(resp):
+                    logit_rows.append(q0 + P - 1 + i)
+                    targets.append(y)
+                    row_ps.append(2 * p_i + side)
+                n_ft += n
+            pair_rows.append(pr)
+
+        def arr(x, shape_tail=()):
+            a = np.asarray(x, dtype=np.int32)
+            return a.reshape((-1,) + shape_tail) if a.size or shape_tail else a.reshape(-1)
+
+        maxpp = self.model.maxpp
+        pt = np.full((len(ptab_rows), maxpp), 0, np.int32)
+        for i, t in enumerate(ptab_rows):
+            if len(t) > maxpp:
+                raise RuntimeError("prompt longer than max_prompt_len")
+            pt[i, : len(t)] = t
+        return TickBatch(
+            tokens=arr(toks), pos=arr(pos), row_seq=arr(rseq), row_kvi=arr(rkvi),
+            seqs=arr(seqs, (8,)), tc_items=arr(tc_items, (4,)), dec_items=arr(dec_items, (2,)),
+            dec_slots=arr(dec_slots), dec_rows=arr(dec_rows), ptab_slots=arr(ptab_slots), ptab_rows=pt,
+            page_copies=arr(copies, (4,)), ft0=ft0, ft_pairs=pairs, ft_logit_rows=arr(logit_rows),
+            ft_targets=arr(targets), pair_rows=arr(pair_rows, (4,)), row_ps=arr(row_ps),
+            ft_seqs=arr(ft_seqs, (8,)), ft_tc_items=arr(ft_tc, (4,)), ft_row_seq=arr(ft_rseq),
+            bwd_items=arr(bwd, (4,)), n_prefill_tokens=n_pre, n_decode_tokens=n_dec, n_ft_tokens=n_ft,
+        )
+
+    # ------------------------------------------------------------------ the override point
+    def _execute(self, plan) -> None:  # engine.py:573
+        bin_ = plan.bin
+        prefills = [r for r in bin_.tasks if r.workload is WorkloadType.PREFILL]
+        decodes = sorted((r for r in bin_.tasks if r.workload is WorkloadType.DECODE), key=lambda r: r.id)
+        fts = sorted((r for r in bin_.tasks if r.workload is WorkloadType.FINETUNE), key=lambda r: r.id)
+        if self.trie is not None and len(prefills) > 1:  # identical ordering rule to engine.py:581-584
+            pending = [(r, self.state[r.id].leaf) for r in prefills]
+            if all(leaf is not None for _, leaf in pending):
+                prefills = dfs_order(self.trie, pending)
+        batch = self.build_batch(prefills, decodes, fts)
+        m = self.model
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        out = m.step(batch)
+        ev1.record()
+        self.h2d_bytes += m.h2d_bytes
+        if self.mode == "M":
+            ev1.synchronize()
+            self.profile._clock[0] = ev0.elapsed_time(ev1)
+        # ---- the reference's own bookkeeping for this bin (timeline, metrics, KV MB, prune, ft_step)
+        super()._execute(plan)
+        # ---- mirror post-tick KV decisions onto the device (retired requests were released already)
+        live_dec = [r for r in decodes if r.id in self.slot_of]
+        if self.pruning and live_dec:
+            slots = np.array([self.slot_of[r.id] for r in live_dec], np.int32)
+            kept = np.array([self.state[r.id].kept for r in live_dec], np.int32)
+            m.apply_trim(slots, kept)
+        if out.dec_tokens is not None:
+            host = torch.empty(batch.n_dec, dtype=torch.int32, pin_memory=True)
+            host.copy_(out.dec_tokens, non_blocking=True)
+            self.d2h_bytes += batch.n_dec * 4
+            self._dec_out.append(([r.id for r in decodes], host))
+        if fts and out.ref_lp is not None:
+            host = torch.empty(len(fts), 2, dtype=torch.float32, pin_memory=True)
+            host.copy_(out.ref_lp, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._pending_ref.append((host, ev, [r.id for r in fts]))
+            self.d2h_bytes += len(fts) * 8
+        self.tick_tokens.append(batch.total_tokens)
+        self.tick_device_ms.append((ev0, ev1))
+        if self.record:
+            self.records.append(dict(tick=self.tick_index - 1, batch=batch, out=out,
+                                     decode_ids=[r.id for r in decodes],
+                                     kept_post={r.id: list(self.state[r.id].kept) for r in decodes if self.pruning},
+                                     ft_ids=[r.id for r in fts]))
+
+    def _exec_prefill(self, req):  # engine.py:444 — check our plan against the reference's charge
+        if self.trie is not None and self.state[req.id].leaf is not None:
+            shared = self.trie.cached_prefix_len(req.prompt_tokens)
+            planned = self._planned_shared.get(req.id)
+            if planned is not None and planned != shared:
+                raise AssertionError(f"req {req.id}: planned shared prefix {planned} != reference {shared}")
+        return super()._exec_prefill(req)
+
+    def _retire(self, req, t_end_ms, rejected=False):  # engine.py:538
+        super()._retire(req, t_end_ms, rejected)
+        slot = self.slot_of.pop(req.id, None)
+        table = self.table_of.pop(req.id, None)
+        if table is not None:
+            for g in table:
+                self.pool.decref(g)
+        if slot is not None:
+            self.model.release_slots([slot])
+            self.free_slots.append(slot)
+
+    # ------------------------------------------------------------------ results
+    def decoded_tokens(self) -> dict[int, list[int]]:
+        torch.cuda.current_stream().synchronize()
+        out: dict[int, list[int]] = {}
+        for ids, host in self._dec_out:
+            arr = host.numpy()
+            for i, rid in enumerate(ids):
+                out.setdefault(rid, []).append(int(arr[i]))
+        return out
+
+    def device_ms(self) -> list[float]:
+        torch.cuda.current_stream().synchronize()
+        return [a.elapsed_time(b) for a, b in self.tick_device_ms]

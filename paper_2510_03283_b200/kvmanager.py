@@ -1,0 +1,170 @@
+"""Host side of the colocated KV memory manager: prompt page groups owned by prefix-trie nodes.
+
+The reference's PrefixTrie (cache.py:67-241) makes every decision (insert/split, cached prefix,
+mark_executed, release, LRU offload) in MB. ``GpuPrefixTrie`` subclasses it WITHOUT changing any
+decision (every override calls the reference implementation first) and mirrors each one onto real
+KV page groups:
+
+  * a page group = 16 consecutive prompt positions x every KV head x every layer (absolute-position
+    aligned, so all prompts sharing a prefix address the same logical pages);
+  * a trie node owns refs to the groups covering its token range; a group straddling a node boundary
+    is referenced by both nodes (split, cache.py:79-105, increments the ref);
+  * a request's prompt page table holds one ref per entry until it retires (cache.py:198-203);
+  * prefills reuse the groups of the deepest cached path node per logical page; the page holding
+    the first uncached position is copy-on-diverge (rows below the split copied on device);
+  * lru_offload (cache.py:217-238) drops the evicted nodes' refs; a group returns to the free list
+    when its last ref goes.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .batch import PAGE
+from .refpath import ensure_macesim
+
+ensure_macesim()
+from macesim.cache import PrefixTrie, TrieNode  # noqa: E402
+
+
+class KvCapacityError(RuntimeError):
+    pass
+
+
+class GroupPool:
+    def __init__(self, n_groups: int):
+        self.n = n_groups
+        self.free = list(range(n_groups - 1, -1, -1))
+        self.ref = np.zeros(n_groups, np.int32)
+
+    def alloc(self) -> int:
+        if not self.free:
+            raise KvCapacityError("prompt KV page groups exhausted (raise prompt_groups)")
+        g = self.free.pop()
+        self.ref[g] = 1
+        return g
+
+    def incref(self, g: int) -> None:
+        assert self.ref[g] > 0, f"incref of free group {g}"
+        self.ref[g] += 1
+
+    def decref(self, g: int) -> None:
+        self.ref[g] -= 1
+        assert self.ref[g] >= 0
+        if self.ref[g] == 0:
+            self.free.append(g)
+
+    @property
+    def in_use(self) -> int:
+        return self.n - len(self.free)
+
+
+def node_start(node: TrieNode) -> int:
+    s = 0
+    n = node.parent
+    while n is not None and n.parent is not None:
+        s += len(n.label)
+        n = n.parent
+    return s
+
+
+def page_range(a: int, b: int) -> range:
+    """Logical pages touched by token range [a, b)."""
+    return range(a // PAGE, (b - 1) // PAGE + 1) if b > a else range(0)
+
+
+class GpuPrefixTrie(PrefixTrie):
+    """Reference trie + page-group ownership mirror (decisions unchanged)."""
+
+    def __init__(self, kv_mb_per_token: float, pool: GroupPool):
+        super().__init__(kv_mb_per_token)
+        self.pool = pool
+        self.node_pages: dict[int, dict[int, int]] = {}
+        self.pending: dict[int, dict[int, int]] = {}   # pages a tick's prefill will hand to newly cached nodes
+
+    # -- decisions stay the reference's; ownership follows
+    def _split(self, node, at):
+        head = super()._split(node, at)
+        pages = self.node_pages.get(node.node_id)
+        if pages:
+            a = node_start(head)
+            cut = a + at
+            b = cut + len(node.label)
+            hp = {i: g for i, g in pages.items() if i in page_range(a, cut)}
+            tp = {i: g for i, g in pages.items() if i in page_range(cut, b)}
+            for i, g in tp.items():
+                if i in hp:
+                    self.pool.incref(g)  # straddling group now referenced by both halves
+            self.node_pages[head.node_id] = hp
+            self.node_pages[node.node_id] = tp
+        return head
+
+    def mark_executed(self, leaf, t):
+        newly = [n for n in leaf.path_nodes() if not n.cached]
+        added = super().mark_executed(leaf, t)
+        for n in newly:
+            pages = self.pending.pop(n.node_id, None)
+            if pages is None:
+                raise AssertionError(f"node {n.node_id} cached without device pages")
+            for g in pages.values():
+                self.pool.incref(g)
+            self.node_pages[n.node_id] = pages
+        return added
+
+    def lru_offload(self, bytes_needed, t):
+        res = super().lru_offload(bytes_needed, t)
+        for n in res.evicted:
+            for g in self.node_pages.pop(n.node_id, {}).values():
+                self.pool.decref(g)
+        return res
+
+
+def plan_prefill_pages(trie: GpuPrefixTrie | None, pool: GroupPool, leaf: TrieNode | None, prompt_len: int,
+                       pending_cached: set[int]) -> tuple[int, list[int], list[tuple[int, int, int]]]:
+    """Decide the device page table of one prefill (in trie-DFS order within the tick).
+
+    Returns (shared, table, copies): ``shared`` is exactly what Engine._exec_prefill will charge as
+    cached (cache.py:164-184, counting nodes an earlier prefill of the same tick will cache), ``table``
+    the group id of every logical prompt page, ``copies`` the copy-on-diverge list (src, dst, rows).
+    The request holds one ref on every table entry. Uncached path nodes get their future pages
+    registered as pending for mark_executed.
+    """
+    n_pages = (prompt_len + PAGE - 1) // PAGE
+    table = [-1] * n_pages
+    copies: list[tuple[int, int, int]] = []
+    if trie is None or leaf is None:
+        return 0, [pool.alloc() for _ in range(n_pages)], copies
+    path = leaf.path_nodes()
+    shared = 0
+    src_pages: dict[int, int] = {}
+    k = 0
+    for n in path:
+        cached = n.cached or n.node_id in pending_cached
+        if not cached:
+            break
+        pages = trie.node_pages.get(n.node_id) if n.cached else trie.pending.get(n.node_id)
+        assert pages is not None, f"cached node {n.node_id} without pages"
+        src_pages.update(pages)  # deeper nodes override shallower ones on a straddling page
+        shared += len(n.label)
+        k += 1
+    if shared == prompt_len:  # whole prompt cached: nothing is written, share every page
+        for i in range(n_pages):
+            table[i] = src_pages[i]
+            pool.incref(table[i])
+        return shared, table, copies
+    full = shared // PAGE
+    for i in range(full):
+        table[i] = src_pages[i]
+        pool.incref(table[i])
+    for i in range(full, n_pages):
+        table[i] = pool.alloc()
+    if shared % PAGE and full < n_pages:
+        copies.append((src_pages[full], table[full], shared % PAGE))
+    # nodes this prefill caches (mark_executed) adopt the request's pages
+    a = shared
+    for n in path[k:]:
+        b = a + len(n.label)
+        if not n.cached:
+            trie.pending[n.node_id] = {i: table[i] for i in page_range(a, b)}
+            pending_cached.add(n.node_id)
+        a = b
+    return shared, table, copies

@@ -1,0 +1,81 @@
+"""The BASELINE.json configs as concrete reference objects (SURVEY.md §8(d) "Configs as concrete
+synthetic inputs"). Every trace comes from the reference's own generate_trace (workload.py:174-218);
+traces are regenerated per run because the Engine mutates Requests in place (quirk Q1).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .config import PRESETS, ModelConfig, TrainConfig
+from .refpath import ensure_macesim
+
+ensure_macesim()
+from macesim.alignment import AlignmentEnv, TenantParams  # noqa: E402
+from macesim.cost_model import CostProfile  # noqa: E402
+from macesim.distributions import parse_dist  # noqa: E402
+from macesim.engine import CacheConfig, EngineConfig  # noqa: E402
+from macesim.priority import PriorityParams  # noqa: E402
+from macesim.scheduler import Policy, SchedulerConfig  # noqa: E402
+from macesim.workload import TraceConfig, generate_trace  # noqa: E402
+
+
+@dataclass
+class Workload:
+    name: str
+    model: ModelConfig
+    trace_cfg: TraceConfig
+    profile: CostProfile
+    sched: SchedulerConfig
+    cache: CacheConfig
+    horizon: float
+    seed: int
+    train: TrainConfig = field(default_factory=TrainConfig)
+    max_prompt_len: int = 4096
+
+    def trace(self):
+        return generate_trace(self.trace_cfg)
+
+    def env(self):
+        return AlignmentEnv.create({0: TenantParams()}, seed=self.trace_cfg.seed)
+
+    def engine_args(self):
+        """Positional args of Engine.__init__ (engine.py:186-196) with a fresh trace and env."""
+        return (self.trace(), self.profile, self.sched, PriorityParams(), self.cache, self.env(),
+                EngineConfig(seed=self.seed), self.horizon)
+
+
+def c1(seed: int = 0) -> Workload:
+    """tiny decoder, single-GPU/CPU correctness config with the golden tick 7."""
+    tc = TraceConfig(arrival_rate=10, retrain_rate=0.3, duration=5, seed=seed,
+                     prompt_len_dist=parse_dist("geometric:mean=64"), output_len_dist=parse_dist("geometric:mean=16"))
+    return Workload("c1", PRESETS["tiny"], tc, CostProfile(capacity=24576.0, weights_resident=14000.0),
+                    SchedulerConfig(), CacheConfig(weak_scale=0.05), 5.0, seed)
+
+
+def c2(seed: int = 1, arrival_rate: float = 100.0, duration: float = 60.0, policy: Policy = Policy.HYBRID) -> Workload:
+    """GPT-2 small hybrid serving + DPO, Poisson trace (prompt uniform 97..512: 1024 positions)."""
+    cfg = PRESETS["gpt2"]
+    tc = TraceConfig(arrival_rate=arrival_rate, retrain_rate=0.1, duration=duration, seed=seed,
+                     prompt_len_dist=parse_dist("uniform:lo=97,hi=512"),
+                     output_len_dist=parse_dist("geometric:mean=128"))
+    kv_mb = cfg.kv_bytes_per_token() / 2**20
+    prof = CostProfile(capacity=184320.0, weights_resident=2 * 247.0, decode_kv_mem_per_token=kv_mb)
+    sched = SchedulerConfig(policy=policy, max_decode_batch=256, tau_task=512, max_ft_batch=4, max_decode_steps=512)
+    return Workload("c2", cfg, tc, prof, sched, CacheConfig(num_heads=cfg.n_kv_heads, weak_scale=0.05), duration,
+                    seed, max_prompt_len=1024)
+
+
+def c3(seed: int = 2, arrival_rate: float = 200.0, duration: float = 20.0) -> Workload:
+    """Llama-3.2-1B decode-heavy: prompt 1920, output 128 (ctx <= 2048), batch 256."""
+    cfg = PRESETS["llama1b"]
+    tc = TraceConfig(arrival_rate=arrival_rate, retrain_rate=0.05, duration=duration, seed=seed,
+                     prompt_len_dist=parse_dist("constant:value=1920"),
+                     output_len_dist=parse_dist("constant:value=128"))
+    kv_mb = cfg.kv_bytes_per_token() / 2**20
+    prof = CostProfile(capacity=184320.0, weights_resident=2471.0 + 2 * 130.0, decode_kv_mem_per_token=kv_mb)
+    sched = SchedulerConfig(max_decode_batch=256, tau_task=512, max_ft_batch=4)
+    return Workload("c3", cfg, tc, prof, sched, CacheConfig(num_heads=cfg.n_kv_heads, weak_scale=0.05), duration,
+                    seed, max_prompt_len=2048)
+
+
+WORKLOADS = {"c1": c1, "c2": c2, "c3": c3}
