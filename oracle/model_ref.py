@@ -253,6 +253,7 @@ class OracleExecutor:
         ref = dict(self.model.w)
         ref.update(self.ref_params)
         losses, margins, total = [], [], 0.0
+        self.last_lp = []
         for rid, prompt, chosen, rejected in pairs:
             if rid not in self.ref_lp_cache:
                 with torch.no_grad():
@@ -266,11 +267,25 @@ class OracleExecutor:
             m = (lc - rc) - (lr_ - rr)
             loss = F.softplus(-beta * m)
             total = total + loss / len(pairs)
-            losses.append(float(loss))
-            margins.append(float(m))
+            losses.append(float(loss.detach()))
+            margins.append(float(m.detach()))
+            self.last_lp.append((float(lc.detach()), float(lr_.detach()), rc, rr))
         total.backward()
         grads = {n: params[n].grad.detach().clone() for n in self.selected}
         return losses, margins, grads
+
+    def load_state(self, master_flat, m_flat, v_flat) -> None:
+        """Adopt the device's optimizer state (flat fp32, selected-name order) so the next tick compares
+        one step from identical weights instead of two drifting trajectories."""
+        off = 0
+        for n in self.selected:
+            k = self.master[n].numel()
+            shape = self.master[n].shape
+            self.master[n] = master_flat[off: off + k].view(shape).clone()
+            self.m[n] = m_flat[off: off + k].view(shape).clone()
+            self.v[n] = v_flat[off: off + k].view(shape).clone()
+            self.model.w[n] = self.master[n].to(torch.bfloat16).float()
+            off += k
 
     def adamw(self, grads: dict[str, torch.Tensor]) -> None:
         """torch.optim.AdamW update order on fp32 masters; working weights = bf16(master)."""
@@ -292,3 +307,123 @@ def adamw_reference(p, m, v, g, lr, b1, b2, eps, wd, bc1, bc2):
     step_size = lr / bc1
     denom = (v.sqrt() / math.sqrt(bc2)).add_(eps)
     p.addcdiv_(m, denom, value=-step_size)
+
+
+class TickOracle:
+    """Replays the GPU's recorded tick batches (same rows, same page tables, same windows) in fp32.
+
+    The tick batch is the *input format* (row order, prompt page tables, copy-on-diverge list,
+    decode windows): the oracle reads it the way the device does, so prefix KV shared through the
+    trie is the KV the sharing request actually sees (computed by whichever earlier prefill, under
+    the weights of that time), exactly like the device pages.
+    """
+
+    PAGE = 16
+
+    def __init__(self, cfg, weights, tcfg, selected_names):
+        self.cfg = cfg
+        self.ex = OracleExecutor(cfg, weights, tcfg, selected_names)
+        self.model = self.ex.model
+        L, H, hd = cfg.n_layers, cfg.n_kv_heads, cfg.head_dim
+        self._shape = (L, H, self.PAGE, hd)
+        self.kstore: dict[int, torch.Tensor] = {}
+        self.vstore: dict[int, torch.Tensor] = {}
+        self.ptab: dict[int, list[int]] = {}
+        self.dec: dict[int, dict] = {}
+        self.last_token: dict[int, int] = {}
+
+    def _page(self, store, g):
+        if g not in store:
+            store[g] = torch.zeros(self._shape)
+        return store[g]
+
+    def run_tick(self, batch, gpu_tokens, kept_post):
+        """Returns (decode logits [n_dec, V], FT (losses, margins, grads) or None)."""
+        c = self.cfg
+        H, G = c.n_kv_heads, c.group
+        for slot, row in zip(batch.ptab_slots.tolist(), batch.ptab_rows.tolist()):
+            self.ptab[slot] = row
+        for src, dst, n, _ in batch.page_copies.tolist():
+            for st in (self.kstore, self.vstore):
+                self._page(st, dst)[:, :, :n] = self._page(st, src)[:, :, :n]
+        ft0 = batch.ft0
+        seqs = batch.seqs.tolist()
+        inf = [s for s in seqs if s[0] != 2]
+        logits = None
+        if ft0 > 0:
+            toks = []
+            for r in range(ft0):
+                t = int(batch.tokens[r])
+                toks.append(self.last_token[-t - 1] if t < 0 else t)
+            pos = batch.pos[:ft0].tolist()
+            x = self.model.embed(toks, pos)
+            for s in inf:  # decode slot state (reset when a slot starts a new request)
+                if s[0] == 1:
+                    j = int(batch.row_kvi[s[1]])
+                    if j == 0 or s[3] not in self.dec:
+                        self.dec[s[3]] = {"k": [[] for _ in range(c.n_layers)], "v": [[] for _ in range(c.n_layers)],
+                                          "first": [0] * H}
+
+            def attend(l, q, k, v):
+                # 1) write this layer's K/V for every row (prefill -> pages, decode -> slot lists)
+                for s in inf:
+                    kind, q0, ql, slot, n_pv = s[:5]
+                    for i in range(ql):
+                        r = q0 + i
+                        t = int(batch.row_kvi[r])
+                        if kind == 0:
+                            g = self.ptab[slot][t // self.PAGE]
+                            self._page(self.kstore, g)[l, :, t % self.PAGE] = k[r]
+                            self._page(self.vstore, g)[l, :, t % self.PAGE] = v[r]
+                        else:
+                            d = self.dec[slot]
+                            assert len(d["k"][l]) == t, "decode slot index mismatch"
+                            d["k"][l].append(k[r].clone())
+                            d["v"][l].append(v[r].clone())
+                # 2) attention per sequence over its visible KV
+                o = torch.zeros(q.shape[0], c.n_heads, c.head_dim)
+                for s in inf:
+                    kind, q0, ql, slot, n_pv = s[:5]
+                    tab = self.ptab[slot]
+                    Kp = torch.stack([self.kstore[tab[t // self.PAGE]][l, :, t % self.PAGE] for t in range(n_pv)]) \
+                        if n_pv else torch.zeros(0, H, c.head_dim)
+                    Vp = torch.stack([self.vstore[tab[t // self.PAGE]][l, :, t % self.PAGE] for t in range(n_pv)]) \
+                        if n_pv else torch.zeros(0, H, c.head_dim)
+                    if kind == 0:
+                        m = n_pv
+                        qlog = torch.arange(ql)[:, None] + (n_pv - ql)
+                        mask = (torch.arange(m)[None, :] <= qlog)[:, None, :].expand(ql, H, m)
+                        o[q0: q0 + ql] = self.model.attention(q[q0: q0 + ql], Kp, Vp, mask)
+                    else:
+                        d = self.dec[slot]
+                        j = int(batch.row_kvi[q0])
+                        Kd = torch.stack(d["k"][l])
+                        Vd = torch.stack(d["v"][l])
+                        K = torch.cat([Kp, Kd])
+                        V = torch.cat([Vp, Vd])
+                        mask = torch.zeros(1, H, K.shape[0], dtype=torch.bool)
+                        mask[:, :, :n_pv] = True
+                        for h in range(H):
+                            mask[0, h, n_pv + d["first"][h]: n_pv + j + 1] = True
+                        o[q0: q0 + 1] = self.model.attention(q[q0: q0 + 1], K, V, mask)
+                return o
+
+            for l in range(c.n_layers):
+                x = self.model.layer(l, x, pos, attend)
+            if batch.n_dec:
+                logits = self.model.final(x[batch.dec_rows.tolist()])
+        # teacher forcing: the next decode input of each slot is the GPU's greedy token
+        for slot, tok in zip(batch.dec_slots.tolist(), gpu_tokens):
+            self.last_token[slot] = int(tok)
+        # post-tick per-head trims (the reference's kept[h] after Engine._exec_decode)
+        for slot, kept in kept_post.items():
+            d = self.dec[slot]
+            end = len(d["k"][0])
+            d["first"] = [max(f, end - kk) for f, kk in zip(d["first"], kept)]
+        ft = None
+        if batch.ft_pairs:
+            pairs = [(p.rid, p.prompt, p.chosen, p.rejected) for p in batch.ft_pairs]
+            losses, margins, grads = self.ex.dpo_step(pairs)
+            self.ex.adamw(grads)
+            ft = (losses, margins, grads)
+        return logits, ft

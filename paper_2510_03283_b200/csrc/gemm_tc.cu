@@ -170,6 +170,9 @@ __global__ void __launch_bounds__(256, 1)
       const int row = m_blk * kBM + quarter * 32 + lane;
       const bool row_ok = row < p.M;
       const bool add_bias = ep.bias != nullptr && split == 0;
+      // deterministic split-K: split s writes its own fp32 slab, reduced later in fixed order
+      void* const ep_out = ep.split_stride ? (void*)(reinterpret_cast<float*>(ep.out) + (size_t)split * ep.split_stride)
+                                           : ep.out;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         const bool full = (col0 + 32 <= p.N) && ((ep.ldo & 7) == 0);
         if (ep.mode == EPI_BF16) {
-          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ep.out) + (size_t)row * ep.ldo + col0;
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ep_out) + (size_t)row * ep.ldo + col0;
           if (full) {
 #pragma unroll
             for (int j = 0; j < 32; j += 8) {
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < 32 && col0 + j < p.N; ++j) out[j] = __float2bfloat16(v[j]);
           }
         } else if (ep.mode == EPI_F32) {
-          float* out = reinterpret_cast<float*>(ep.out) + (size_t)row * ep.ldo + col0;
+          float* out = reinterpret_cast<float*>(ep_out) + (size_t)row * ep.ldo + col0;
           if (full) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -241,13 +244,23 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-// split-K finalize: ws fp32 [M,N] -> bf16 out (bias already added by split 0)
-__global__ void gemm_finalize_bf16(const float* __restrict__ ws, int M, int N, __nv_bfloat16* __restrict__ out,
-                                   int ldo) {
+// split-K finalize: out (op)= sum_s ws[s][M][N] in fixed split order (deterministic, no atomics).
+// mode: EPI_BF16 -> bf16 store, EPI_F32 -> fp32 store, EPI_F32_ADD -> fp32 +=
+__global__ void gemm_finalize(const float* __restrict__ ws, int splits, int M, int N, void* __restrict__ out, int ldo,
+                              int mode) {
   const size_t total = (size_t)M * N;
+  const size_t slab = total;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const size_t r = i / N, c = i % N;
-    out[r * ldo + c] = __float2bfloat16(ws[i]);
+    float v = 0.f;
+    for (int sp = 0; sp < splits; ++sp) v += ws[sp * slab + i];
+    if (mode == EPI_BF16) {
+      reinterpret_cast<__nv_bfloat16*>(out)[r * ldo + c] = __float2bfloat16(v);
+    } else if (mode == EPI_F32) {
+      reinterpret_cast<float*>(out)[r * ldo + c] = v;
+    } else {
+      reinterpret_cast<float*>(out)[r * ldo + c] += v;
+    }
   }
 }
 
@@ -337,24 +350,23 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   ep.bias = reinterpret_cast<const __nv_bfloat16*>(g->bias);
   ep.alpha = g->alpha == 0.f ? 1.f : g->alpha;
   ep.mode = g->mode;
+  ep.split_stride = 0;
   bool need_finalize = false;
-  if (splits > 1) {
-    if (g->mode == EPI_F32_ADD || g->mode == EPI_F32_ATOMIC) {
-      ep.mode = EPI_F32_ATOMIC;  // partial sums accumulate straight into the destination
-    } else if (g->mode == EPI_F32) {
-      // zero the rows of the destination then accumulate
-      cudaMemset2DAsync(g->out, (size_t)g->ldo * 4, 0, (size_t)g->N * 4, g->M, stream);
-      ep.mode = EPI_F32_ATOMIC;
-    } else {  // bf16 output: fp32 workspace + finalize
-      if (!g->workspace || g->workspace_bytes < (size_t)g->M * g->N * 4) {
-        splits = 1;
-      } else {
-        cudaMemsetAsync(g->workspace, 0, (size_t)g->M * g->N * 4, stream);
-        ep.out = g->workspace;
-        ep.ldo = g->N;
-        ep.mode = EPI_F32_ATOMIC;
-        need_finalize = true;
-      }
+  if (splits > 1 && g->mode != EPI_F32_ATOMIC) {
+    // keep the per-split slabs inside the caller's workspace
+    const size_t slab = (size_t)g->M * g->N;
+    const size_t fit = g->workspace ? g->workspace_bytes / (slab * 4) : 0;
+    if ((size_t)splits > fit) splits = (int)fit;
+    if (splits > 1) {
+      const int kbp = (kb_total + splits - 1) / splits;
+      splits = (kb_total + kbp - 1) / kbp;  // the splits the kernel will actually run
+      ep.out = g->workspace;
+      ep.ldo = g->N;
+      ep.mode = EPI_F32;
+      ep.split_stride = slab;
+      need_finalize = true;
+    } else {
+      splits = 1;
     }
   }
   int rc;
@@ -366,8 +378,8 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     rc = dispatch_major<64>(ctx, g, splits, stream, ep);
   if (rc) return rc;
   if (need_finalize) {
-    gemm_finalize_bf16<<<ctx->num_sms * 4, 256, 0, stream>>>(reinterpret_cast<const float*>(g->workspace), g->M, g->N,
-                                                             reinterpret_cast<__nv_bfloat16*>(g->out), g->ldo);
+    gemm_finalize<<<ctx->num_sms * 4, 256, 0, stream>>>(reinterpret_cast<const float*>(g->workspace), splits, g->M,
+                                                        g->N, g->out, g->ldo, g->mode);
     ctx->launches++;
   }
   return mace_check_launch(ctx, "gemm");

@@ -21,6 +21,7 @@ struct GemmEpilogue {
   int mode;
   const __nv_bfloat16* bias;
   float alpha;
+  size_t split_stride;  // != 0: split s writes out + s * split_stride (fp32 slabs, deterministic split-K)
 };
 
 struct MaceCtx {

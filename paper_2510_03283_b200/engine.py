@@ -164,6 +164,7 @@ class GpuEngine(Engine):
             rkvi.append(k0)
             n_dec += 1
         ft0 = len(toks)
+        n_tc_inference = len(tc_items)
         pairs: list[FtPair] = []
         logit_rows, targets, pair_rows, row_ps = [], [], [], []
         ft_seqs, ft_tc, ft_rseq, bwd = [], [], [], []
@@ -220,6 +221,7 @@ class GpuEngine(Engine):
             ft_targets=arr(targets), pair_rows=arr(pair_rows, (4,)), row_ps=arr(row_ps),
             ft_seqs=arr(ft_seqs, (8,)), ft_tc_items=arr(ft_tc, (4,)), ft_row_seq=arr(ft_rseq),
             bwd_items=arr(bwd, (4,)), n_prefill_tokens=n_pre, n_decode_tokens=n_dec, n_ft_tokens=n_ft,
+            meta={"n_tc_inference": n_tc_inference},
         )
 
     # ------------------------------------------------------------------ the override point
@@ -265,11 +267,18 @@ class GpuEngine(Engine):
             self.d2h_bytes += len(fts) * 8
         self.tick_tokens.append(batch.total_tokens)
         self.tick_device_ms.append((ev0, ev1))
-        if self.record:
-            self.records.append(dict(tick=self.tick_index - 1, batch=batch, out=out,
-                                     decode_ids=[r.id for r in decodes],
-                                     kept_post={r.id: list(self.state[r.id].kept) for r in decodes if self.pruning},
-                                     ft_ids=[r.id for r in fts]))
+        if self.record:  # host copies for the oracle replay (tests only; synchronizes)
+            torch.cuda.current_stream().synchronize()
+            rec = dict(tick=self.tick_index - 1, batch=batch,
+                       kept_post={self.slot_of[r.id]: list(self.state[r.id].kept) for r in live_dec if self.pruning},
+                       dec_tokens=None if out.dec_tokens is None else out.dec_tokens.cpu().numpy().copy(),
+                       dec_logits=None if out.dec_tokens is None else m.dec_logits[: batch.n_dec].cpu().clone())
+            if fts:
+                rec.update(ft_loss=out.ft_loss.cpu().numpy().copy(), ft_margin=out.ft_margin.cpu().numpy().copy(),
+                           ft_lp=out.ft_lp.cpu().numpy().copy(), ref_lp=out.ref_lp.cpu().numpy().copy(),
+                           grad={n: t.cpu().clone() for n, t in m.gview.items()},
+                           master=m.master.cpu().clone(), adam_m=m.m.cpu().clone(), adam_v=m.v.cpu().clone())
+            self.records.append(rec)
 
     def _exec_prefill(self, req):  # engine.py:444 — check our plan against the reference's charge
         if self.trie is not None and self.state[req.id].leaf is not None:

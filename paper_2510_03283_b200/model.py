@@ -148,6 +148,9 @@ class HybridModel:
                 )
             # ref-pass + backward scratch (FT rows only)
             self.rx = torch.empty(cap, c.d_model, **f32)
+            self.rx2 = torch.empty(cap, c.d_model, **f32)
+            self.x_lmin = torch.empty(cap, c.d_model, **f32)
+            self.rlse = torch.empty(cap, c.n_heads, **f32)
             self.rh = torch.empty(cap, c.d_model, **bf)
             self.rqkv = torch.empty(cap, c.qkv_dim, **bf)
             self.ro = torch.empty(cap, c.n_heads * c.head_dim, **bf)
@@ -284,12 +287,24 @@ class HybridModel:
                                self.w["embed"].data_ptr(), _p(self.w.get("pos_embed")), T, c.d_model,
                                self.x.data_ptr(), s), "embed")
         has_ft = n_ft > 0 and len(batch.ft_pairs) > 0
+        n_tc_all = 0 if v["tc_items"] is None else v["tc_items"].shape[0]
+        n_tc_inf = int(batch.meta.get("n_tc_inference", n_tc_all))
         for l in range(c.n_layers):
-            save = self.sav[l] if (has_ft and l in self.sel_layers) else None
+            # FT rows ride in the shared ragged batch below the lowest selected layer; from there on they
+            # run as their own sub-batch (policy with saved activations + the pi_ref pass) so the two
+            # log-prob paths are kernel-for-kernel identical (margin exactly 0 while pi_theta = pi_ref)
+            top = has_ft and l >= self.l_min
+            T_l = ft0 if top else T
+            if has_ft and l == self.l_min:
+                self.x_lmin[:n_ft].copy_(self.x[ft0:T])
+            if T_l == 0:
+                continue
+            tci = v["tc_items"][:n_tc_inf] if top else v["tc_items"]
+            if tci is not None and tci.shape[0] == 0:
+                tci = None
             hn = self.hn if l == c.n_layers - 1 else None
-            self._layer(l, self.w, T, self.x, self.h, self.qkv, self.o, self.u, self.a, v["seqs"], v["tc_items"],
-                        v["dec_items"], v["row_seq"], v["pos"], v["row_kvi"], paged=True,
-                        lse=self.lse if save is not None else None, hn=hn, save=save, ft0=ft0)
+            self._layer(l, self.w, T_l, self.x, self.h, self.qkv, self.o, self.u, self.a, v["seqs"], tci,
+                        v["dec_items"], v["row_seq"], v["pos"], v["row_kvi"], paged=True, hn=hn)
         # ---- decode rows: final norm on gathered rows -> lm_head -> greedy token
         if n_dec:
             self._norm(self.x, c.d_model, v["dec_rows"], n_dec, "final_norm.w", self.w, self.dec_h, c.d_model)
@@ -342,26 +357,30 @@ class HybridModel:
         loss = torch.empty(P, **f32)
         margin = torch.empty(P, **f32)
         coef = torch.empty(P, 2, **f32)
-        logit_rows = v["ft_logit_rows"]
-        local_rows = logit_rows - ft0
-        # ---- pi_ref log-probs (once per pair): top layers with frozen weights from the shared l_min input
+        local_rows = v["ft_logit_rows"] - ft0
+        ft_pos = v["pos"][ft0:T]
+
+        def sub_pass(W, x, save: bool):
+            x[:n].copy_(self.x_lmin[:n])
+            for l in self.sel_layers:
+                self._layer(l, W, n, x, self.rh, self.rqkv, self.ro, self.ru, self.ra, v["ft_seqs"], v["ft_tc_items"],
+                            None, v["ft_row_seq"], ft_pos, None, paged=False, lse=self.rlse if save else None,
+                            save=self.sav[l] if save else None, ft0=0)
+            self._lm_rows(x, local_rows, R, W, self.ft_h, self.ft_logits)
+
+        # ---- pi_ref log-probs (once per pair): selected layers with the frozen weights from the shared input
         if any(p.ref_lp is None for p in batch.ft_pairs):
             Wref = dict(self.w)
             Wref.update(self.ref_w)
-            self.rx[:n].copy_(self.sav[self.l_min]["x_in"][:n])
-            ft_pos = v["pos"][ft0:T]
-            for l in self.sel_layers:
-                self._layer(l, Wref, n, self.rx, self.rh, self.rqkv, self.ro, self.ru, self.ra, v["ft_seqs"],
-                            v["ft_tc_items"], None, v["ft_row_seq"], ft_pos, None, paged=False)
-            self._lm_rows(self.rx, local_rows, R, Wref, self.ft_h, self.ft_logits)
+            sub_pass(Wref, self.rx2, save=False)
             self._chk(L.mace_dpo_fused(self.ctx.h, self.ft_logits.data_ptr(), R, c.vocab, c.vocab,
                                        v["ft_targets"].data_ptr(), v["pair_rows"].data_ptr(), P, v["row_ps"].data_ptr(),
                                        None, 0.0, self.row_lse.data_ptr(), self.row_lp.data_ptr(), ref_lp.data_ptr(),
                                        None, None, None, None, 0, s), "dpo_ref")
         else:
             ref_lp.copy_(torch.tensor([p.ref_lp for p in batch.ft_pairs], dtype=torch.float32), non_blocking=True)
-        # ---- policy log-probs, DPO loss and dlogits
-        self._lm_rows(self.x, logit_rows, R, self.w, self.ft_h, self.ft_logits)
+        # ---- policy log-probs (saving activations), DPO loss and dlogits
+        sub_pass(self.w, self.rx, save=True)
         self._chk(L.mace_dpo_fused(self.ctx.h, self.ft_logits.data_ptr(), R, c.vocab, c.vocab,
                                    v["ft_targets"].data_ptr(), v["pair_rows"].data_ptr(), P, v["row_ps"].data_ptr(),
                                    ref_lp.data_ptr(), self.tcfg.dpo_beta, self.row_lse.data_ptr(),
@@ -372,8 +391,7 @@ class HybridModel:
         self.grad.zero_()
         self._gemm(self.dlogits[:R], self.w["embed"], self.dh[:R], "f32", b_mn=True)
         self.dx[:n].zero_()
-        self._norm_bwd(self.x, logit_rows, self.dh, R, "final_norm", self.dx, local_rows)
-        ft_pos = v["pos"][ft0:T]
+        self._norm_bwd(self.rx, local_rows, self.dh, R, "final_norm", self.dx, local_rows)
         for l in reversed(self.sel_layers):
             self._layer_bwd(l, n, v, ft_pos)
         # ---- exchange + masked AdamW

@@ -68,7 +68,7 @@ def test_gemm_splitk_bf16_workspace(ctx):
     M, N, K = 64, 512, 4096
     a = torch.randn(M, K, device="cuda").bfloat16()
     b = torch.randn(N, K, device="cuda").bfloat16()
-    ws = torch.empty(M * N, device="cuda")
+    ws = torch.empty(8 * M * N, device="cuda")
     y = ops.gemm(ctx, a, b, mode="bf16", split_k=8, workspace=ws)
     ref = a.float() @ b.float().t()
     assert torch.allclose(y.float(), ref, atol=0.5, rtol=1e-2)
