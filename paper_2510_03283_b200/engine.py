@@ -64,9 +64,15 @@ def measured_profile(profile: CostProfile) -> _MeasuredProfile:
     return p
 
 
+class TickBudgetReached(Exception):
+    """Raised at the END of a tick (after all its effects) to pause Engine.run(); calling run() again
+    resumes exactly where it stopped (the loop keeps all state on self, engine.py:680-732)."""
+
+
 class GpuEngine(Engine):
     def __init__(self, trace, profile, sched_cfg, priority_params, cache_cfg, env, engine_cfg, metrics_horizon=None,
-                 *, model: HybridModel, mode: str = "P", seed: int | None = None, record: bool = False):
+                 *, model: HybridModel, mode: str = "P", seed: int | None = None, record: bool = False,
+                 lockstep=None):
         if mode not in ("P", "M"):
             raise ValueError("mode must be 'P' (parity clock) or 'M' (measured clock)")
         if mode == "M":
@@ -95,6 +101,10 @@ class GpuEngine(Engine):
         self.d2h_bytes = 0
         self._planned_shared: dict[int, int] = {}
         self._dec_out: list = []
+        self.lockstep = lockstep
+        self.ticks_done = 0
+        self._budget_end: int | None = None
+        self.keep_outputs = True
 
     # ------------------------------------------------------------------ helpers
     def _slot(self, rid: int) -> int:
@@ -239,7 +249,8 @@ class GpuEngine(Engine):
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
-        out = m.step(batch)
+        ft_global = self.lockstep.any_ft(bool(fts)) if self.lockstep is not None else None
+        out = m.step(batch, ft_global=ft_global)
         ev1.record()
         self.h2d_bytes += m.h2d_bytes
         if self.mode == "M":
@@ -253,7 +264,7 @@ class GpuEngine(Engine):
             slots = np.array([self.slot_of[r.id] for r in live_dec], np.int32)
             kept = np.array([self.state[r.id].kept for r in live_dec], np.int32)
             m.apply_trim(slots, kept)
-        if out.dec_tokens is not None:
+        if out.dec_tokens is not None and self.keep_outputs:
             host = torch.empty(batch.n_dec, dtype=torch.int32, pin_memory=True)
             host.copy_(out.dec_tokens, non_blocking=True)
             self.d2h_bytes += batch.n_dec * 4
@@ -267,6 +278,7 @@ class GpuEngine(Engine):
             self.d2h_bytes += len(fts) * 8
         self.tick_tokens.append(batch.total_tokens)
         self.tick_device_ms.append((ev0, ev1))
+        self.last_batch = batch
         if self.record:  # host copies for the oracle replay (tests only; synchronizes)
             torch.cuda.current_stream().synchronize()
             rec = dict(tick=self.tick_index - 1, batch=batch,
@@ -279,6 +291,24 @@ class GpuEngine(Engine):
                            grad={n: t.cpu().clone() for n, t in m.gview.items()},
                            master=m.master.cpu().clone(), adam_m=m.m.cpu().clone(), adam_v=m.v.cpu().clone())
             self.records.append(rec)
+        self._after_tick()
+
+    def _after_tick(self) -> None:
+        self.ticks_done += 1
+        if self._budget_end is not None and self.ticks_done >= self._budget_end:
+            raise TickBudgetReached()
+
+    def run_ticks(self, n: int) -> int:
+        """Advance the reference loop by exactly n executed ticks (fewer if the trace drains)."""
+        start = self.ticks_done
+        self._budget_end = start + n
+        try:
+            self.run()
+        except TickBudgetReached:
+            pass
+        finally:
+            self._budget_end = None
+        return self.ticks_done - start
 
     def _exec_prefill(self, req):  # engine.py:444 — check our plan against the reference's charge
         if self.trie is not None and self.state[req.id].leaf is not None:

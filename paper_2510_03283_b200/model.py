@@ -117,7 +117,9 @@ class HybridModel:
         self._R_cap = 0
         self._ndec_cap = 0
         self.ws = torch.empty(16 << 20, dtype=torch.float32, device=self.dev)  # 64 MB split-K / reduction scratch
-        self.pinned = torch.empty(1 << 16, dtype=torch.int32, pin_memory=True)
+        self.tape: list | None = None   # when a list: every device-side call is appended (bench replay)
+        self.instrument: list | None = None  # when a list: (ev0, ev1, bytes) per decode-attention launch
+        self._attn_bytes = 0
         self.idx = torch.empty(1 << 16, dtype=torch.int32, device=self.dev)
 
     # ------------------------------------------------------------------ buffers
@@ -170,7 +172,8 @@ class HybridModel:
             cap = max(R, int(self._R_cap * 1.5), 64)
             self.ft_h = torch.empty(cap, c.d_model, **bf)
             self.ft_logits = torch.empty(cap, c.vocab, **f32)
-            self.dlogits = torch.empty(cap, c.vocab, **bf)
+            self.vpad = (c.vocab + 7) // 8 * 8  # 16-byte aligned rows for the TMA operand of dX = dlogits . E
+            self.dlogits = torch.empty(cap, self.vpad, **bf)
             self.dh = torch.empty(cap, c.d_model, **f32)
             self.row_lse = torch.empty(cap, **f32)
             self.row_lp = torch.empty(cap, **f32)
@@ -182,14 +185,27 @@ class HybridModel:
             self.dec_tok = torch.empty(cap, dtype=torch.int32, device=dev)
             self._ndec_cap = cap
 
+    def replay(self, tape) -> None:
+        """Re-issue a recorded sequence of device calls (bench: device-only throughput)."""
+        for op in tape:
+            if op[0] == "step":
+                self.step(op[1], ft_global=op[2])
+            elif op[0] == "trim":
+                self.apply_trim(op[1], op[2])
+            else:
+                self.release_slots(op[1])
+
     def _upload(self, batch: TickBatch) -> dict[str, torch.Tensor]:
-        buf, layout = batch.packed()
+        if getattr(batch, "_packed", None) is None:
+            batch._packed = batch.packed()
+        buf, layout = batch._packed
         n = buf.size
-        if n > self.pinned.numel():
-            self.pinned = torch.empty(int(n * 1.5), dtype=torch.int32, pin_memory=True)
+        if n > self.idx.numel():
             self.idx = torch.empty(int(n * 1.5), dtype=torch.int32, device=self.dev)
-        self.pinned[:n].numpy()[:] = buf
-        self.idx[:n].copy_(self.pinned[:n], non_blocking=True)
+        # a fresh block from torch's caching pinned allocator per tick: the allocator records the copy's
+        # stream event, so the host can run ticks ahead without overwriting an in-flight H2D source
+        host = torch.from_numpy(buf).pin_memory()
+        self.idx[:n].copy_(host, non_blocking=True)
         self.h2d_bytes = n * 4
         views = {}
         for name, (off, shape) in layout.items():
@@ -232,8 +248,19 @@ class HybridModel:
                                           row_pos.data_ptr(), row_seq.data_ptr(), _p(row_kvi), seqs.data_ptr(),
                                           self.cos_t.data_ptr(), self.sin_t.data_ptr(), int(c.family == "llama"),
                                           C.byref(lay), _p(kp), _p(vp), self._s), "rope_kv")
-        ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, tc_items, dec_items, lay,
-                     kp, vp, o[:T], lse=lse, head_norm=hn)
+        if self.instrument is not None and dec_items is not None:
+            if tc_items is not None:
+                ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, tc_items, None, lay,
+                             kp, vp, o[:T], lse=lse, head_norm=hn)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, None, dec_items, lay,
+                         kp, vp, o[:T], lse=lse, head_norm=hn)
+            e1.record()
+            self.instrument.append((e0, e1, self._attn_bytes))
+        else:
+            ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, tc_items, dec_items, lay,
+                         kp, vp, o[:T], lse=lse, head_norm=hn)
         if save is not None:
             n = T - ft0
             save["h1"][:n].copy_(h[ft0:T])
@@ -256,8 +283,14 @@ class HybridModel:
 
     # ------------------------------------------------------------------ tick
     @torch.no_grad()
-    def step(self, batch: TickBatch, trim: tuple[np.ndarray, np.ndarray] | None = None) -> StepOutputs:
-        """Run one hybrid tick on the device (asynchronous; outputs are device tensors)."""
+    def step(self, batch: TickBatch, trim: tuple[np.ndarray, np.ndarray] | None = None,
+             ft_global: bool | None = None) -> StepOutputs:
+        """Run one hybrid tick on the device (asynchronous; outputs are device tensors).
+
+        ``ft_global``: whether ANY replica has fine-tune rows this tick (lockstep multi-GPU); defaults to
+        this replica's own rows."""
+        if self.tape is not None:
+            self.tape.append(("step", batch, ft_global))
         c = self.cfg
         T, ft0 = batch.T, batch.ft0
         n_ft = T - ft0
@@ -279,8 +312,12 @@ class HybridModel:
         if n_dec:
             self._chk(L.mace_kv_decode_alloc(self.ctx.h, C.byref(self.kv), v["dec_slots"].data_ptr(), n_dec, s),
                       "decode_alloc")
+        if self.instrument is not None and n_dec:
+            self._attn_bytes = self.decode_attn_bytes(batch)
         out = StepOutputs(None, None, None, None, None, None)
         if T == 0:
+            if ft_global:
+                self.apply_update(False)
             return out
         # ---- forward through all layers (one ragged batch)
         self._chk(L.mace_embed(self.ctx.h, v["tokens"].data_ptr(), v["pos"].data_ptr(), self.last_token.data_ptr(),
@@ -318,13 +355,28 @@ class HybridModel:
             self.apply_trim(*trim)
         if has_ft:
             self._ft_step(batch, v, out)
+        if has_ft or ft_global:
+            self.apply_update(has_ft)
         return out
+
+    def decode_attn_bytes(self, batch: TickBatch) -> int:
+        """Algorithmic bytes of ONE decode-attention launch (one layer) of this tick: every visible K and
+        V row of every (decode sequence, kv head) read once + q rows read + o rows written (syncs)."""
+        c = self.cfg
+        slots = torch.from_numpy(batch.dec_slots.astype(np.int64)).to(self.dev)
+        de = self.dec_end[slots].cpu().numpy()
+        df = self.dec_first[slots].cpu().numpy()
+        n_pv = batch.seqs[batch.seqs[:, 0] == 1][:, 4]
+        tokens = int((n_pv[:, None] + (de[:, None] - df)).sum())
+        return tokens * c.head_dim * 2 * 2 + batch.n_dec * c.n_heads * c.head_dim * 2 * 2
 
     def apply_trim(self, slots: np.ndarray, kept: np.ndarray) -> None:
         """Post-tick per-head prune trim (engine.py:506-529 decisions) -> page compaction on device."""
         n = slots.shape[0]
         if n == 0:
             return
+        if self.tape is not None:
+            self.tape.append(("trim", slots.copy(), kept.copy()))
         t_s = torch.from_numpy(np.ascontiguousarray(slots, np.int32)).pin_memory().to(self.dev, non_blocking=True)
         t_k = torch.from_numpy(np.ascontiguousarray(kept, np.int32).reshape(-1)).pin_memory().to(self.dev, non_blocking=True)
         self._keep = (t_s, t_k)  # keep alive until the stream consumes them
@@ -334,6 +386,8 @@ class HybridModel:
     def release_slots(self, slots: list[int]) -> None:
         if not slots:
             return
+        if self.tape is not None:
+            self.tape.append(("release", list(slots)))
         t_s = torch.tensor(slots, dtype=torch.int32).pin_memory().to(self.dev, non_blocking=True)
         self._keep_rel = t_s
         self._chk(self.ctx.L.mace_kv_release(self.ctx.h, C.byref(self.kv), t_s.data_ptr(), len(slots), self._s),
@@ -385,16 +439,23 @@ class HybridModel:
                                    v["ft_targets"].data_ptr(), v["pair_rows"].data_ptr(), P, v["row_ps"].data_ptr(),
                                    ref_lp.data_ptr(), self.tcfg.dpo_beta, self.row_lse.data_ptr(),
                                    self.row_lp.data_ptr(), lp.data_ptr(), loss.data_ptr(), margin.data_ptr(),
-                                   coef.data_ptr(), self.dlogits.data_ptr(), c.vocab, s), "dpo")
+                                   coef.data_ptr(), self.dlogits.data_ptr(), self.vpad, s), "dpo")
         out.ft_loss, out.ft_margin, out.ft_lp, out.ref_lp = loss, margin, lp, ref_lp
         # ---- backward: lm_head (tied, frozen) -> final norm -> selected layers top-down
         self.grad.zero_()
-        self._gemm(self.dlogits[:R], self.w["embed"], self.dh[:R], "f32", b_mn=True)
+        self._gemm(self.dlogits[:R, : c.vocab], self.w["embed"], self.dh[:R], "f32", b_mn=True)
         self.dx[:n].zero_()
         self._norm_bwd(self.rx, local_rows, self.dh, R, "final_norm", self.dx, local_rows)
         for l in reversed(self.sel_layers):
             self._layer_bwd(l, n, v, ft_pos)
-        # ---- exchange + masked AdamW
+
+    def apply_update(self, local_ft: bool) -> None:
+        """Gradient exchange (NCCL all-reduce over the request-stream replicas) and the
+        masked AdamW. A replica without FT rows this tick contributes zeros and applies the same
+        update, so every replica keeps bit-identical weights."""
+        L, s = self.ctx.L, self._s
+        if not local_ft:
+            self.grad.zero_()
         if self.pg is not None:
             torch.distributed.all_reduce(self.grad, group=self.pg)
         self.adam_step += 1
