@@ -105,6 +105,7 @@ class GpuEngine(Engine):
         self.ticks_done = 0
         self._budget_end: int | None = None
         self.keep_outputs = True
+        self.time_ticks = False
 
     # ------------------------------------------------------------------ helpers
     def _slot(self, rid: int) -> int:
@@ -131,6 +132,7 @@ class GpuEngine(Engine):
         ptab_slots, ptab_rows, copies = [], [], []
         n_pre = n_dec = n_ft = 0
         pending_cached: set[int] = set()
+        fresh: set[int] = set()
         self._planned_shared = {}
 
         def add_tc(si, q_len):
@@ -142,23 +144,23 @@ class GpuEngine(Engine):
             rs = self.state[req.id]
             slot = self._slot(req.id)
             P = len(req.prompt_tokens)
-            shared, table, cps = plan_prefill_pages(self.trie, self.pool, rs.leaf, P, pending_cached)
+            shared, start, table, cps = plan_prefill_pages(self.trie, self.pool, rs.leaf, P, pending_cached, fresh)
             self._planned_shared[req.id] = shared
             self.table_of[req.id] = table
             ptab_slots.append(slot)
             ptab_rows.append(table)
             copies += [(s_, d_, n_, 0) for s_, d_, n_ in cps]
-            q = P - shared
+            q = P - start
             if q <= 0:
                 continue
             si = len(seqs)
             seqs.append((KIND_PREFILL, len(toks), q, slot, P, P, -1, 0))
             add_tc(si, q)
-            toks += req.prompt_tokens[shared:]
-            pos += list(range(shared, P))
+            toks += req.prompt_tokens[start:]
+            pos += list(range(start, P))
             rseq += [si] * q
-            rkvi += list(range(shared, P))
-            n_pre += q
+            rkvi += list(range(start, P))
+            n_pre += P - shared  # tokens the reference charges (engine.py:449-450)
         for j, req in enumerate(decodes):
             slot = self.slot_of[req.id]
             P = len(req.prompt_tokens)
@@ -246,12 +248,15 @@ class GpuEngine(Engine):
                 prefills = dfs_order(self.trie, pending)
         batch = self.build_batch(prefills, decodes, fts)
         m = self.model
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record()
+        timed = self.mode == "M" or self.time_ticks
+        if timed:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
         ft_global = self.lockstep.any_ft(bool(fts)) if self.lockstep is not None else None
         out = m.step(batch, ft_global=ft_global)
-        ev1.record()
+        if timed:
+            ev1.record()
         self.h2d_bytes += m.h2d_bytes
         if self.mode == "M":
             ev1.synchronize()
@@ -277,7 +282,8 @@ class GpuEngine(Engine):
             self._pending_ref.append((host, ev, [r.id for r in fts]))
             self.d2h_bytes += len(fts) * 8
         self.tick_tokens.append(batch.total_tokens)
-        self.tick_device_ms.append((ev0, ev1))
+        if timed:
+            self.tick_device_ms.append((ev0, ev1))
         self.last_batch = batch
         if self.record:  # host copies for the oracle replay (tests only; synchronizes)
             torch.cuda.current_stream().synchronize()

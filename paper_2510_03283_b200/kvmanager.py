@@ -119,20 +119,27 @@ class GpuPrefixTrie(PrefixTrie):
 
 
 def plan_prefill_pages(trie: GpuPrefixTrie | None, pool: GroupPool, leaf: TrieNode | None, prompt_len: int,
-                       pending_cached: set[int]) -> tuple[int, list[int], list[tuple[int, int, int]]]:
+                       pending_cached: set[int], fresh: set[int] | None = None
+                       ) -> tuple[int, int, list[int], list[tuple[int, int, int]]]:
     """Decide the device page table of one prefill (in trie-DFS order within the tick).
 
-    Returns (shared, table, copies): ``shared`` is exactly what Engine._exec_prefill will charge as
-    cached (cache.py:164-184, counting nodes an earlier prefill of the same tick will cache), ``table``
-    the group id of every logical prompt page, ``copies`` the copy-on-diverge list (src, dst, rows).
+    Returns (shared, start, table, copies): ``shared`` is exactly what Engine._exec_prefill will charge
+    as cached (cache.py:164-184, counting nodes an earlier prefill of the same tick will cache);
+    ``start`` is the first position the device computes (= shared, or the page boundary below it when
+    the diverging page is itself being written by an earlier prefill of the same tick, which a
+    pre-tick copy could not see); ``table`` the group id of every logical prompt page; ``copies`` the
+    copy-on-diverge list (src, dst, rows). ``fresh`` collects the groups written this tick.
     The request holds one ref on every table entry. Uncached path nodes get their future pages
     registered as pending for mark_executed.
     """
     n_pages = (prompt_len + PAGE - 1) // PAGE
     table = [-1] * n_pages
     copies: list[tuple[int, int, int]] = []
+    fresh = set() if fresh is None else fresh
     if trie is None or leaf is None:
-        return 0, [pool.alloc() for _ in range(n_pages)], copies
+        table = [pool.alloc() for _ in range(n_pages)]
+        fresh.update(table)
+        return 0, 0, table, copies
     path = leaf.path_nodes()
     shared = 0
     src_pages: dict[int, int] = {}
@@ -150,15 +157,20 @@ def plan_prefill_pages(trie: GpuPrefixTrie | None, pool: GroupPool, leaf: TrieNo
         for i in range(n_pages):
             table[i] = src_pages[i]
             pool.incref(table[i])
-        return shared, table, copies
+        return shared, shared, table, copies
     full = shared // PAGE
     for i in range(full):
         table[i] = src_pages[i]
         pool.incref(table[i])
     for i in range(full, n_pages):
         table[i] = pool.alloc()
+    fresh.update(table[full:])
+    start = shared
     if shared % PAGE and full < n_pages:
-        copies.append((src_pages[full], table[full], shared % PAGE))
+        if src_pages[full] in fresh:
+            start = full * PAGE   # same-tick source: recompute the partial page instead of copying
+        else:
+            copies.append((src_pages[full], table[full], shared % PAGE))
     # nodes this prefill caches (mark_executed) adopt the request's pages
     a = shared
     for n in path[k:]:
@@ -167,4 +179,4 @@ def plan_prefill_pages(trie: GpuPrefixTrie | None, pool: GroupPool, leaf: TrieNo
             trie.pending[n.node_id] = {i: table[i] for i in page_range(a, b)}
             pending_cached.add(n.node_id)
         a = b
-    return shared, table, copies
+    return shared, start, table, copies

@@ -14,6 +14,12 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
 
+def pytest_collection_modifyitems(config, items):
+    for item in items:
+        if item.fspath.basename == "diag_ft.py":
+            item.add_marker(pytest.mark.skip)
+
+
 @pytest.fixture(scope="session")
 def ctx():
     import torch
