@@ -119,10 +119,15 @@ int mace_argmax(mace_ctx* ctx, const float* logits, int n, int V, int ld, int* o
 /* ---------------------------------------------------------------- (1) ragged paged attention fwd
  * Prefill and fine-tune sequences run as tcgen05 tiles (128 query rows x one query head; S = QK^T
  * and O = PV on the tensor cores, K/V pages TMA-staged, online softmax in registers); decode
- * sequences run as bandwidth-bound (sequence, kv-head) items streaming K/V pages with
- * cp.async.bulk.  Work lists are built per tick by the host:
+ * sequences run as bandwidth-bound warp items streaming K/V page pairs with cp.async.bulk.
+ * Work lists are built per tick by the host:
  *   tc_items  int4 [n_tc]  = (seq, q_head, q_block, 0)
- *   dec_items int2 [n_dec] = (seq, kv_head)                                                       */
+ *   dec_items int4 [n_dec] = (seq, kv_head, chunk << 16 | n_chunks, partial_base), ordered longest
+ *             first; warps take items dynamically from the monotonic 64-bit ticket counter dec_work
+ *             (never reset; the ctx remembers where each counter's next launch starts). Multi-chunk
+ *             partials go to
+ *             dec_workspace[partial_base + chunk] ((2G + G*hd) fp32 each) and are merged in chunk
+ *             order; dec_counters is a zero-initialised int [slots * Hkv] left zeroed.            */
 typedef struct MaceAttnArgs {
   void* qkv; int T; int Hq; int Hkv; int hd; /* packed [T, (Hq+2Hkv)*hd] bf16 after RoPE */
   const MaceSeq* seqs;
@@ -134,6 +139,9 @@ typedef struct MaceAttnArgs {
   float* lse;         /* [T, Hq] natural-log LSE (tc rows) or NULL */
   float* head_norm;   /* [T, Hq] ||o_{t,h}||_2 of decode rows or NULL */
   float scale;        /* softmax scale, 0 -> 1/sqrt(hd) */
+  void* dec_workspace; size_t dec_workspace_bytes;
+  int* dec_counters;
+  unsigned long long* dec_work;  /* zero-initialised ticket counter, owned by the caller, one per ctx */
 } MaceAttnArgs;
 int mace_attn_fwd(mace_ctx* ctx, const MaceAttnArgs* args, void* stream);
 

@@ -35,7 +35,7 @@ class TickBatch:
     row_kvi: np.ndarray         # [T] int32 prompt index (prefill) / decode slot index (decode) / -1 (FT)
     seqs: np.ndarray            # [S, 8] int32 MaceSeq
     tc_items: np.ndarray        # [n, 4] int32 (seq, q_head, q_block, 0)
-    dec_items: np.ndarray       # [n, 2] int32 (seq, kv_head)
+    dec_items: np.ndarray       # [n, 4] int32 (seq, kv_head, chunk, n_chunks)
     dec_slots: np.ndarray       # [n_dec] int32 KV slot of each decode row (alloc + token scatter)
     dec_rows: np.ndarray        # [n_dec] int32 batch row of each decode row
     ptab_slots: np.ndarray      # [u] int32 slots whose prompt page table is (re)written this tick

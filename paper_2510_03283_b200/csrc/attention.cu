@@ -9,11 +9,7 @@
 //    (TMEM lane i) for the online softmax; the P.V partial is folded into registers so the next S tile
 //    overlaps the accumulation. Paged K/V come from the head-major page pools, dense FT K/V straight
 //    from the packed qkv rows.
-//  * decode path (HBM bound): CTA = (decode sequence, kv head); each warp streams its share of
-//    the sequence's pages (prompt pages + the per-head decode window, cache.py:355-362 semantics)
-//    through a private cp.async.bulk ring and keeps an online softmax for the G query heads of the
-//    group (GQA reuse of each K/V byte). Warps are merged in shared memory; the epilogue also emits
-//    the per-head output norms ||a_{t,h}||_2 the pruning statistics consume.
+//  * decode path (HBM bound): attention_decode.cu (warp per (sequence, kv head, chunk) item).
 #include <cmath>
 
 #include "common.cuh"
@@ -261,217 +257,6 @@ __global__ void __launch_bounds__(128) attn_tc_kernel(const __grid_constant__ Tc
 }
 
 // =====================================================================================================
-// decode path
-// =====================================================================================================
-template <int HD, int G>
-struct DecCfg {
-  static constexpr int STAGES = HD >= 128 ? 2 : 3;
-  static constexpr int PAGE = kPageTokens * HD * 2;
-  static constexpr int WARP_RING = STAGES * 2 * PAGE;
-  static constexpr int RING_OFF = 0;
-  static constexpr int Q_OFF = 4 * WARP_RING;                  // fp32 [G][HD]
-  static constexpr int PS_OFF = Q_OFF + G * HD * 4;            // fp32 [4][G][16] probabilities
-  static constexpr int AL_OFF = PS_OFF + 4 * G * 16 * 4;       // fp32 [4][G] alpha
-  static constexpr int CMB_OFF = AL_OFF + 4 * G * 4;           // fp32 [4][G][HD+2] merge buffer
-  static constexpr int BAR_OFF = CMB_OFF + 4 * G * (HD + 2) * 4;
-  static constexpr int SMEM = BAR_OFF + 4 * STAGES * 8 + 16;
-};
-
-template <int HD, int G>
-__global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* __restrict__ qkv, const MaceSeq* __restrict__ seqs,
-                                                          const int2* __restrict__ items, const MaceKvLayout kv,
-                                                          const __nv_bfloat16* __restrict__ k_pool,
-                                                          const __nv_bfloat16* __restrict__ v_pool, int Hq, int Hkv,
-                                                          float scale_log2, __nv_bfloat16* __restrict__ out,
-                                                          float* __restrict__ head_norm) {
-  using C = DecCfg<HD, G>;
-  constexpr int DPL = HD / 32;          // head dims per lane
-  constexpr int ROUNDS = (G + 1) / 2;   // score rounds: 16 tokens x 2 heads per warp pass
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int2 it = items[blockIdx.x];
-  const MaceSeq sq = seqs[it.x];
-  const int h = it.y;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int W = (Hq + 2 * Hkv) * HD;
-  float* qs = reinterpret_cast<float*>(smem + C::Q_OFF);
-  float* ps = reinterpret_cast<float*>(smem + C::PS_OFF) + warp * G * 16;
-  float* al = reinterpret_cast<float*>(smem + C::AL_OFF) + warp * G;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF) + warp * C::STAGES;
-  uint8_t* ring = smem + C::RING_OFF + warp * C::WARP_RING;
-
-  const __nv_bfloat16* qrow = qkv + (size_t)sq.q_start * W + (size_t)h * G * HD;
-  for (int i = tid; i < G * HD; i += 128) qs[i] = __bfloat162float(qrow[i]);
-  if (lane == 0)
-    for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
-  fence_barrier_init();
-  __syncthreads();
-
-  // ---- the sequence's page slots for kv head h
-  const int n_pv = sq.n_pv;
-  const int npp = (n_pv + 15) / 16;
-  const int kvh = sq.slot * Hkv + h;
-  const int d0 = kv.dec_first[kvh], db = kv.dec_base[kvh], de = kv.dec_end[sq.slot];
-  const int r0 = (d0 - db) / 16;
-  const int ndp = de > d0 ? ((de - 1 - db) / 16 - r0 + 1) : 0;
-  const int n_slots = npp + ndp;
-  auto slot_info = [&](int p, int& page, int& lo, int& hi) {
-    if (p < npp) {
-      page = kv.ptab[(size_t)sq.slot * kv.max_prompt_pages + p] * Hkv + h;
-      lo = 0;
-      hi = min(16, n_pv - 16 * p);
-    } else {
-      const int r = r0 + (p - npp);
-      page = kv.dtab[(size_t)kvh * kv.max_dec_pages + r];
-      const int s0 = db + 16 * r;
-      lo = max(0, d0 - s0);
-      hi = min(16, de - s0);
-    }
-  };
-  auto issue = [&](int p, int stage) {
-    int page, lo, hi;
-    slot_info(p, page, lo, hi);
-    uint8_t* dst = ring + stage * 2 * C::PAGE;
-    mbar_arrive_expect_tx(&bars[stage], 2 * C::PAGE);
-    bulk_load(dst, k_pool + (size_t)page * 16 * HD, C::PAGE, &bars[stage]);
-    bulk_load(dst + C::PAGE, v_pool + (size_t)page * 16 * HD, C::PAGE, &bars[stage]);
-  };
-
-  float m_r[ROUNDS], l_r[ROUNDS];
-  float acc[G][DPL];
-#pragma unroll
-  for (int r = 0; r < ROUNDS; ++r) {
-    m_r[r] = -INFINITY;
-    l_r[r] = 0.f;
-  }
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-#pragma unroll
-    for (int d = 0; d < DPL; ++d) acc[g][d] = 0.f;
-
-  if (lane == 0) {
-    int k = 0;
-    for (int p = warp; p < n_slots && k < C::STAGES; p += 4, ++k) issue(p, k);
-  }
-  const int t = lane & 15;
-  int iter = 0;
-  for (int p = warp; p < n_slots; p += 4, ++iter) {
-    const int stage = iter % C::STAGES;
-    mbar_wait(&bars[stage], (iter / C::STAGES) & 1);
-    int page, lo, hi;
-    slot_info(p, page, lo, hi);
-    const __nv_bfloat16* ks = reinterpret_cast<const __nv_bfloat16*>(ring + stage * 2 * C::PAGE);
-    const __nv_bfloat16* vs = ks + 16 * HD;
-    // ---- scores: lane -> (token t, head g = 2r + lane/16)
-#pragma unroll
-    for (int r = 0; r < ROUNDS; ++r) {
-      const int g = 2 * r + (lane >> 4);
-      float s = -INFINITY;
-      if (g < G && t >= lo && t < hi) {
-        float dot = 0.f;
-        const float* qg = qs + g * HD;
-#pragma unroll
-        for (int c = 0; c < HD / 8; ++c) {
-          const int cc = (c + t) % (HD / 8);
-          const uint4 u = *reinterpret_cast<const uint4*>(ks + t * HD + cc * 8);
-          const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(&u);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) dot = fmaf(qg[cc * 8 + e], __bfloat162float(kb[e]), dot);
-        }
-        s = dot * scale_log2;
-      }
-      float mx = s;
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const float m_new = fmaxf(m_r[r], mx);
-      const float pv = (s == -INFINITY) ? 0.f : exp2f(s - m_new);
-      float sum = pv;
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      const float a = (m_r[r] == -INFINITY) ? (m_new == -INFINITY ? 1.f : 0.f) : exp2f(m_r[r] - m_new);
-      l_r[r] = l_r[r] * a + sum;
-      m_r[r] = m_new;
-      if (g < G) {
-        ps[g * 16 + t] = pv;
-        if (t == 0) al[g] = a;
-      }
-    }
-    __syncwarp();
-    // ---- P.V: lane owns DPL head dims for all G heads
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float a = al[g];
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) acc[g][d] *= a;
-    }
-#pragma unroll 4
-    for (int tt = lo; tt < hi; ++tt) {
-      float vv[DPL];
-      if constexpr (DPL == 2) {
-        const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162*>(vs + tt * HD + lane * 2);
-        vv[0] = __bfloat162float(v2.x);
-        vv[1] = __bfloat162float(v2.y);
-      } else {
-#pragma unroll
-        for (int d = 0; d < DPL; ++d) vv[d] = __bfloat162float(vs[tt * HD + lane * DPL + d]);
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float pw = ps[g * 16 + tt];
-#pragma unroll
-        for (int d = 0; d < DPL; ++d) acc[g][d] = fmaf(pw, vv[d], acc[g][d]);
-      }
-    }
-    __syncwarp();
-    if (lane == 0 && p + 4 * C::STAGES < n_slots) issue(p + 4 * C::STAGES, stage);
-  }
-
-  // ---- merge the 4 warps
-  float* cmb = reinterpret_cast<float*>(smem + C::CMB_OFF);
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    float* row = cmb + (warp * G + g) * (HD + 2);
-#pragma unroll
-    for (int d = 0; d < DPL; ++d) row[lane * DPL + d] = acc[g][d];
-  }
-#pragma unroll
-  for (int r = 0; r < ROUNDS; ++r) {
-    const int g = 2 * r + (lane >> 4);
-    if (g < G && t == 0) {
-      float* row = cmb + (warp * G + g) * (HD + 2);
-      row[HD] = m_r[r];
-      row[HD + 1] = l_r[r];
-    }
-  }
-  __syncthreads();
-  const int row_out = sq.q_start;
-  for (int g = warp; g < G; g += 4) {
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, cmb[(w * G + g) * (HD + 2) + HD]);
-    float L = 0.f, sc[4];
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = cmb[(w * G + g) * (HD + 2) + HD];
-      sc[w] = mw == -INFINITY ? 0.f : exp2f(mw - M);
-      L += cmb[(w * G + g) * (HD + 2) + HD + 1] * sc[w];
-    }
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    float nrm = 0.f;
-    __nv_bfloat16* o = out + (size_t)row_out * Hq * HD + (size_t)(h * G + g) * HD;
-    for (int d = lane; d < HD; d += 32) {
-      float v = 0.f;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) v += cmb[(w * G + g) * (HD + 2) + d] * sc[w];
-      v *= inv;
-      o[d] = __float2bfloat16(v);
-      nrm += v * v;
-    }
-    nrm = warp_sum(nrm);
-    if (head_norm && lane == 0) head_norm[(size_t)row_out * Hq + h * G + g] = sqrtf(nrm);
-  }
-}
-
-// =====================================================================================================
 // host
 // =====================================================================================================
 static bool encode_2d(MaceCtx* ctx, CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
@@ -511,32 +296,7 @@ static int launch_tc(MaceCtx* ctx, const MaceAttnArgs* a, float scale_log2, cuda
   return 0;
 }
 
-template <int HD, int G>
-static int launch_dec(MaceCtx* ctx, const MaceAttnArgs* a, float scale_log2, cudaStream_t s) {
-  using C = DecCfg<HD, G>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_decode_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
-  }
-  attn_decode_kernel<HD, G><<<a->n_dec, 128, C::SMEM, s>>>(
-      (const __nv_bfloat16*)a->qkv, a->seqs, reinterpret_cast<const int2*>(a->dec_items), a->kv,
-      (const __nv_bfloat16*)a->k_pool, (const __nv_bfloat16*)a->v_pool, a->Hq, a->Hkv, scale_log2,
-      (__nv_bfloat16*)a->out, a->head_norm);
-  ctx->launches++;
-  return 0;
-}
-
-template <int HD>
-static int dispatch_dec(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStream_t s) {
-  switch (a->Hq / a->Hkv) {
-    case 1: return launch_dec<HD, 1>(ctx, a, sl2, s);
-    case 2: return launch_dec<HD, 2>(ctx, a, sl2, s);
-    case 4: return launch_dec<HD, 4>(ctx, a, sl2, s);
-    case 8: return launch_dec<HD, 8>(ctx, a, sl2, s);
-    default: return mace_fail(ctx, MACE_ERR_UNSUPPORTED, "attn: GQA group must be 1, 2, 4 or 8");
-  }
-}
+int dispatch_decode2(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStream_t s);
 
 }  // namespace mace
 
@@ -560,12 +320,7 @@ extern "C" int mace_attn_fwd(mace_ctx* ctx, const MaceAttnArgs* a, void* stream)
   }
   if (a->n_dec > 0) {
     if (!a->k_pool || !a->v_pool) return mace_fail(ctx, MACE_ERR_ARG, "attn: decode rows need KV pools");
-    switch (a->hd) {
-      case 32: rc = dispatch_dec<32>(ctx, a, sl2, s); break;
-      case 64: rc = dispatch_dec<64>(ctx, a, sl2, s); break;
-      case 128: rc = dispatch_dec<128>(ctx, a, sl2, s); break;
-      default: return mace_fail(ctx, MACE_ERR_UNSUPPORTED, "attn: head_dim must be 32, 64 or 128");
-    }
+    rc = dispatch_decode2(ctx, a, sl2, s);
     if (rc) return rc;
   }
   return mace_check_launch(ctx, "attn_fwd");

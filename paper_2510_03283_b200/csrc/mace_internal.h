@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <string>
+#include <unordered_map>
 
 #include "../../include/mace_b200.h"
 
@@ -30,6 +31,7 @@ struct MaceCtx {
   long long launches = 0;
   std::string last_error;
   PFN_cuTensorMapEncodeTiled_v12000 encode_tiled = nullptr;
+  std::unordered_map<const void*, unsigned long long> work_next;  // decode-attention ticket counters
 };
 
 int mace_fail(MaceCtx* ctx, int code, const std::string& msg);

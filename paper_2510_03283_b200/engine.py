@@ -28,6 +28,7 @@ import torch
 
 from .batch import KIND_DECODE, KIND_FT, KIND_PREFILL, PAGE, FtPair, TickBatch
 from .config import ModelConfig, TrainConfig
+from .hoststats import BatchedHeadStats
 from .kvmanager import GpuPrefixTrie, GroupPool, plan_prefill_pages
 from .model import HybridModel
 from .refpath import ensure_macesim
@@ -37,6 +38,9 @@ from macesim.cache import dfs_order  # noqa: E402
 from macesim.cost_model import CostProfile  # noqa: E402
 from macesim.engine import Engine  # noqa: E402
 from macesim.workload import WorkloadType  # noqa: E402
+
+
+DECODE_CHUNK_PAGES = 32  # long decode contexts are split into chunks of <= 32 prompt pages (512 tokens)
 
 
 def synthetic_pair_tokens(seed: int, rid: int, n_c: int, n_r: int, vocab: int) -> tuple[list[int], list[int]]:
@@ -62,6 +66,17 @@ def measured_profile(profile: CostProfile) -> _MeasuredProfile:
     p = _MeasuredProfile(**fields)
     object.__setattr__(p, "_clock", [0.0])
     return p
+
+
+def path_dfs_order(pending) -> list:
+    """Same order as macesim.cache.dfs_order (cache.py:253-273) without walking the whole trie: a pre-order
+    DFS visiting children by ascending first token lists a request when its leaf is reached, i.e. in
+    lexicographic order of the first tokens along its root path (a path before its extensions), ties by id."""
+    def key(item):
+        req, leaf = item
+        return ([n.label[0] for n in leaf.path_nodes()], req.id)
+
+    return [r for r, _ in sorted(pending, key=key)]
 
 
 class TickBudgetReached(Exception):
@@ -106,6 +121,13 @@ class GpuEngine(Engine):
         self._budget_end: int | None = None
         self.keep_outputs = True
         self.time_ticks = False
+        # batched bit-exact head-stats/prune bookkeeping (engine.py:482-532 restated over all rows)
+        self.fast_host = True
+        cc = cache_cfg
+        self.hstats = BatchedHeadStats(model.max_slots, cc.num_heads, cc.norm_window, cc.c_total, cc.prune_window,
+                                       cc.norm_tau)
+        self._dec_list: list = []
+        self._dec_pending: dict | None = None
 
     # ------------------------------------------------------------------ helpers
     def _slot(self, rid: int) -> int:
@@ -125,21 +147,31 @@ class GpuEngine(Engine):
 
     # ------------------------------------------------------------------ batch building
     def build_batch(self, prefills, decodes, fts) -> TickBatch:
+        """Row tables of one tick (numpy-vectorised; the per-row Python is the reference's, not ours)."""
         c = self.mcfg
-        toks, pos, rseq, rkvi = [], [], [], []
-        seqs, tc_items, dec_items = [], [], []
-        dec_slots, dec_rows = [], []
+        Hq, Hkv = c.n_heads, c.n_kv_heads
+        i32 = np.int32
+        tok_seg, pos_seg, seq_seg, kvi_seg = [], [], [], []
+        seqs: list[tuple] = []
+        tc_seg = []
         ptab_slots, ptab_rows, copies = [], [], []
-        n_pre = n_dec = n_ft = 0
+        n_rows = 0
+        n_pre = n_ft = 0
         pending_cached: set[int] = set()
         fresh: set[int] = set()
         self._planned_shared = {}
+        hq_grid = np.arange(Hq, dtype=i32)
 
-        def add_tc(si, q_len):
-            for hq in range(c.n_heads):
-                for qb in range((q_len + 127) // 128):
-                    tc_items.append((si, hq, qb, 0))
+        def tc_block(si, q_len):
+            nb = (q_len + 127) // 128
+            g = np.empty((Hq * nb, 4), i32)
+            g[:, 0] = si
+            g[:, 1] = np.repeat(hq_grid, nb)
+            g[:, 2] = np.tile(np.arange(nb, dtype=i32), Hq)
+            g[:, 3] = 0
+            return g
 
+        # ---- prefill rows (trie-DFS order): uncached suffix of each prompt
         for req in prefills:
             rs = self.state[req.id]
             slot = self._slot(req.id)
@@ -154,32 +186,68 @@ class GpuEngine(Engine):
             if q <= 0:
                 continue
             si = len(seqs)
-            seqs.append((KIND_PREFILL, len(toks), q, slot, P, P, -1, 0))
-            add_tc(si, q)
-            toks += req.prompt_tokens[start:]
-            pos += list(range(start, P))
-            rseq += [si] * q
-            rkvi += list(range(start, P))
+            seqs.append((KIND_PREFILL, n_rows, q, slot, P, P, -1, 0))
+            tc_seg.append(tc_block(si, q))
+            tok_seg.append(np.asarray(req.prompt_tokens[start:], i32))
+            r = np.arange(start, P, dtype=i32)
+            pos_seg.append(r)
+            kvi_seg.append(r)
+            seq_seg.append(np.full(q, si, i32))
+            n_rows += q
             n_pre += P - shared  # tokens the reference charges (engine.py:449-450)
-        for j, req in enumerate(decodes):
-            slot = self.slot_of[req.id]
-            P = len(req.prompt_tokens)
-            k0 = req.decode_pos
-            si = len(seqs)
-            seqs.append((KIND_DECODE, len(toks), 1, slot, P - 1, 0, j, 0))
-            dec_items += [(si, h) for h in range(c.n_kv_heads)]
-            dec_slots.append(slot)
-            dec_rows.append(len(toks))
-            toks.append(req.prompt_tokens[-1] if k0 == 0 else -(slot + 1))
-            pos.append(P - 1 + k0)
-            rseq.append(si)
-            rkvi.append(k0)
-            n_dec += 1
-        ft0 = len(toks)
-        n_tc_inference = len(tc_items)
+        # ---- decode rows (id order): one row each
+        n_dec = len(decodes)
+        dec_items = np.zeros((0, 4), i32)
+        dec_slots = np.zeros(0, i32)
+        dec_rows = np.zeros(0, i32)
+        if n_dec:
+            slot_of = self.slot_of
+            P = np.fromiter((len(r.prompt_tokens) for r in decodes), i32, n_dec)
+            k0 = np.fromiter((r.decode_pos for r in decodes), i32, n_dec)
+            dec_slots = np.fromiter((slot_of[r.id] for r in decodes), i32, n_dec)
+            last = np.fromiter((r.prompt_tokens[-1] for r in decodes), i32, n_dec)
+            si0 = len(seqs)
+            dec_rows = np.arange(n_rows, n_rows + n_dec, dtype=i32)
+            sarr = np.zeros((n_dec, 8), i32)
+            sarr[:, 0] = KIND_DECODE
+            sarr[:, 1] = dec_rows
+            sarr[:, 2] = 1
+            sarr[:, 3] = dec_slots
+            sarr[:, 4] = P - 1
+            sarr[:, 6] = np.arange(n_dec, dtype=i32)
+            seqs.extend(map(tuple, sarr.tolist()))
+            tok_seg.append(np.where(k0 == 0, last, -(dec_slots + 1)).astype(i32))
+            pos_seg.append((P - 1 + k0).astype(i32))
+            seq_seg.append(np.arange(si0, si0 + n_dec, dtype=i32))
+            kvi_seg.append(k0)
+            n_rows += n_dec
+            # decode attention work items: (seq, kv head, chunk << 16 | n_chunks, partial base), LPT order
+            npp = (P - 1 + PAGE - 1) // PAGE
+            nch = np.maximum(1, -(-npp // DECODE_CHUNK_PAGES))
+            per = -(-npp // nch)
+            n_it = nch * Hkv
+            seq_i = np.repeat(np.arange(si0, si0 + n_dec, dtype=i32), n_it)
+            within = np.concatenate([np.arange(k, dtype=i32) for k in n_it]) if n_dec else np.zeros(0, i32)
+            nch_r = np.repeat(nch, n_it)
+            per_r = np.repeat(per, n_it)
+            npp_r = np.repeat(npp, n_it)
+            head = within // nch_r
+            ch = within % nch_r
+            multi = nch_r > 1
+            # partial slots: consecutive per (decode, head) for multi-chunk items
+            starts = np.cumsum(np.where(nch > 1, n_it, 0)) - np.where(nch > 1, n_it, 0)
+            base = np.repeat(starts, n_it) + head * nch_r
+            base = np.where(multi, base, 0)
+            pages = np.minimum(per_r, npp_r - ch * per_r) + np.where(ch == nch_r - 1, np.repeat(k0, n_it) // PAGE + 1, 0)
+            dec_items = np.stack([seq_i, head, (ch << 16) | nch_r, base], 1).astype(i32)
+            dec_items = dec_items[np.argsort(-pages, kind="stable")]
+        ft0 = n_rows
+        n_tc_inference = int(sum(t.shape[0] for t in tc_seg))
+        # ---- fine-tune rows (id order): [prompt | chosen], [prompt | rejected]
         pairs: list[FtPair] = []
-        logit_rows, targets, pair_rows, row_ps = [], [], [], []
-        ft_seqs, ft_tc, ft_rseq, bwd = [], [], [], []
+        lr_seg, tg_seg, ps_seg, pair_rows = [], [], [], []
+        ft_seqs, ft_tc_seg, ft_seq_seg, bwd_seg = [], [], [], []
+        n_logit = 0
         if fts:
             self._resolve_ref()
         for p_i, req in enumerate(fts):
@@ -187,52 +255,61 @@ class GpuEngine(Engine):
             room = max(1, c.max_pos - P)
             n_c = min(req.pair.tokens_chosen, room)
             n_r = min(req.pair.tokens_rejected, room)
-            ch, rj = synthetic_pair_tokens(self.seed, req.id, n_c, n_r, c.vocab)
-            pairs.append(FtPair(req.id, req.prompt_tokens, ch, rj, self.ref_lp.get(req.id)))
+            chs, rjs = synthetic_pair_tokens(self.seed, req.id, n_c, n_r, c.vocab)
+            pairs.append(FtPair(req.id, req.prompt_tokens, chs, rjs, self.ref_lp.get(req.id)))
             pr = []
-            for side, resp in enumerate((ch, rj)):
+            for side, resp in enumerate((chs, rjs)):
                 n = P + len(resp)
                 si = len(seqs)
-                q0 = len(toks)
+                q0 = n_rows
                 seqs.append((KIND_FT, q0, n, -1, 0, n, -1, 0))
-                add_tc(si, n)
+                tc_seg.append(tc_block(si, n))
                 fs = len(ft_seqs)
                 ft_seqs.append((KIND_FT, q0 - ft0, n, -1, 0, n, -1, 0))
-                for hq in range(c.n_heads):
-                    for qb in range((n + 127) // 128):
-                        ft_tc.append((fs, hq, qb, 0))
-                bwd += [(fs, h, kb, 0) for h in range(c.n_kv_heads) for kb in range((n + 63) // 64)]
-                toks += list(req.prompt_tokens) + list(resp)
-                pos += list(range(n))
-                rseq += [si] * n
-                rkvi += [-1] * n
-                ft_rseq += [fs] * n
-                pr += [len(logit_rows), len(resp)]
-                for i, y in enumerate(resp):
-                    logit_rows.append(q0 + P - 1 + i)
-                    targets.append(y)
-                    row_ps.append(2 * p_i + side)
+                ft_tc_seg.append(tc_block(fs, n))
+                nkb = (n + 63) // 64
+                bw = np.zeros((Hkv * nkb, 4), i32)
+                bw[:, 0] = fs
+                bw[:, 1] = np.repeat(np.arange(Hkv, dtype=i32), nkb)
+                bw[:, 2] = np.tile(np.arange(nkb, dtype=i32), Hkv)
+                bwd_seg.append(bw)
+                tok_seg.append(np.asarray(list(req.prompt_tokens) + list(resp), i32))
+                pos_seg.append(np.arange(n, dtype=i32))
+                seq_seg.append(np.full(n, si, i32))
+                kvi_seg.append(np.full(n, -1, i32))
+                ft_seq_seg.append(np.full(n, fs, i32))
+                pr += [n_logit, len(resp)]
+                lr_seg.append(np.arange(q0 + P - 1, q0 + P - 1 + len(resp), dtype=i32))
+                tg_seg.append(np.asarray(resp, i32))
+                ps_seg.append(np.full(len(resp), 2 * p_i + side, i32))
+                n_logit += len(resp)
+                n_rows += n
                 n_ft += n
             pair_rows.append(pr)
 
-        def arr(x, shape_tail=()):
-            a = np.asarray(x, dtype=np.int32)
-            return a.reshape((-1,) + shape_tail) if a.size or shape_tail else a.reshape(-1)
+        def cat(segs, tail=None):
+            if not segs:
+                return np.zeros((0,) + ((tail,) if tail else ()), i32)
+            return np.concatenate(segs).astype(i32, copy=False)
+
+        def arr(x, tail):
+            a = np.asarray(x, dtype=i32)
+            return a.reshape(-1, tail)
 
         maxpp = self.model.maxpp
-        pt = np.full((len(ptab_rows), maxpp), 0, np.int32)
+        pt = np.zeros((len(ptab_rows), maxpp), i32)
         for i, t in enumerate(ptab_rows):
             if len(t) > maxpp:
                 raise RuntimeError("prompt longer than max_prompt_len")
             pt[i, : len(t)] = t
         return TickBatch(
-            tokens=arr(toks), pos=arr(pos), row_seq=arr(rseq), row_kvi=arr(rkvi),
-            seqs=arr(seqs, (8,)), tc_items=arr(tc_items, (4,)), dec_items=arr(dec_items, (2,)),
-            dec_slots=arr(dec_slots), dec_rows=arr(dec_rows), ptab_slots=arr(ptab_slots), ptab_rows=pt,
-            page_copies=arr(copies, (4,)), ft0=ft0, ft_pairs=pairs, ft_logit_rows=arr(logit_rows),
-            ft_targets=arr(targets), pair_rows=arr(pair_rows, (4,)), row_ps=arr(row_ps),
-            ft_seqs=arr(ft_seqs, (8,)), ft_tc_items=arr(ft_tc, (4,)), ft_row_seq=arr(ft_rseq),
-            bwd_items=arr(bwd, (4,)), n_prefill_tokens=n_pre, n_decode_tokens=n_dec, n_ft_tokens=n_ft,
+            tokens=cat(tok_seg), pos=cat(pos_seg), row_seq=cat(seq_seg), row_kvi=cat(kvi_seg),
+            seqs=arr(seqs, 8), tc_items=cat(tc_seg, 4), dec_items=dec_items,
+            dec_slots=dec_slots.astype(i32), dec_rows=dec_rows, ptab_slots=np.asarray(ptab_slots, i32), ptab_rows=pt,
+            page_copies=arr(copies, 4), ft0=ft0, ft_pairs=pairs, ft_logit_rows=cat(lr_seg),
+            ft_targets=cat(tg_seg), pair_rows=arr(pair_rows, 4), row_ps=cat(ps_seg),
+            ft_seqs=arr(ft_seqs, 8), ft_tc_items=cat(ft_tc_seg, 4), ft_row_seq=cat(ft_seq_seg),
+            bwd_items=cat(bwd_seg, 4), n_prefill_tokens=n_pre, n_decode_tokens=n_dec, n_ft_tokens=n_ft,
             meta={"n_tc_inference": n_tc_inference},
         )
 
@@ -245,8 +322,10 @@ class GpuEngine(Engine):
         if self.trie is not None and len(prefills) > 1:  # identical ordering rule to engine.py:581-584
             pending = [(r, self.state[r.id].leaf) for r in prefills]
             if all(leaf is not None for _, leaf in pending):
-                prefills = dfs_order(self.trie, pending)
+                prefills = path_dfs_order(pending)
         batch = self.build_batch(prefills, decodes, fts)
+        self._dec_list = decodes
+        self._dec_pending = None
         m = self.model
         timed = self.mode == "M" or self.time_ticks
         if timed:
@@ -323,6 +402,59 @@ class GpuEngine(Engine):
             if planned is not None and planned != shared:
                 raise AssertionError(f"req {req.id}: planned shared prefix {planned} != reference {shared}")
         return super()._exec_prefill(req)
+
+    def _exec_decode(self, req, t_end_ms):  # engine.py:482 — same effects, head stats batched per tick
+        if not (self.fast_host and self.pruning):
+            return super()._exec_decode(req, t_end_ms)
+        rs = self.state[req.id]
+        if rs.head_stats is None:
+            return super()._exec_decode(req, t_end_ms)
+        if self._dec_pending is None:
+            self._dec_pending = self._batch_head_stats()
+        kept, released = self._dec_pending[req.id]
+        req.decode_pos += 1
+        self.metrics.decoded_tokens += 1
+        if rs.first_token_ms is None:
+            rs.first_token_ms = t_end_ms
+            self.metrics.ttft_ms[req.id] = t_end_ms - req.arrival_time * 1000.0
+            self.metrics.tbt_ms[req.id] = []
+        else:
+            self.metrics.tbt_ms[req.id].append(t_end_ms - rs.last_token_ms)
+        rs.last_token_ms = t_end_ms
+        kv = self.profile.decode_kv_mem_per_token
+        heads = self.cache_cfg.num_heads
+        per_head = kv / heads
+        rs.kept = kept
+        self.slots_created += heads
+        grown = per_head * heads
+        rs.resident_kv_mb += grown
+        self._resident_kv_total += grown
+        if released:
+            self.slots_released += released
+            freed = released * per_head
+            rs.resident_kv_mb -= freed
+            self._resident_kv_total -= freed
+            self.timeline.append({"kind": "cache_event", "t": self.clock, "event": "prune", "req_id": req.id,
+                                  "bytes_mb": -freed, "slots": released})
+
+    def _batch_head_stats(self) -> dict:
+        """Head-stats + allocation + prune for every decode row of this tick (id order)."""
+        rows = [r for r in self._dec_list if self.state[r.id].head_stats is not None]
+        out: dict = {}
+        if not rows:
+            return out
+        slots = np.fromiter((self.slot_of[r.id] for r in rows), np.int64, len(rows))
+        first = np.fromiter((r.decode_pos == 0 for r in rows), bool, len(rows))
+        if first.any():
+            self.hstats.reset(slots[first])
+        steps = np.fromiter((r.decode_pos + 1 for r in rows), np.int64, len(rows))
+        norms = np.array([self._synth_norms(r, self.state[r.id]) for r in rows], dtype=np.float64)
+        kept, released = self.hstats.step(slots, steps, norms)
+        kl = kept.tolist()
+        rl = released.tolist()
+        for i, r in enumerate(rows):
+            out[r.id] = (kl[i], rl[i])
+        return out
 
     def _retire(self, req, t_end_ms, rejected=False):  # engine.py:538
         super()._retire(req, t_end_ms, rejected)

@@ -106,6 +106,8 @@ class HybridModel:
         self.free_stack = torch.arange(prompt_groups * H, self.pages_per_layer, **i32)
         self.free_top = torch.tensor([decode_pages], **i32)
         self.last_token = torch.zeros(max_slots, **i32)
+        self.dec_counters = torch.zeros(max_slots * H, **i32)  # decode chunk-merge counters (self-cleaning)
+        self.dec_work = torch.zeros(1, dtype=torch.int64, device=self.dev)  # decode ticket counter (monotonic)
         self.kv = MaceKvLayout(
             ptab=self.ptab.data_ptr(), max_prompt_pages=self.maxpp, dtab=self.dtab.data_ptr(),
             max_dec_pages=self.maxdp, dec_base=self.dec_base.data_ptr(), dec_first=self.dec_first.data_ptr(),
@@ -183,6 +185,7 @@ class HybridModel:
             self.dec_h = torch.empty(cap, c.d_model, **bf)
             self.dec_logits = torch.empty(cap, c.vocab, **f32)
             self.dec_tok = torch.empty(cap, dtype=torch.int32, device=dev)
+            self.dec_ws = torch.empty(cap * c.n_kv_heads * 4 * (2 * c.group + c.group * c.head_dim), **f32)
             self._ndec_cap = cap
 
     def replay(self, tape) -> None:
@@ -255,12 +258,14 @@ class HybridModel:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, None, dec_items, lay,
-                         kp, vp, o[:T], lse=lse, head_norm=hn)
+                         kp, vp, o[:T], lse=lse, head_norm=hn, dec_workspace=self.dec_ws,
+                         dec_counters=self.dec_counters, dec_work=self.dec_work)
             e1.record()
             self.instrument.append((e0, e1, self._attn_bytes))
         else:
             ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, tc_items, dec_items, lay,
-                         kp, vp, o[:T], lse=lse, head_norm=hn)
+                         kp, vp, o[:T], lse=lse, head_norm=hn, dec_workspace=self.dec_ws,
+                         dec_counters=self.dec_counters, dec_work=self.dec_work)
         if save is not None:
             n = T - ft0
             save["h1"][:n].copy_(h[ft0:T])

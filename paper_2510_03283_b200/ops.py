@@ -89,6 +89,9 @@ def attn_fwd(
     lse: torch.Tensor | None = None,
     head_norm: torch.Tensor | None = None,
     stream: torch.cuda.Stream | None = None,
+    dec_workspace: torch.Tensor | None = None,
+    dec_counters: torch.Tensor | None = None,
+    dec_work: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """Ragged paged attention of one tick (prefill + FT tiles on tcgen05, decode rows streamed)."""
     from ._lib import MaceAttnArgs
@@ -103,6 +106,9 @@ def attn_fwd(
         kv=kv_layout,
         k_pool=_ptr(k_pool), v_pool=_ptr(v_pool), pool_pages=0 if k_pool is None else k_pool.shape[0],
         out=out.data_ptr(), lse=_ptr(lse), head_norm=_ptr(head_norm), scale=0.0,
+        dec_workspace=_ptr(dec_workspace),
+        dec_workspace_bytes=0 if dec_workspace is None else dec_workspace.numel() * dec_workspace.element_size(),
+        dec_counters=_ptr(dec_counters), dec_work=_ptr(dec_work),
     )
     ctx.check(ctx.L.mace_attn_fwd(ctx.h, C.byref(a), _stream(stream)), "mace_attn_fwd")
     return out

@@ -8,6 +8,10 @@ ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
+from paper_2510_03283_b200.refpath import ensure_macesim  # noqa: E402
+
+ensure_macesim()  # the unmodified reference scheduler (baseline/_ref), importable as `macesim`
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built libmace_b200.so")

@@ -12,14 +12,14 @@ pytestmark = pytest.mark.gpu
 PG = 16
 
 
-def _build(hd, Hq, Hkv, seed, prefill=((200, 120), (40, 40), (300, 1)), decode=((150, 37), (16, 1), (33, 100)),
-           ft=(130, 77, 256)):
+def _build(hd, Hq, Hkv, seed, prefill=((200, 120), (40, 40), (300, 1)),
+           decode=((150, 37), (16, 1), (33, 100), (1537, 60)), ft=(130, 77, 256)):
     g = torch.Generator().manual_seed(seed)
     rng = np.random.default_rng(seed)
     dev = "cuda"
     W = (Hq + 2 * Hkv) * hd
     n_slots = len(prefill) + len(decode)
-    maxpp = 32
+    maxpp = 128
     maxdp = 16
     # page allocation: prompt groups then per-head decode pages
     total_groups = sum((n + PG - 1) // PG for n, _ in prefill) + sum((n + PG - 1) // PG for n, _ in decode)
@@ -67,8 +67,11 @@ def _build(hd, Hq, Hkv, seed, prefill=((200, 120), (40, 40), (300, 1)), decode=(
     T = row
     for si, s in enumerate(seqs):
         if s[0] == 1:
+            nch = max(1, -(-((s[4] + 15) // 16) // 32))
             for h in range(Hkv):
-                dec_items.append([si, h])
+                base = len(dec_items)
+                for ch in range(nch):
+                    dec_items.append([si, h, (ch << 16) | nch, base])
         else:
             for hq in range(Hq):
                 for qb in range((s[2] + 127) // 128):
@@ -81,7 +84,11 @@ def _build(hd, Hq, Hkv, seed, prefill=((200, 120), (40, 40), (300, 1)), decode=(
     d = {k: (torch.from_numpy(v).to(dev) if isinstance(v, np.ndarray) else v.to(dev)) for k, v in host.items() if k != "seqs"}
     d["seqs"] = torch.tensor(seqs, dtype=torch.int32, device=dev)
     d["tc_items"] = torch.tensor(tc_items, dtype=torch.int32, device=dev).reshape(-1, 4) if tc_items else None
-    d["dec_items"] = torch.tensor(dec_items, dtype=torch.int32, device=dev).reshape(-1, 2) if dec_items else None
+    d["dec_items"] = torch.tensor(dec_items, dtype=torch.int32, device=dev).reshape(-1, 4) if dec_items else None
+    d["dec_ws"] = torch.empty(len(dec_items) * (2 * (Hq // Hkv) + (Hq // Hkv) * hd), device=dev)
+    d["dec_cnt"] = torch.zeros(n_slots * Hkv, dtype=torch.int32, device=dev)
+    d["dec_work"] = torch.zeros(1, dtype=torch.int64, device=dev)
+    rng.shuffle(dec_items)  # any order: items carry their partial slot
     lay = MaceKvLayout(ptab=d["ptab"].data_ptr(), max_prompt_pages=maxpp, dtab=d["dtab"].data_ptr(), max_dec_pages=maxdp,
                        dec_base=d["dec_base"].data_ptr(), dec_first=d["dec_first"].data_ptr(),
                        dec_end=d["dec_end"].data_ptr(), free_stack=None, free_top=None, stack_cap=0, n_kv_heads=Hkv)
@@ -123,8 +130,11 @@ def test_attention_ragged(ctx, hd, Hq, Hkv):
     out = torch.zeros(T, Hq * hd, dtype=torch.bfloat16, device="cuda")
     hn = torch.zeros(T, Hq, device="cuda")
     lse = torch.zeros(T, Hq, device="cuda")
-    ops.attn_fwd(ctx, d["qkv"], Hq, Hkv, hd, d["seqs"], d["tc_items"], d["dec_items"], lay, d["kp"], d["vp"], out,
-                 lse=lse, head_norm=hn)
+    for _ in range(2):  # twice: the chunk-merge counters must come back zeroed
+        ops.attn_fwd(ctx, d["qkv"], Hq, Hkv, hd, d["seqs"], d["tc_items"], d["dec_items"], lay, d["kp"], d["vp"], out,
+                     lse=lse, head_norm=hn, dec_workspace=d["dec_ws"], dec_counters=d["dec_cnt"],
+                     dec_work=d["dec_work"])
+    assert int(d["dec_cnt"].abs().sum()) == 0
     torch.cuda.synchronize()
     ref = _reference(host, Hq, Hkv, hd, T)
     got = out.float().cpu().reshape(T, Hq, hd)

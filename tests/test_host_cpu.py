@@ -115,3 +115,66 @@ def test_baseline_policies_share_execute(policy):
     res = eng.run()
     assert json.dumps(res.timeline, sort_keys=True) == json.dumps(ref.timeline, sort_keys=True)
     assert not fm.violations
+
+
+def test_path_dfs_order_matches_reference():
+    """The engine's O(path) DFS ordering equals the reference's whole-trie dfs_order on real tries."""
+    import random
+
+    from macesim.cache import PrefixTrie, dfs_order
+    from macesim.workload import Request, WorkloadType
+    from paper_2510_03283_b200.engine import path_dfs_order
+
+    rnd = random.Random(0)
+    for trial in range(30):
+        trie = PrefixTrie(0.1)
+        reqs = []
+        base = [rnd.randrange(6) for _ in range(12)]
+        for i in range(rnd.randrange(2, 25)):
+            cut = rnd.randrange(0, 12)
+            prompt = base[:cut] + [rnd.randrange(6) for _ in range(rnd.randrange(1, 8))]
+            r = Request(id=i, tenant=0, workload=WorkloadType.PREFILL, arrival_time=0.0, prompt_tokens=prompt,
+                        target_output_len=1)
+            reqs.append((r, trie.insert(prompt, 0.0).leaf))
+        sub = rnd.sample(reqs, rnd.randrange(2, len(reqs) + 1))
+        assert [r.id for r in path_dfs_order(sub)] == [r.id for r in dfs_order(trie, sub)]
+
+
+@pytest.mark.parametrize("wl_name,ticks", [("c1", None), ("c2", 260)])
+def test_batched_head_stats_bit_identical(wl_name, ticks):
+    """The batched head-stats/prune bookkeeping (hoststats.py) reproduces the reference's per-row
+    _exec_decode exactly: same timeline (prune events carry MB deltas), kept[] and metrics."""
+    from paper_2510_03283_b200.workloads import WORKLOADS
+
+    def run(fast):
+        wl = WORKLOADS[wl_name]()
+        eng, fm = _engine(wl, prompt_groups=1 << 15, max_slots=1024)
+        eng.fast_host = fast
+        if ticks is None:
+            res = eng.run()
+            return res.timeline, res.metrics.tbt_ms, {k: list(v.kept) for k, v in eng.state.items()}
+        eng.run_ticks(ticks)
+        return eng.timeline, eng.metrics.tbt_ms, {k: list(v.kept) for k, v in eng.state.items()}
+
+    a, b = run(True), run(False)
+    assert json.dumps(a[0], sort_keys=True) == json.dumps(b[0], sort_keys=True)
+    assert a[1] == b[1]
+    assert a[2] == b[2]
+    assert any(e.get("event") == "prune" for e in a[0])
+
+
+def test_batched_allocate_matches_reference_fuzz():
+    import numpy as np
+
+    from macesim.cache import allocate_capacity
+    from paper_2510_03283_b200.hoststats import BatchedHeadStats
+
+    rng = np.random.default_rng(0)
+    for H, C in ((8, 160), (12, 160), (4, 10), (3, 7)):
+        hs = BatchedHeadStats(1, H, 4, C, 128, None)
+        means = rng.random((4000, H)) * rng.choice([1.0, 0.01], size=(4000, H))
+        means[rng.random((4000, H)) < 0.1] = 0.0
+        means[:5] = 0.0
+        got = hs._allocate(means)
+        want = np.array([allocate_capacity(m.tolist(), C) for m in means])
+        assert (got == want).all()
