@@ -87,6 +87,8 @@ __global__ void __launch_bounds__(128) attn_tc_kernel(const __grid_constant__ Tc
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
   const uint32_t tmem_s = tmem, tmem_o = tmem + 128;
 
   auto load_kv = [&](int j, int stage) {
@@ -290,7 +292,7 @@ static int launch_tc(MaceCtx* ctx, const MaceAttnArgs* a, float scale_log2, cuda
     cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  attn_tc_kernel<HD><<<a->n_tc, 128, C::SMEM, s>>>(maps, a->seqs, reinterpret_cast<const int4*>(a->tc_items), a->kv,
+  launch_k(attn_tc_kernel<HD>, a->n_tc, 128, C::SMEM, s, maps, a->seqs, reinterpret_cast<const int4*>(a->tc_items), a->kv,
                                                    a->Hq, a->Hkv, scale_log2, (__nv_bfloat16*)a->out, a->lse);
   ctx->launches++;
   return 0;

@@ -49,6 +49,8 @@ __global__ void __launch_bounds__(Dec2<HD, G>::WARPS * 32) attn_decode2_kernel(
     for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
   fence_barrier_init();
   __syncwarp();
+  pdl_wait();
+  pdl_trigger();
   const int W = (Hq + 2 * Hkv) * HD;
   const int t = lane & 15, half = lane >> 4;
   uint32_t ring_count = 0;  // pages issued by this warp so far (mbarrier phase bookkeeping across items)
@@ -312,7 +314,7 @@ int launch_decode2(MaceCtx* ctx, const MaceAttnArgs* a, float scale_log2, cudaSt
   unsigned long long& next = ctx->work_next[a->dec_work];
   const unsigned long long base = next;
   next += (unsigned long long)a->n_dec + (unsigned long long)grid * C::WARPS;
-  attn_decode2_kernel<HD, G><<<grid, C::WARPS * 32, C::SMEM, s>>>(
+  launch_k(attn_decode2_kernel<HD, G>, grid, C::WARPS * 32, C::SMEM, s, 
       (const __nv_bfloat16*)a->qkv, a->seqs, reinterpret_cast<const int4*>(a->dec_items), a->n_dec, a->kv,
       (const __nv_bfloat16*)a->k_pool, (const __nv_bfloat16*)a->v_pool, a->Hq, a->Hkv, scale_log2,
       (__nv_bfloat16*)a->out, a->head_norm, (float*)a->dec_workspace, a->dec_counters, a->dec_work, base);

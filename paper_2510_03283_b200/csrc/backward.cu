@@ -20,6 +20,8 @@ __global__ void norm_bwd_kernel(const float* __restrict__ x, int ldx, const int*
                                 const float* __restrict__ dy, int lddy, int n, int d, const __nv_bfloat16* __restrict__ w,
                                 int layernorm, float eps, float* __restrict__ dx, int lddx, const int* __restrict__ dxrows,
                                 float* __restrict__ part, int rows_per_block) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sh[];  // [2][d] block partials
   for (int c = threadIdx.x; c < 2 * d; c += blockDim.x) sh[c] = 0.f;
   __syncthreads();
@@ -95,6 +97,8 @@ __global__ void norm_bwd_kernel(const float* __restrict__ x, int ldx, const int*
 
 // out[c] += sum_b part[b * ld + c]   (fixed order over b)
 __global__ void col_reduce_kernel(const float* __restrict__ part, int nb, int ld, int ncols, float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncols) return;
   float s = 0.f;
@@ -105,6 +109,8 @@ __global__ void col_reduce_kernel(const float* __restrict__ part, int nb, int ld
 // column sums of a bf16 matrix (bias grads), partial per row-chunk then col_reduce
 __global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ y, int n, int N, int ld, int rows_per_block,
                                    float* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
   const int r0 = blockIdx.y * rows_per_block, r1 = min(n, r0 + rows_per_block);
@@ -116,6 +122,8 @@ __global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ y, int n, i
 // ------------------------------------------------------------------ activation backward
 __global__ void act_bwd_kernel(const __nv_bfloat16* __restrict__ u, const __nv_bfloat16* __restrict__ da, int n, int F,
                                int swiglu, __nv_bfloat16* __restrict__ du) {
+  pdl_wait();
+  pdl_trigger();
   const size_t total = (size_t)n * F;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const size_t r = i / F, c = i % F;
@@ -140,6 +148,8 @@ __global__ void act_bwd_kernel(const __nv_bfloat16* __restrict__ u, const __nv_b
 // ------------------------------------------------------------------ RoPE backward on dq / dk (fp32 rows)
 __global__ void rope_bwd_kernel(float* __restrict__ dqkv, int n, int Hq, int Hkv, int hd, const int* __restrict__ pos,
                                 const float* __restrict__ cos_t, const float* __restrict__ sin_t) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   if (r >= n) return;
   const int W = (Hq + 2 * Hkv) * hd, half = hd / 2;
@@ -156,6 +166,8 @@ __global__ void rope_bwd_kernel(float* __restrict__ dqkv, int n, int Hq, int Hkv
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ x, long long n, __nv_bfloat16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     y[i] = __float2bfloat16(x[i]);
 }
@@ -164,6 +176,8 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ x, long long n, __n
 // D[r, hq] = sum_d dO[r, hq, d] * O[r, hq, d]
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout, int n,
                                      int Hq, int hd, float* __restrict__ Dout) {
+  pdl_wait();
+  pdl_trigger();
   const int idx = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (idx >= n * Hq) return;
@@ -183,6 +197,8 @@ __global__ void __launch_bounds__(256) attn_bwd_kernel(const __nv_bfloat16* __re
                                                        const MaceSeq* __restrict__ seqs, const int4* __restrict__ items,
                                                        int Hq, int Hkv, float scale, float* __restrict__ dqkv,
                                                        int row_offset) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int B = 64;
   constexpr int LDH = HD + 1;
   extern __shared__ float sm[];
@@ -347,17 +363,17 @@ extern "C" int mace_norm_bwd(mace_ctx* ctx, const float* x, int ldx, const int* 
   const int per_lane = (d + 31) / 32;
   const size_t sh = 2 * d * sizeof(float);
   auto* W = (const __nv_bfloat16*)w;
-#define MACE_NB(K) norm_bwd_kernel<K><<<nb, 256, sh, s>>>(x, ldx, xrows, dy, lddy, n, d, W, layernorm, eps, dx, lddx, dxrows, workspace, rows_per_block)
+#define MACE_NB(K) launch_k(norm_bwd_kernel<K>, nb, 256, sh, s, x, ldx, xrows, dy, lddy, n, d, W, layernorm, eps, dx, lddx, dxrows, workspace, rows_per_block)
   if (per_lane <= 8) MACE_NB(8);
   else if (per_lane <= 24) MACE_NB(24);
   else if (per_lane <= 64) MACE_NB(64);
   else if (per_lane <= 128) MACE_NB(128);
   else return mace_fail(ctx, MACE_ERR_ARG, "norm_bwd: d too large");
 #undef MACE_NB
-  col_reduce_kernel<<<(d + 255) / 256, 256, 0, s>>>(workspace, nb, 2 * d, d, dw);
+  launch_k(col_reduce_kernel, (d + 255) / 256, 256, 0, s, workspace, nb, 2 * d, d, dw);
   ctx->launches += 2;
   if (layernorm && db) {
-    col_reduce_kernel<<<(d + 255) / 256, 256, 0, s>>>(workspace + d, nb, 2 * d, d, db);
+    launch_k(col_reduce_kernel, (d + 255) / 256, 256, 0, s, workspace + d, nb, 2 * d, d, db);
     ctx->launches++;
   }
   return mace_check_launch(ctx, "norm_bwd");
@@ -370,8 +386,8 @@ extern "C" int mace_colsum_bf16(mace_ctx* ctx, const void* y, int n, int N, int 
   const int rpb = 64;
   const int nb = (n + rpb - 1) / rpb;
   if (workspace_bytes < (size_t)nb * N * 4) return mace_fail(ctx, MACE_ERR_ARG, "colsum: workspace too small");
-  colsum_bf16_kernel<<<dim3((N + 255) / 256, nb), 256, 0, s>>>((const __nv_bfloat16*)y, n, N, ld, rpb, workspace);
-  col_reduce_kernel<<<(N + 255) / 256, 256, 0, s>>>(workspace, nb, N, N, out);
+  launch_k(colsum_bf16_kernel, dim3((N + 255) / 256, nb), 256, 0, s, (const __nv_bfloat16*)y, n, N, ld, rpb, workspace);
+  launch_k(col_reduce_kernel, (N + 255) / 256, 256, 0, s, workspace, nb, N, N, out);
   ctx->launches += 2;
   return mace_check_launch(ctx, "colsum");
 }
@@ -381,7 +397,7 @@ extern "C" int mace_act_bwd(mace_ctx* ctx, const void* u, const void* da, int n,
   if (n <= 0) return 0;
   int grid = (int)(((size_t)n * F + 255) / 256);
   if (grid > ctx->num_sms * 16) grid = ctx->num_sms * 16;
-  act_bwd_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)u, (const __nv_bfloat16*)da, n, F, swiglu,
+  launch_k(act_bwd_kernel, grid, 256, 0, (cudaStream_t)stream, (const __nv_bfloat16*)u, (const __nv_bfloat16*)da, n, F, swiglu,
                                                          (__nv_bfloat16*)du);
   ctx->launches++;
   return mace_check_launch(ctx, "act_bwd");
@@ -390,7 +406,7 @@ extern "C" int mace_act_bwd(mace_ctx* ctx, const void* u, const void* da, int n,
 extern "C" int mace_rope_bwd(mace_ctx* ctx, float* dqkv, int n, int Hq, int Hkv, int hd, const int* pos,
                              const float* cos_t, const float* sin_t, void* stream) {
   if (n <= 0) return 0;
-  rope_bwd_kernel<<<n, 128, 0, (cudaStream_t)stream>>>(dqkv, n, Hq, Hkv, hd, pos, cos_t, sin_t);
+  launch_k(rope_bwd_kernel, n, 128, 0, (cudaStream_t)stream, dqkv, n, Hq, Hkv, hd, pos, cos_t, sin_t);
   ctx->launches++;
   return mace_check_launch(ctx, "rope_bwd");
 }
@@ -399,7 +415,7 @@ extern "C" int mace_f32_to_bf16(mace_ctx* ctx, const float* x, long long n, void
   if (n <= 0) return 0;
   long long grid = (n + 255) / 256;
   if (grid > ctx->num_sms * 16) grid = ctx->num_sms * 16;
-  f32_to_bf16_kernel<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(x, n, (__nv_bfloat16*)y);
+  launch_k(f32_to_bf16_kernel, (int)grid, 256, 0, (cudaStream_t)stream, x, n, (__nv_bfloat16*)y);
   ctx->launches++;
   return mace_check_launch(ctx, "f32_to_bf16");
 }
@@ -411,13 +427,13 @@ extern "C" int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, cons
                              float* Dbuf, float* dqkv, void* stream) {
   if (n_items <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
-  attn_bwd_prep_kernel<<<(n_rows * Hq + 7) / 8, 256, 0, s>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, n_rows,
+  launch_k(attn_bwd_prep_kernel, (n_rows * Hq + 7) / 8, 256, 0, s, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, n_rows,
                                                              Hq, hd, Dbuf);
   const float scale = 1.f / sqrtf((float)hd);
   auto go = [&](auto kern, int HD) {
     const size_t sh = (4 * 64 * (HD + 1) + 2 * 64 * 65 + 128) * sizeof(float);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
-    kern<<<n_items, 256, sh, s>>>((const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse, Dbuf, seqs,
+    launch_k(kern, n_items, 256, sh, s, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse, Dbuf, seqs,
                                   reinterpret_cast<const int4*>(items), Hq, Hkv, scale, dqkv, row_offset);
   };
   switch (hd) {

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #define MACE_DEV __device__ __forceinline__
 
 namespace mace {
@@ -28,6 +30,13 @@ MACE_DEV bool elect_one() {
       : "=r"(pred));
   return pred != 0;
 }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the tick is launched with programmatic stream serialisation: it may start (prologue,
+// barrier init, TMEM alloc, descriptor prefetch) while its predecessor drains, and waits here before
+// touching the predecessor's outputs. No-ops when launched without the attribute.
+MACE_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+MACE_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---------------------------------------------------------------- mbarrier
 MACE_DEV void mbar_init(uint64_t* bar, uint32_t count) {
@@ -184,6 +193,23 @@ MACE_DEV float warp_max(float v) {
 MACE_DEV uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// host: launch with the PDL attribute (cudaLaunchKernelEx)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 }  // namespace mace

@@ -18,6 +18,8 @@ namespace mace {
 
 __global__ void dpo_row_kernel(const float* __restrict__ logits, int V, int ld, const int* __restrict__ targets,
                                float* __restrict__ row_lse, float* __restrict__ row_lp) {
+  pdl_wait();
+  pdl_trigger();
   const float* x = logits + (size_t)blockIdx.x * ld;
   __shared__ float red[32];
   float mx = -INFINITY;
@@ -54,6 +56,8 @@ __global__ void dpo_pair_kernel(const float* __restrict__ row_lp, const int* __r
                                 const float* __restrict__ ref_lp, float beta, float grad_scale,
                                 float* __restrict__ lp_out, float* __restrict__ loss, float* __restrict__ margin,
                                 float* __restrict__ coef) {
+  pdl_wait();
+  pdl_trigger();
   const int p = blockIdx.x;
   const int lane = threadIdx.x;
   if (p >= n_pairs) return;
@@ -86,6 +90,8 @@ __global__ void dpo_pair_kernel(const float* __restrict__ row_lp, const int* __r
 __global__ void dpo_grad_kernel(const float* __restrict__ logits, int V, int ld, const int* __restrict__ targets,
                                 const float* __restrict__ row_lse, const int* __restrict__ row_ps,
                                 const float* __restrict__ coef, __nv_bfloat16* __restrict__ dlogits, int ldd) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.y;
   const float g = coef[row_ps[r]];
   const float lse = row_lse[r];
@@ -115,6 +121,8 @@ struct AdamSeg {
 __global__ void adamw_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
                              const float* __restrict__ grad, long long n, AdamSeg seg, float decay, float w1,
                              float b2, float w2, float step_size, float sbc2, float eps) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ long long offs[65];
   for (int i = threadIdx.x; i <= seg.n_seg && i < 65; i += blockDim.x) offs[i] = seg.offsets[i];
   __syncthreads();
@@ -147,13 +155,13 @@ extern "C" int mace_dpo_fused(mace_ctx* ctx, const float* logits, int R, int V, 
                               void* dlogits, int ldd, void* stream) {
   if (R <= 0 || n_pairs <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
-  dpo_row_kernel<<<R, 1024, 0, s>>>(logits, V, ld, targets, row_lse, row_lp);
-  dpo_pair_kernel<<<n_pairs, 32, 0, s>>>(row_lp, pair_rows, n_pairs, ref_lp, beta, 1.f / n_pairs, lp_out, loss, margin,
+  launch_k(dpo_row_kernel, R, 1024, 0, s, logits, V, ld, targets, row_lse, row_lp);
+  launch_k(dpo_pair_kernel, n_pairs, 32, 0, s, row_lp, pair_rows, n_pairs, ref_lp, beta, 1.f / n_pairs, lp_out, loss, margin,
                                          coef);
   ctx->launches += 2;
   if (dlogits && ref_lp) {
     dim3 grid((V + 2047) / 2048, R);
-    dpo_grad_kernel<<<grid, 1024, 0, s>>>(logits, V, ld, targets, row_lse, row_ps, coef, (__nv_bfloat16*)dlogits, ldd);
+    launch_k(dpo_grad_kernel, grid, 1024, 0, s, logits, V, ld, targets, row_lse, row_ps, coef, (__nv_bfloat16*)dlogits, ldd);
     ctx->launches++;
   }
   return mace_check_launch(ctx, "dpo_fused");
@@ -168,7 +176,7 @@ extern "C" int mace_adamw_masked(mace_ctx* ctx, float* master, float* m, float* 
   AdamSeg seg{seg_offsets, reinterpret_cast<__nv_bfloat16* const*>(seg_weights), n_seg};
   int grid = (int)((n + 255) / 256);
   if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
-  adamw_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+  launch_k(adamw_kernel, grid, 256, 0, (cudaStream_t)stream, 
       master, m, v, grad, n, seg, (float)(1.0 - (double)lr * weight_decay), (float)(1.0 - (double)beta1), beta2,
       (float)(1.0 - (double)beta2), (float)((double)lr / bc1), (float)sqrt(bc2), eps);
   ctx->launches++;

@@ -17,6 +17,8 @@ namespace mace {
 __global__ void embed_kernel(const int* __restrict__ tokens, const int* __restrict__ pos,
                              const int* __restrict__ last_token, const __nv_bfloat16* __restrict__ emb,
                              const __nv_bfloat16* __restrict__ pos_emb, int T, int d, float* __restrict__ x) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (row >= T) return;
   const int lane = threadIdx.x & 31;
@@ -48,6 +50,8 @@ template <int kPerLane>
 __global__ void norm_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ rows, int n_rows, int d,
                             const __nv_bfloat16* __restrict__ w, const __nv_bfloat16* __restrict__ b, int layernorm,
                             float eps, __nv_bfloat16* __restrict__ out, int ldo, float* __restrict__ rstd_out) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (i >= n_rows) return;
   const int lane = threadIdx.x & 31;
@@ -109,6 +113,8 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int T, int Hq, i
                                const float* __restrict__ cos_t, const float* __restrict__ sin_t, int apply_rope,
                                const MaceKvLayout kv, __nv_bfloat16* __restrict__ k_pool,
                                __nv_bfloat16* __restrict__ v_pool) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x;
   if (row >= T) return;
   const int W = (Hq + 2 * Hkv) * hd;
@@ -150,6 +156,8 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int T, int Hq, i
 // llama: up row = [gate(F) | up(F)] -> silu(gate) * up ; gpt2: gelu_tanh(up)
 __global__ void act_kernel(const __nv_bfloat16* __restrict__ u, int T, int F, int swiglu,
                            __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const size_t total = (size_t)T * F / 8;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const size_t row = (i * 8) / F, c = (i * 8) % F;
@@ -179,6 +187,8 @@ __global__ void act_kernel(const __nv_bfloat16* __restrict__ u, int T, int F, in
 
 // ------------------------------------------------------------------ argmax over fp32 logits rows
 __global__ void argmax_kernel(const float* __restrict__ logits, int V, int ld, int* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const float* r = logits + (size_t)blockIdx.x * ld;
   float best = -INFINITY;
   int idx = 0x7fffffff;
@@ -231,7 +241,7 @@ extern "C" int mace_embed(mace_ctx* ctx, const int* tokens, const int* pos, cons
                           const void* pos_emb, int T, int d, float* x, void* stream) {
   if (T <= 0) return 0;
   if (d % 256) return mace_fail(ctx, MACE_ERR_ARG, "embed: d must be a multiple of 256");
-  embed_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>(tokens, pos, last_token, (const __nv_bfloat16*)emb,
+  launch_k(embed_kernel, (T + 7) / 8, 256, 0, (cudaStream_t)stream, tokens, pos, last_token, (const __nv_bfloat16*)emb,
                                                                  (const __nv_bfloat16*)pos_emb, T, d, x);
   ctx->launches++;
   return mace_check_launch(ctx, "embed");
@@ -248,13 +258,13 @@ extern "C" int mace_norm(mace_ctx* ctx, const float* x, int ldx, const int* rows
   auto* O = (__nv_bfloat16*)out;
   cudaStream_t s = (cudaStream_t)stream;
   if (per_lane <= 8)
-    norm_kernel<8><<<grid, 256, 0, s>>>(x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
+    launch_k(norm_kernel<8>, grid, 256, 0, s, x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
   else if (per_lane <= 24)
-    norm_kernel<24><<<grid, 256, 0, s>>>(x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
+    launch_k(norm_kernel<24>, grid, 256, 0, s, x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
   else if (per_lane <= 64)
-    norm_kernel<64><<<grid, 256, 0, s>>>(x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
+    launch_k(norm_kernel<64>, grid, 256, 0, s, x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
   else if (per_lane <= 128)
-    norm_kernel<128><<<grid, 256, 0, s>>>(x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
+    launch_k(norm_kernel<128>, grid, 256, 0, s, x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
   else
     return mace_fail(ctx, MACE_ERR_ARG, "norm: d too large");
   ctx->launches++;
@@ -267,7 +277,7 @@ extern "C" int mace_rope_kv(mace_ctx* ctx, void* qkv, int T, int Hq, int Hkv, in
                             void* stream) {
   if (T <= 0) return 0;
   if (hd % 8) return mace_fail(ctx, MACE_ERR_ARG, "rope_kv: hd % 8");
-  rope_kv_kernel<<<T, 128, 0, (cudaStream_t)stream>>>((__nv_bfloat16*)qkv, T, Hq, Hkv, hd, row_pos, row_seq, row_kvi,
+  launch_k(rope_kv_kernel, T, 128, 0, (cudaStream_t)stream, (__nv_bfloat16*)qkv, T, Hq, Hkv, hd, row_pos, row_seq, row_kvi,
                                                       seqs, cos_t, sin_t, apply_rope, *kv, (__nv_bfloat16*)k_pool,
                                                       (__nv_bfloat16*)v_pool);
   ctx->launches++;
@@ -280,14 +290,14 @@ extern "C" int mace_act(mace_ctx* ctx, const void* u, int T, int F, int swiglu, 
   const size_t work = (size_t)T * F / 8;
   int grid = (int)((work + 255) / 256);
   if (grid > ctx->num_sms * 16) grid = ctx->num_sms * 16;
-  act_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)u, T, F, swiglu, (__nv_bfloat16*)out);
+  launch_k(act_kernel, grid, 256, 0, (cudaStream_t)stream, (const __nv_bfloat16*)u, T, F, swiglu, (__nv_bfloat16*)out);
   ctx->launches++;
   return mace_check_launch(ctx, "act");
 }
 
 extern "C" int mace_argmax(mace_ctx* ctx, const float* logits, int n, int V, int ld, int* out, void* stream) {
   if (n <= 0) return 0;
-  argmax_kernel<<<n, 1024, 0, (cudaStream_t)stream>>>(logits, V, ld, out);
+  launch_k(argmax_kernel, n, 1024, 0, (cudaStream_t)stream, logits, V, ld, out);
   ctx->launches++;
   return mace_check_launch(ctx, "argmax");
 }

@@ -74,6 +74,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -248,6 +250,8 @@ __global__ void __launch_bounds__(256, 1)
 // mode: EPI_BF16 -> bf16 store, EPI_F32 -> fp32 store, EPI_F32_ADD -> fp32 +=
 __global__ void gemm_finalize(const float* __restrict__ ws, int splits, int M, int N, void* __restrict__ out, int ldo,
                               int mode) {
+  pdl_wait();
+  pdl_trigger();
   const size_t total = (size_t)M * N;
   const size_t slab = total;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -304,7 +308,7 @@ static int launch_gemm(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStre
   }
   const int tiles = p.num_m * p.num_n * p.splits;
   const int grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
-  kern<<<grid, 256, Cfg::kSmemBytes, stream>>>(ma, mb, p);
+  launch_k(kern, grid, 256, Cfg::kSmemBytes, stream, ma, mb, p);
   ctx->launches++;
   return 0;
 }
@@ -378,7 +382,7 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     rc = dispatch_major<64>(ctx, g, splits, stream, ep);
   if (rc) return rc;
   if (need_finalize) {
-    gemm_finalize<<<ctx->num_sms * 4, 256, 0, stream>>>(reinterpret_cast<const float*>(g->workspace), splits, g->M,
+    launch_k(gemm_finalize, ctx->num_sms * 4, 256, 0, stream, reinterpret_cast<const float*>(g->workspace), splits, g->M,
                                                         g->N, g->out, g->ldo, g->mode);
     ctx->launches++;
   }

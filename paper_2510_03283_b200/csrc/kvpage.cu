@@ -17,6 +17,8 @@
 namespace mace {
 
 __global__ void decode_alloc_kernel(const int* __restrict__ slots, int n, MaceKvLayout kv) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int H = kv.n_kv_heads;
   if (i >= n * H) return;
@@ -32,12 +34,16 @@ __global__ void decode_alloc_kernel(const int* __restrict__ slots, int n, MaceKv
 }
 
 __global__ void bump_end_kernel(const int* __restrict__ slots, int n, int* __restrict__ dec_end) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dec_end[slots[i]] += 1;
 }
 
 // kept: [n][H] post-tick retained decode slots per head (Engine._exec_decode's rs.kept)
 __global__ void trim_kernel(const int* __restrict__ slots, const int* __restrict__ kept, int n, MaceKvLayout kv) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int H = kv.n_kv_heads;
   if (i >= n * H) return;
@@ -63,6 +69,8 @@ __global__ void trim_kernel(const int* __restrict__ slots, const int* __restrict
 }
 
 __global__ void release_kernel(const int* __restrict__ slots, int n, MaceKvLayout kv) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int H = kv.n_kv_heads;
   if (i >= n * H) return;
@@ -80,6 +88,8 @@ __global__ void release_kernel(const int* __restrict__ slots, int n, MaceKvLayou
 }
 
 __global__ void reset_slot_kernel(const int* __restrict__ slots, int n, MaceKvLayout kv) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) kv.dec_end[slots[i]] = 0;
 }
@@ -88,6 +98,8 @@ __global__ void reset_slot_kernel(const int* __restrict__ slots, int n, MaceKvLa
 // group, every layer, both pools. pool layout [L][pages][16][hd].
 __global__ void page_copy_kernel(const int4* __restrict__ copies, int n, int H, int hd, long long pages_per_layer,
                                  int L, __nv_bfloat16* __restrict__ kp, __nv_bfloat16* __restrict__ vp) {
+  pdl_wait();
+  pdl_trigger();
   const int4 c = copies[blockIdx.x];
   const int row_elems = c.z * hd;
   for (int l = 0; l < L; ++l) {
@@ -110,8 +122,8 @@ extern "C" int mace_kv_decode_alloc(mace_ctx* ctx, const MaceKvLayout* kv, const
   if (n <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   const int tot = n * kv->n_kv_heads;
-  decode_alloc_kernel<<<(tot + 255) / 256, 256, 0, s>>>(slots, n, *kv);
-  bump_end_kernel<<<(n + 255) / 256, 256, 0, s>>>(slots, n, kv->dec_end);
+  launch_k(decode_alloc_kernel, (tot + 255) / 256, 256, 0, s, slots, n, *kv);
+  launch_k(bump_end_kernel, (n + 255) / 256, 256, 0, s, slots, n, kv->dec_end);
   ctx->launches += 2;
   return mace_check_launch(ctx, "kv_decode_alloc");
 }
@@ -120,7 +132,7 @@ extern "C" int mace_kv_trim(mace_ctx* ctx, const MaceKvLayout* kv, const int* sl
                             void* stream) {
   if (n <= 0) return 0;
   const int tot = n * kv->n_kv_heads;
-  trim_kernel<<<(tot + 255) / 256, 256, 0, (cudaStream_t)stream>>>(slots, kept, n, *kv);
+  launch_k(trim_kernel, (tot + 255) / 256, 256, 0, (cudaStream_t)stream, slots, kept, n, *kv);
   ctx->launches++;
   return mace_check_launch(ctx, "kv_trim");
 }
@@ -129,8 +141,8 @@ extern "C" int mace_kv_release(mace_ctx* ctx, const MaceKvLayout* kv, const int*
   if (n <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   const int tot = n * kv->n_kv_heads;
-  release_kernel<<<(tot + 255) / 256, 256, 0, s>>>(slots, n, *kv);
-  reset_slot_kernel<<<(n + 255) / 256, 256, 0, s>>>(slots, n, *kv);
+  launch_k(release_kernel, (tot + 255) / 256, 256, 0, s, slots, n, *kv);
+  launch_k(reset_slot_kernel, (n + 255) / 256, 256, 0, s, slots, n, *kv);
   ctx->launches += 2;
   return mace_check_launch(ctx, "kv_release");
 }
@@ -138,7 +150,7 @@ extern "C" int mace_kv_release(mace_ctx* ctx, const MaceKvLayout* kv, const int*
 extern "C" int mace_kv_page_copy(mace_ctx* ctx, const int* copies, int n, int n_kv_heads, int hd, long long pages_per_layer,
                                  int n_layers, void* k_pools, void* v_pools, void* stream) {
   if (n <= 0) return 0;
-  page_copy_kernel<<<n, 128, 0, (cudaStream_t)stream>>>(reinterpret_cast<const int4*>(copies), n, n_kv_heads, hd,
+  launch_k(page_copy_kernel, n, 128, 0, (cudaStream_t)stream, reinterpret_cast<const int4*>(copies), n, n_kv_heads, hd,
                                                         pages_per_layer, n_layers, (__nv_bfloat16*)k_pools,
                                                         (__nv_bfloat16*)v_pools);
   ctx->launches++;
@@ -148,6 +160,8 @@ extern "C" int mace_kv_page_copy(mace_ctx* ctx, const int* copies, int n, int n_
 namespace mace {
 __global__ void set_tables_kernel(const int* __restrict__ slots, const int* __restrict__ tables, int n, int ncols,
                                   int* __restrict__ ptab, int maxpp) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   if (r >= n) return;
   for (int c = threadIdx.x; c < ncols && c < maxpp; c += blockDim.x)
@@ -155,6 +169,8 @@ __global__ void set_tables_kernel(const int* __restrict__ slots, const int* __re
 }
 __global__ void scatter_tokens_kernel(const int* __restrict__ src, const int* __restrict__ slots, int n,
                                       int* __restrict__ last_token) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) last_token[slots[i]] = src[i];
 }
@@ -163,7 +179,7 @@ __global__ void scatter_tokens_kernel(const int* __restrict__ src, const int* __
 extern "C" int mace_kv_set_prompt_tables(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, const int* tables,
                                          int n, int ncols, void* stream) {
   if (n <= 0) return 0;
-  mace::set_tables_kernel<<<n, 128, 0, (cudaStream_t)stream>>>(slots, tables, n, ncols, const_cast<int*>(kv->ptab),
+  launch_k(mace::set_tables_kernel, n, 128, 0, (cudaStream_t)stream, slots, tables, n, ncols, const_cast<int*>(kv->ptab),
                                                                kv->max_prompt_pages);
   ctx->launches++;
   return mace::mace_check_launch(ctx, "kv_set_prompt_tables");
@@ -172,7 +188,7 @@ extern "C" int mace_kv_set_prompt_tables(mace_ctx* ctx, const MaceKvLayout* kv, 
 extern "C" int mace_scatter_tokens(mace_ctx* ctx, const int* src, const int* slots, int n, int* last_token,
                                    void* stream) {
   if (n <= 0) return 0;
-  mace::scatter_tokens_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(src, slots, n, last_token);
+  launch_k(mace::scatter_tokens_kernel, (n + 255) / 256, 256, 0, (cudaStream_t)stream, src, slots, n, last_token);
   ctx->launches++;
   return mace::mace_check_launch(ctx, "scatter_tokens");
 }
