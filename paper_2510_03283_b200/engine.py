@@ -292,6 +292,11 @@ class GpuEngine(Engine):
                 return np.zeros((0,) + ((tail,) if tail else ()), i32)
             return np.concatenate(segs).astype(i32, copy=False)
 
+        tokens = cat(tok_seg)
+        if tokens.size and int(tokens.max()) >= c.vocab:
+            raise ValueError(f"token id {int(tokens.max())} >= model vocab {c.vocab} "
+                             "(TraceConfig.vocab_size must not exceed the model's vocabulary)")
+
         def arr(x, tail):
             a = np.asarray(x, dtype=i32)
             return a.reshape(-1, tail)
@@ -303,7 +308,7 @@ class GpuEngine(Engine):
                 raise RuntimeError("prompt longer than max_prompt_len")
             pt[i, : len(t)] = t
         return TickBatch(
-            tokens=cat(tok_seg), pos=cat(pos_seg), row_seq=cat(seq_seg), row_kvi=cat(kvi_seg),
+            tokens=tokens, pos=cat(pos_seg), row_seq=cat(seq_seg), row_kvi=cat(kvi_seg),
             seqs=arr(seqs, 8), tc_items=cat(tc_seg, 4), dec_items=dec_items,
             dec_slots=dec_slots.astype(i32), dec_rows=dec_rows, ptab_slots=np.asarray(ptab_slots, i32), ptab_rows=pt,
             page_copies=arr(copies, 4), ft0=ft0, ft_pairs=pairs, ft_logit_rows=cat(lr_seg),
