@@ -42,8 +42,12 @@ restore(model, snap)
 model.replay(tape)
 restore(model, snap)
 torch.cuda.synchronize()
+model.instrument = []  # record the algorithmic bytes of every decode-attention launch (per layer, in order)
 torch.cuda.profiler.start()
 model.replay(tape)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
+import json  # noqa: E402
+Path("gpurun_out").mkdir(exist_ok=True)
+Path("gpurun_out/decode_attn_bytes.json").write_text(json.dumps([b for _, _, b in model.instrument]))
 print("ticks", sum(1 for op in tape if op[0] == "step"), "tokens", sum(op[1].total_tokens for op in tape if op[0] == "step"))
