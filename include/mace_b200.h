@@ -59,6 +59,7 @@ enum mace_epilogue {
   MACE_EPI_F32 = 1,        /* out fp32 = result                                  */
   MACE_EPI_F32_ADD = 2,    /* out fp32 += result (residual stream, grad accumulate) */
   MACE_EPI_F32_ATOMIC = 3, /* out fp32 += result via atomics (shared destination)   */
+  MACE_EPI_BF16_GELU = 4,  /* out bf16 = gelu_tanh(result) (fused GPT-2 MLP activation) */
 };
 typedef struct MaceGemmArgs {
   const void* a; int lda; int a_mn_major;
@@ -142,6 +143,7 @@ typedef struct MaceAttnArgs {
   void* dec_workspace; size_t dec_workspace_bytes;
   int* dec_counters;
   unsigned long long* dec_work;  /* zero-initialised ticket counter, owned by the caller, one per ctx */
+  int decode_impl;    /* 0 auto, 1 CUDA-core streaming kernel, 2 tcgen05 swap-AB kernel */
 } MaceAttnArgs;
 int mace_attn_fwd(mace_ctx* ctx, const MaceAttnArgs* args, void* stream);
 

@@ -49,7 +49,7 @@ class MaceAttnArgs(C.Structure):
         ("out", C.c_void_p), ("lse", C.c_void_p), ("head_norm", C.c_void_p),
         ("scale", C.c_float),
         ("dec_workspace", C.c_void_p), ("dec_workspace_bytes", C.c_size_t), ("dec_counters", C.c_void_p),
-        ("dec_work", C.c_void_p),
+        ("dec_work", C.c_void_p), ("decode_impl", C.c_int),
     ]
 
 

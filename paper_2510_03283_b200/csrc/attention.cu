@@ -299,6 +299,7 @@ static int launch_tc(MaceCtx* ctx, const MaceAttnArgs* a, float scale_log2, cuda
 }
 
 int dispatch_decode2(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStream_t s);
+int dispatch_decode_tc(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStream_t s);
 
 }  // namespace mace
 
@@ -322,7 +323,7 @@ extern "C" int mace_attn_fwd(mace_ctx* ctx, const MaceAttnArgs* a, void* stream)
   }
   if (a->n_dec > 0) {
     if (!a->k_pool || !a->v_pool) return mace_fail(ctx, MACE_ERR_ARG, "attn: decode rows need KV pools");
-    rc = dispatch_decode2(ctx, a, sl2, s);
+    rc = a->decode_impl == 1 ? dispatch_decode2(ctx, a, sl2, s) : dispatch_decode_tc(ctx, a, sl2, s);
     if (rc) return rc;
   }
   return mace_check_launch(ctx, "attn_fwd");

@@ -357,7 +357,7 @@ extern "C" int mace_norm_bwd(mace_ctx* ctx, const float* x, int ldx, const int* 
                              float* dw, float* db, float* workspace, size_t workspace_bytes, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
-  const int rows_per_block = 32;
+  const int rows_per_block = 8;  // one row per warp: n/8 CTAs keep every SM busy
   const int nb = (n + rows_per_block - 1) / rows_per_block;
   if (workspace_bytes < (size_t)nb * 2 * d * 4) return mace_fail(ctx, MACE_ERR_ARG, "norm_bwd: workspace too small");
   const int per_lane = (d + 31) / 32;

@@ -178,6 +178,9 @@ MACE_DEV float2 ffma2(float2 a, float2 b, float2 c) {
         "l"(*reinterpret_cast<unsigned long long*>(&c)));
   return *reinterpret_cast<float2*>(&d);
 }
+MACE_DEV float gelu_tanh(float x) {  // GPT-2 "gelu_new"
+  return 0.5f * x * (1.f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+}
 // bf16x2 (packed in a u32) -> two fp32
 MACE_DEV float2 bf2_to_f2(uint32_t w) { return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u)); }
 MACE_DEV float warp_sum(float v) {

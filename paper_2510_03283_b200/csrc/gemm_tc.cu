@@ -191,7 +191,11 @@ __global__ void __launch_bounds__(256, 1)
             if (col0 + j < p.N) v[j] += __bfloat162float(ep.bias[col0 + j]);
         }
         const bool full = (col0 + 32 <= p.N) && ((ep.ldo & 7) == 0);
-        if (ep.mode == EPI_BF16) {
+        if (ep.mode == EPI_BF16_GELU) {  // fused GPT-2 MLP activation (gelu_tanh) on the up projection
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+        }
+        if (ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU) {
           __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ep_out) + (size_t)row * ep.ldo + col0;
           if (full) {
 #pragma unroll
@@ -258,7 +262,8 @@ __global__ void gemm_finalize(const float* __restrict__ ws, int splits, int M, i
     const size_t r = i / N, c = i % N;
     float v = 0.f;
     for (int sp = 0; sp < splits; ++sp) v += ws[sp * slab + i];
-    if (mode == EPI_BF16) {
+    if (mode == EPI_BF16_GELU) v = gelu_tanh(v);
+    if (mode == EPI_BF16 || mode == EPI_BF16_GELU) {
       reinterpret_cast<__nv_bfloat16*>(out)[r * ldo + c] = __float2bfloat16(v);
     } else if (mode == EPI_F32) {
       reinterpret_cast<float*>(out)[r * ldo + c] = v;
@@ -332,7 +337,7 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 0;  // empty ragged batch: nothing to do
   if ((g->lda & 7) || (g->ldb & 7) || ((uintptr_t)g->a & 15) || ((uintptr_t)g->b & 15))
     return mace_fail(ctx, MACE_ERR_ARG, "gemm: operands need 16-byte aligned rows (ld % 8 == 0)");
-  if (g->mode < EPI_BF16 || g->mode > EPI_F32_ATOMIC) return mace_fail(ctx, MACE_ERR_ARG, "gemm: bad epilogue mode");
+  if (g->mode < EPI_BF16 || g->mode > EPI_BF16_GELU) return mace_fail(ctx, MACE_ERR_ARG, "gemm: bad epilogue mode");
 
   // tile shape / split-K heuristic: fill the 148 SMs
   const int num_m = (g->M + kBM - 1) / kBM;

@@ -95,8 +95,10 @@ class HybridModel:
             decode_pages = max_slots * H * 4
         self.decode_pages = decode_pages
         self.pages_per_layer = prompt_groups * H + decode_pages
-        self.k_pool = torch.empty(L, self.pages_per_layer, PAGE, hd, dtype=torch.bfloat16, device=self.dev)
-        self.v_pool = torch.empty_like(self.k_pool)
+        # zero-initialised: page rows outside a sequence's window are multiplied by exact zeros on the
+        # tensor cores, so they must hold finite values
+        self.k_pool = torch.zeros(L, self.pages_per_layer, PAGE, hd, dtype=torch.bfloat16, device=self.dev)
+        self.v_pool = torch.zeros_like(self.k_pool)
         i32 = dict(dtype=torch.int32, device=self.dev)
         self.ptab = torch.zeros(max_slots, self.maxpp, **i32)
         self.dtab = torch.zeros(max_slots, H, self.maxdp, **i32)
@@ -108,6 +110,7 @@ class HybridModel:
         self.last_token = torch.zeros(max_slots, **i32)
         self.dec_counters = torch.zeros(max_slots * H, **i32)  # decode chunk-merge counters (self-cleaning)
         self.dec_work = torch.zeros(1, dtype=torch.int64, device=self.dev)  # decode ticket counter (monotonic)
+        self.decode_impl = 0  # 0 auto (tcgen05 swap-AB), 1 CUDA-core streaming kernel
         self.kv = MaceKvLayout(
             ptab=self.ptab.data_ptr(), max_prompt_pages=self.maxpp, dtab=self.dtab.data_ptr(),
             max_dec_pages=self.maxdp, dec_base=self.dec_base.data_ptr(), dec_first=self.dec_first.data_ptr(),
@@ -259,13 +262,15 @@ class HybridModel:
             e0.record()
             ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, None, dec_items, lay,
                          kp, vp, o[:T], lse=lse, head_norm=hn, dec_workspace=self.dec_ws,
-                         dec_counters=self.dec_counters, dec_work=self.dec_work)
+                         dec_counters=self.dec_counters, dec_work=self.dec_work,
+                         decode_impl=self.decode_impl)
             e1.record()
             self.instrument.append((e0, e1, self._attn_bytes))
         else:
             ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, tc_items, dec_items, lay,
                          kp, vp, o[:T], lse=lse, head_norm=hn, dec_workspace=self.dec_ws,
-                         dec_counters=self.dec_counters, dec_work=self.dec_work)
+                         dec_counters=self.dec_counters, dec_work=self.dec_work,
+                         decode_impl=self.decode_impl)
         if save is not None:
             n = T - ft0
             save["h1"][:n].copy_(h[ft0:T])
@@ -276,9 +281,13 @@ class HybridModel:
         if save is not None:
             save["x_mid"][: T - ft0].copy_(x[ft0:T])
         self._norm(x, c.d_model, None, T, p + "mlp_norm.w", W, h, c.d_model)
-        self._gemm(h[:T], W[p + "up.w"], u[:T], "bf16", bias("up"))
-        self._chk(self.ctx.L.mace_act(self.ctx.h, u.data_ptr(), T, c.ffn, int(c.family == "llama"), a.data_ptr(),
-                                      self._s), "act")
+        if c.family == "gpt2" and save is None:
+            # GELU fused into the up-projection epilogue (no pre-activation needed without a backward)
+            self._gemm(h[:T], W[p + "up.w"], a[:T], "bf16_gelu", bias("up"))
+        else:
+            self._gemm(h[:T], W[p + "up.w"], u[:T], "bf16", bias("up"))
+            self._chk(self.ctx.L.mace_act(self.ctx.h, u.data_ptr(), T, c.ffn, int(c.family == "llama"),
+                                          a.data_ptr(), self._s), "act")
         if save is not None:
             n = T - ft0
             save["h2"][:n].copy_(h[ft0:T])

@@ -11,7 +11,7 @@ import torch
 
 from ._lib import Ctx, MaceGemmArgs
 
-EPI = {"bf16": 0, "f32": 1, "f32_add": 2, "f32_atomic": 3}
+EPI = {"bf16": 0, "f32": 1, "f32_add": 2, "f32_atomic": 3, "bf16_gelu": 4}
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -55,10 +55,10 @@ def gemm(
         N, Kb = b.shape
     assert Kb == K, f"K mismatch {K} vs {Kb}"
     if out is None:
-        assert mode in ("bf16", "f32")
-        out = torch.empty(M, N, device=a.device, dtype=torch.bfloat16 if mode == "bf16" else torch.float32)
+        assert mode in ("bf16", "f32", "bf16_gelu")
+        out = torch.empty(M, N, device=a.device, dtype=torch.float32 if mode == "f32" else torch.bfloat16)
     assert out.shape[0] >= M and out.shape[1] >= N and out.stride(1) == 1
-    assert out.dtype == (torch.bfloat16 if mode == "bf16" else torch.float32)
+    assert out.dtype == (torch.bfloat16 if mode in ("bf16", "bf16_gelu") else torch.float32)
     if bias is not None:
         assert bias.dtype == torch.bfloat16 and bias.numel() == N
     g = MaceGemmArgs(
@@ -92,6 +92,7 @@ def attn_fwd(
     dec_workspace: torch.Tensor | None = None,
     dec_counters: torch.Tensor | None = None,
     dec_work: torch.Tensor | None = None,
+    decode_impl: int = 0,
 ) -> torch.Tensor:
     """Ragged paged attention of one tick (prefill + FT tiles on tcgen05, decode rows streamed)."""
     from ._lib import MaceAttnArgs
@@ -108,7 +109,7 @@ def attn_fwd(
         out=out.data_ptr(), lse=_ptr(lse), head_norm=_ptr(head_norm), scale=0.0,
         dec_workspace=_ptr(dec_workspace),
         dec_workspace_bytes=0 if dec_workspace is None else dec_workspace.numel() * dec_workspace.element_size(),
-        dec_counters=_ptr(dec_counters), dec_work=_ptr(dec_work),
+        dec_counters=_ptr(dec_counters), dec_work=_ptr(dec_work), decode_impl=int(decode_impl),
     )
     ctx.check(ctx.L.mace_attn_fwd(ctx.h, C.byref(a), _stream(stream)), "mace_attn_fwd")
     return out

@@ -124,8 +124,9 @@ def _reference(host, Hq, Hkv, hd, T):
     return out
 
 
-@pytest.mark.parametrize("hd,Hq,Hkv", [(32, 8, 8), (64, 12, 12), (64, 32, 8), (128, 8, 2)])
-def test_attention_ragged(ctx, hd, Hq, Hkv):
+@pytest.mark.parametrize("impl", [1, 2])
+@pytest.mark.parametrize("hd,Hq,Hkv", [(32, 8, 8), (64, 12, 12), (64, 32, 8), (128, 8, 2), (128, 32, 8)])
+def test_attention_ragged(ctx, hd, Hq, Hkv, impl):
     host, d, lay, T = _build(hd, Hq, Hkv, seed=hd + Hq)
     out = torch.zeros(T, Hq * hd, dtype=torch.bfloat16, device="cuda")
     hn = torch.zeros(T, Hq, device="cuda")
@@ -133,7 +134,7 @@ def test_attention_ragged(ctx, hd, Hq, Hkv):
     for _ in range(2):  # twice: the chunk-merge counters must come back zeroed
         ops.attn_fwd(ctx, d["qkv"], Hq, Hkv, hd, d["seqs"], d["tc_items"], d["dec_items"], lay, d["kp"], d["vp"], out,
                      lse=lse, head_norm=hn, dec_workspace=d["dec_ws"], dec_counters=d["dec_cnt"],
-                     dec_work=d["dec_work"])
+                     dec_work=d["dec_work"], decode_impl=impl)
     assert int(d["dec_cnt"].abs().sum()) == 0
     torch.cuda.synchronize()
     ref = _reference(host, Hq, Hkv, hd, T)

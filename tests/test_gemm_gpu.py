@@ -54,6 +54,9 @@ def test_gemm_epilogues(ctx, M, N, K):
     ref = a.float() @ b.float().t()
     y = ops.gemm(ctx, a, b, mode="bf16", bias=bias)
     assert torch.allclose(y.float(), (ref + bias.float()), atol=0.1, rtol=1e-2)
+    g = ops.gemm(ctx, a, b, mode="bf16_gelu", bias=bias)
+    gref = torch.nn.functional.gelu(ref + bias.float(), approximate="tanh")
+    assert torch.allclose(g.float(), gref, atol=0.1, rtol=1e-2)
     acc = torch.randn(M, N, device="cuda")
     acc0 = acc.clone()
     ops.gemm(ctx, a, b, acc, mode="f32_add", alpha=0.5)
