@@ -71,7 +71,7 @@ class ClockSampler:
                 r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
             except Exception:
                 r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-            self.samples.append((sm, r))
+            self.samples.append((time.perf_counter(), sm, r))
             time.sleep(0.002)
 
     def __enter__(self):
@@ -90,12 +90,16 @@ class ClockSampler:
         if self.t is not None:
             self.t.join()
 
-    def summary(self):
-        if not self.samples:
+    def summary(self, t0: float | None = None, t1: float | None = None):
+        """Samples inside the timed window [t0, t1] (host perf_counter); all samples if no window."""
+        smp = [(s, r) for t, s, r in self.samples if (t0 is None or t >= t0) and (t1 is None or t <= t1)]
+        if not smp:  # window shorter than one NVML poll: take the nearest samples around it
+            smp = [(s, r) for t, s, r in self.samples][-3:]
+        if not smp:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
-        reasons = sorted({n for _, r in self.samples for bit, n in self.REASONS.items() if r & bit})
-        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples)}
+        reasons = sorted({n for _, r in smp for bit, n in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in smp), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(smp)}
 
 
 def snapshot(model):
@@ -172,21 +176,25 @@ def run_ours(args, rank, world, lock):
     d2h = (eng.d2h_bytes - d2h0) / max(done, 1)
     # ---- value: replay the same device calls from the snapshot (inputs resident), CUDA events
     launches0 = model.ctx.launches
+    clk = ClockSampler(local).__enter__()  # sampling runs through the warm replay and the timed region
     restore(model, snap)
     model.replay(tape)  # warm replay
     restore(model, snap)
     torch.cuda.synchronize()
     lock.barrier()
-    with ClockSampler(local) as clk:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        l0 = model.ctx.launches
-        model.replay(tape)
-        ev1.record()
-        ev1.synchronize()
-        launches = model.ctx.launches - l0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_on = time.perf_counter()
+    ev0.record()
+    l0 = model.ctx.launches
+    model.replay(tape)
+    ev1.record()
+    ev1.synchronize()
+    t_off = time.perf_counter()
+    launches = model.ctx.launches - l0
+    time.sleep(0.01)
+    clk.__exit__()
     dev_ms = lock.max_over_ranks(ev0.elapsed_time(ev1))
-    clocks = clk.summary()
+    clocks = clk.summary(t_on, t_off)
     # ---- roofline of the dominant kernel: paged decode attention, per-launch CUDA events
     restore(model, snap)
     hbm_peak, tc_peak, peak_src = _peaks()

@@ -323,7 +323,10 @@ extern "C" int mace_attn_fwd(mace_ctx* ctx, const MaceAttnArgs* a, void* stream)
   }
   if (a->n_dec > 0) {
     if (!a->k_pool || !a->v_pool) return mace_fail(ctx, MACE_ERR_ARG, "attn: decode rows need KV pools");
-    rc = a->decode_impl == 1 ? dispatch_decode2(ctx, a, sl2, s) : dispatch_decode_tc(ctx, a, sl2, s);
+    // auto: GQA groups (G >= 2) run on the tcgen05 swap-AB kernel (the CUDA-core kernel is issue-bound
+    // there, G dots per K row); plain MHA (G = 1) keeps the CUDA-core streaming kernel (measured faster)
+    const int impl = a->decode_impl ? a->decode_impl : (a->Hq / a->Hkv >= 2 ? 2 : 1);
+    rc = impl == 1 ? dispatch_decode2(ctx, a, sl2, s) : dispatch_decode_tc(ctx, a, sl2, s);
     if (rc) return rc;
   }
   return mace_check_launch(ctx, "attn_fwd");

@@ -64,6 +64,11 @@ MACE_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// named barrier among `count` threads (id 1..15; 0 is __syncthreads)
+MACE_DEV void named_bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 MACE_DEV void fence_proxy_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -40,7 +40,7 @@ from macesim.engine import Engine  # noqa: E402
 from macesim.workload import WorkloadType  # noqa: E402
 
 
-DECODE_CHUNK_PAGES = 32  # long decode contexts are split into chunks of <= 32 prompt pages (512 tokens)
+DECODE_CHUNK_PAGES = 128  # decode contexts longer than 2048 tokens are split into chunks (merged on device)
 
 
 def synthetic_pair_tokens(seed: int, rid: int, n_c: int, n_r: int, vocab: int) -> tuple[list[int], list[int]]:
