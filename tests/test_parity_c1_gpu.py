@@ -4,9 +4,10 @@
 Tolerances (bf16 storage / fp32 accumulation vs an fp32 oracle on the same bf16 weights):
   decode logits        rel-L2 <= 1e-2
   decode token ids     bit-exact except oracle near-ties (top-1/top-2 gap < 0.05, counted, <= 5%)
-  sequence log-probs   |d lp| <= 5e-4*|lp| + 1e-3*n + 1e-2*sqrt(n) + 0.02 for a sum of n token
-                       log-probs: each token's log-prob inherits the ~1e-2 absolute logit error that the
-                       1e-2 logits rel-L2 bound allows (random part ~sqrt(n), systematic part ~n); the
+  sequence log-probs   |d lp| <= 5e-4*|lp| + 2e-3*n + 2.5e-2*sqrt(n) + 0.02 for a sum of n token
+                       log-probs: each token's log-prob inherits the absolute logit error the bf16 path has
+                       at the model's logit scale (GPT-2 random init: logit std ~2.8, error up to ~0.05 on a
+                       single token; random part ~sqrt(n), systematic part ~n); the
                        relative part covers the slight systematic shrink of fp32-accumulated tensor-core
                        dot products (observed ~1e-4 |lp| on GPT-2 / Llama shapes)
   DPO margin           |d m|  <= sum of the four log-prob tolerances; loss |d L| <= beta * |d m|
@@ -58,7 +59,7 @@ def test_c1_every_tick_matches_oracle(ctx):
             for i, (lc, lr_, rc, rr) in enumerate(orc.ex.last_lp):
                 g_lp, g_ref = rec["ft_lp"][i], rec["ref_lp"][i]
                 nc, nr = int(b.pair_rows[i, 1]), int(b.pair_rows[i, 3])
-                tol = [5e-4 * abs(x) + 1e-3 * n + 1e-2 * n ** 0.5 + 0.02
+                tol = [5e-4 * abs(x) + 2e-3 * n + 2.5e-2 * n ** 0.5 + 0.02
                        for x, n in zip((lc, lr_, rc, rr), (nc, nr, nc, nr))]
                 for a, o, t in zip((g_lp[0], g_lp[1], g_ref[0], g_ref[1]), (lc, lr_, rc, rr), tol):
                     assert abs(a - o) <= t, f"tick {rec['tick']}: log-prob {a} vs {o}"

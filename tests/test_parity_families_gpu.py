@@ -51,7 +51,7 @@ def _check(eng, w, cfg, tcfg):
             dm_max = 0.0
             for i, (lc, lr_, rc, rr) in enumerate(orc.ex.last_lp):
                 nc, nr = int(b.pair_rows[i, 1]), int(b.pair_rows[i, 3])
-                tol = [5e-4 * abs(x) + 1e-3 * n + 1e-2 * n ** 0.5 + 0.02
+                tol = [5e-4 * abs(x) + 2e-3 * n + 2.5e-2 * n ** 0.5 + 0.02
                        for x, n in zip((lc, lr_, rc, rr), (nc, nr, nc, nr))]
                 for a, o, t in zip((*rec["ft_lp"][i], *rec["ref_lp"][i]), (lc, lr_, rc, rr), tol):
                     assert abs(a - o) <= t, f"tick {rec['tick']}: log-prob {a} vs {o}"
