@@ -188,6 +188,7 @@ def run_ours(args, rank, world, lock):
     l0 = model.ctx.launches
     model.replay(tape)
     ev1.record()
+    t_issued = time.perf_counter()
     ev1.synchronize()
     t_off = time.perf_counter()
     launches = model.ctx.launches - l0
@@ -245,6 +246,7 @@ def run_ours(args, rank, world, lock):
         "clocks": clocks,
         "tpot_reference_clock_ms": {"p50": lat["tbt_p50"], "p99": lat["tbt_p99"]},
         "device_ms_per_tick": one_tick_ms,
+        "host_issue_ms_per_tick": (t_issued - t_on) * 1e3 / max(done, 1),
         "finetune_samples_per_s": None,
     }
     n_ft_ticks = sum(1 for op in tape if op[0] == "step" and op[1].ft_pairs)

@@ -33,6 +33,7 @@ extern "C" {
 #endif
 
 typedef struct mace_ctx mace_ctx;
+typedef struct mace_model mace_model;  /* native tick executor (section 5) */
 
 enum mace_status {
   MACE_OK = 0,
@@ -186,6 +187,74 @@ int mace_kv_page_copy(mace_ctx* ctx, const int* copies, int n, int n_kv_heads, i
 int mace_kv_set_prompt_tables(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, const int* tables, int n,
                               int ncols, void* stream);
 int mace_scatter_tokens(mace_ctx* ctx, const int* src, const int* slots, int n, int* last_token, void* stream);
+
+/* ---------------------------------------------------------------- (5) native tick executor
+ * One call issues a whole hybrid tick, i.e. the device work the reference charges for one bin in
+ * Engine._execute (engine.py:573-676): page-table maintenance, embed, every decoder layer over the
+ * ragged [prefill | decode | FT] batch, the decode head (final norm -> lm_head -> greedy token ->
+ * last_token scatter) and, for FT rows, the pi_ref and policy sub-passes over the selected layers,
+ * the fused DPO loss and the backward of the selected layers into the flat fp32 gradient.  The
+ * optimizer step stays a separate call (mace_adamw_masked) so a gradient all-reduce can sit between.
+ * All launches go to `stream` in order; nothing synchronizes.                                      */
+typedef struct MaceLayerWeights {          /* bf16 device pointers; biases / norm bias NULL for llama */
+  const void *attn_norm_w, *attn_norm_b, *qkv_w, *qkv_b, *o_w, *o_b;
+  const void *mlp_norm_w, *mlp_norm_b, *up_w, *up_b, *down_w, *down_b;
+} MaceLayerWeights;
+typedef struct MaceLayerGrads {            /* fp32 views into the flat gradient (NULL: not trained) */
+  float *attn_norm_w, *attn_norm_b, *qkv_w, *qkv_b, *o_w, *o_b;
+  float *mlp_norm_w, *mlp_norm_b, *up_w, *up_b, *down_w, *down_b;
+} MaceLayerGrads;
+typedef struct MaceModelDesc {
+  int family;                              /* 0 llama (RMSNorm, RoPE, SwiGLU), 1 gpt2 (LayerNorm, GELU) */
+  int n_layers, d_model, n_heads, n_kv_heads, head_dim, ffn, up_dim, vocab;
+  float norm_eps, dpo_beta;
+  const void *embed, *pos_embed, *final_norm_w, *final_norm_b;
+  const MaceLayerWeights* layers;          /* [n_layers] working weights (updated in place by AdamW) */
+  int n_sel; const int* sel_layers;        /* [n_sel] ascending selected (trained) layers          */
+  const MaceLayerWeights* ref_layers;      /* [n_sel] frozen pi_ref copies of the selected layers  */
+  const void *ref_final_norm_w, *ref_final_norm_b;  /* frozen pi_ref final norm                 */
+  const MaceLayerGrads* grads;             /* [n_sel] */
+  float *grad_final_norm_w, *grad_final_norm_b;
+  float* grad_flat; long long n_grad;      /* zeroed by the tick before the backward               */
+  const float *cos_t, *sin_t;              /* RoPE tables [max_pos][head_dim/2]                    */
+  MaceKvLayout kv;
+  void *k_pool, *v_pool; long long pages_per_layer;
+  int* last_token;                         /* [slots] previous greedy token of each slot           */
+  int* dec_counters; unsigned long long* dec_work;
+  int decode_impl;                         /* see MaceAttnArgs */
+} MaceModelDesc;
+typedef struct MaceSavedActs {             /* policy activations of one selected layer (FT rows)   */
+  float* x_in; void* h1; void* qkv; void* o; float* lse; float* x_mid; void* h2; void* u; void* a;
+} MaceSavedActs;
+typedef struct MaceTickBuffers {           /* device scratch sized by the caller for this tick;    */
+                                           /* ld_vocab: row stride (>= vocab, multiple of 8) of     */
+                                           /* ft_logits, dlogits and dec_logits                     */
+  float* x; void *h, *qkv, *o; float *lse, *hn; void *u, *a;   /* [T, .] ragged batch          */
+  MaceSavedActs* sav;                      /* host array [n_sel]                                   */
+  float *rx, *rx2, *x_lmin, *rlse; void *rh, *rqkv, *ro, *ru, *ra;  /* FT sub-batch [n_ft, .]   */
+  float *dx; void* dy16; float* df; int ld_df; void *da16, *du16, *do16; float* dqkv; void* dqkv16;
+  float* Dbuf;
+  void* ft_h; float* ft_logits; void* dlogits; int ld_vocab; float *dh, *row_lse, *row_lp;  /* [R, .] */
+  void* dec_h; float* dec_logits; int* dec_tok; float* dec_ws; size_t dec_ws_bytes;        /* [n_dec, .] */
+  float *lp, *ref_lp, *loss, *margin, *coef;  /* [n_pairs][2] / [n_pairs] DPO outputs           */
+  float* ws; size_t ws_bytes;              /* split-K / reduction scratch                          */
+} MaceTickBuffers;
+typedef struct MaceTickDesc {              /* device row tables of one tick (see TickBatch)        */
+  int T, ft0, n_dec, R, n_pairs, need_ref; /* need_ref 0: ref_cached holds pi_ref log-probs       */
+  const int *tokens, *pos, *row_seq, *row_kvi; const MaceSeq* seqs;
+  const int* tc_items; int n_tc, n_tc_inference;   /* FT tiles follow the first n_tc_inference   */
+  const int* dec_items; int n_dec_items;
+  const int *dec_slots, *dec_rows;
+  const int *ptab_slots, *ptab_rows; int n_ptab, ptab_cols;
+  const int* page_copies; int n_copies;
+  const int *ft_local_rows, *ft_targets, *pair_rows, *row_ps; const float* ref_cached;
+  const MaceSeq* ft_seqs; const int* ft_tc_items; int n_ft_tc; const int* ft_row_seq;
+  const int* bwd_items; int n_bwd;
+  void** attn_events;                      /* optional cudaEvent_t[2*n_layers] around decode attention */
+} MaceTickDesc;
+int mace_model_create(mace_ctx* ctx, const MaceModelDesc* desc, mace_model** out);
+int mace_model_destroy(mace_model* model);
+int mace_tick_run(mace_model* model, const MaceTickBuffers* bufs, const MaceTickDesc* tick, void* stream);
 
 #ifdef __cplusplus
 }

@@ -10,7 +10,10 @@ import threading
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libmace_b200.so"
+import os  # noqa: E402
+
+# MACE_LIB selects an alternative in-tree build (e.g. the phase-traced GEMM of tools/gemm_trace.py)
+LIB_PATH = _PKG / os.environ.get("MACE_LIB", "libmace_b200.so")
 
 
 class MaceError(RuntimeError):
@@ -53,6 +56,75 @@ class MaceAttnArgs(C.Structure):
     ]
 
 
+_LAYER_FIELDS = ("attn_norm_w", "attn_norm_b", "qkv_w", "qkv_b", "o_w", "o_b",
+                 "mlp_norm_w", "mlp_norm_b", "up_w", "up_b", "down_w", "down_b")
+
+
+class MaceLayerWeights(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in _LAYER_FIELDS]
+
+
+class MaceLayerGrads(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in _LAYER_FIELDS]
+
+
+class MaceModelDesc(C.Structure):
+    _fields_ = [
+        ("family", C.c_int), ("n_layers", C.c_int), ("d_model", C.c_int), ("n_heads", C.c_int),
+        ("n_kv_heads", C.c_int), ("head_dim", C.c_int), ("ffn", C.c_int), ("up_dim", C.c_int), ("vocab", C.c_int),
+        ("norm_eps", C.c_float), ("dpo_beta", C.c_float),
+        ("embed", C.c_void_p), ("pos_embed", C.c_void_p), ("final_norm_w", C.c_void_p), ("final_norm_b", C.c_void_p),
+        ("layers", C.POINTER(MaceLayerWeights)),
+        ("n_sel", C.c_int), ("sel_layers", C.POINTER(C.c_int)),
+        ("ref_layers", C.POINTER(MaceLayerWeights)),
+        ("ref_final_norm_w", C.c_void_p), ("ref_final_norm_b", C.c_void_p),
+        ("grads", C.POINTER(MaceLayerGrads)),
+        ("grad_final_norm_w", C.c_void_p), ("grad_final_norm_b", C.c_void_p),
+        ("grad_flat", C.c_void_p), ("n_grad", C.c_longlong),
+        ("cos_t", C.c_void_p), ("sin_t", C.c_void_p),
+        ("kv", MaceKvLayout),
+        ("k_pool", C.c_void_p), ("v_pool", C.c_void_p), ("pages_per_layer", C.c_longlong),
+        ("last_token", C.c_void_p), ("dec_counters", C.c_void_p), ("dec_work", C.c_void_p),
+        ("decode_impl", C.c_int),
+    ]
+
+
+class MaceSavedActs(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("x_in", "h1", "qkv", "o", "lse", "x_mid", "h2", "u", "a")]
+
+
+class MaceTickBuffers(C.Structure):
+    _fields_ = [
+        *[(n, C.c_void_p) for n in ("x", "h", "qkv", "o", "lse", "hn", "u", "a")],
+        ("sav", C.POINTER(MaceSavedActs)),
+        *[(n, C.c_void_p) for n in ("rx", "rx2", "x_lmin", "rlse", "rh", "rqkv", "ro", "ru", "ra", "dx", "dy16", "df")],
+        ("ld_df", C.c_int),
+        *[(n, C.c_void_p) for n in ("da16", "du16", "do16", "dqkv", "dqkv16", "Dbuf", "ft_h", "ft_logits", "dlogits")],
+        ("ld_vocab", C.c_int),
+        *[(n, C.c_void_p) for n in ("dh", "row_lse", "row_lp", "dec_h", "dec_logits", "dec_tok", "dec_ws")],
+        ("dec_ws_bytes", C.c_size_t),
+        *[(n, C.c_void_p) for n in ("lp", "ref_lp", "loss", "margin", "coef", "ws")],
+        ("ws_bytes", C.c_size_t),
+    ]
+
+
+class MaceTickDesc(C.Structure):
+    _fields_ = [
+        *[(n, C.c_int) for n in ("T", "ft0", "n_dec", "R", "n_pairs", "need_ref")],
+        *[(n, C.c_void_p) for n in ("tokens", "pos", "row_seq", "row_kvi", "seqs", "tc_items")],
+        ("n_tc", C.c_int), ("n_tc_inference", C.c_int),
+        ("dec_items", C.c_void_p), ("n_dec_items", C.c_int),
+        ("dec_slots", C.c_void_p), ("dec_rows", C.c_void_p),
+        ("ptab_slots", C.c_void_p), ("ptab_rows", C.c_void_p), ("n_ptab", C.c_int), ("ptab_cols", C.c_int),
+        ("page_copies", C.c_void_p), ("n_copies", C.c_int),
+        *[(n, C.c_void_p) for n in ("ft_local_rows", "ft_targets", "pair_rows", "row_ps", "ref_cached", "ft_seqs",
+                                    "ft_tc_items")],
+        ("n_ft_tc", C.c_int),
+        ("ft_row_seq", C.c_void_p), ("bwd_items", C.c_void_p), ("n_bwd", C.c_int),
+        ("attn_events", C.c_void_p),
+    ]
+
+
 # MaceSeq is 8 x int32 (see include/mace_b200.h); built as numpy/torch int32 [S, 8] arrays
 SEQ_FIELDS = ("kind", "q_start", "q_len", "slot", "n_pv", "kv_len", "out_row", "pad")
 
@@ -89,6 +161,9 @@ SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_kv_page_copy": (C.c_int, [_vp, _ip, _i, _i, _i, C.c_longlong, _i, _vp, _vp, _vp]),
     "mace_kv_set_prompt_tables": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _ip, _i, _i, _vp]),
     "mace_scatter_tokens": (C.c_int, [_vp, _ip, _ip, _i, _ip, _vp]),
+    "mace_model_create": (C.c_int, [_vp, C.POINTER(MaceModelDesc), C.POINTER(C.c_void_p)]),
+    "mace_model_destroy": (C.c_int, [_vp]),
+    "mace_tick_run": (C.c_int, [_vp, C.POINTER(MaceTickBuffers), C.POINTER(MaceTickDesc), _vp]),
 }
 
 _lib = None

@@ -76,6 +76,11 @@ class TickBatch:
 
     def packed(self) -> tuple[np.ndarray, dict[str, tuple[int, tuple[int, ...]]]]:
         """Concatenate every int32 table (16-byte aligned segments) -> (buffer, {name: (offset, shape)})."""
+        local_rows = (self.ft_logit_rows - self.ft0).astype(np.int32)
+        if self.ft_pairs and all(p.ref_lp is not None for p in self.ft_pairs):
+            ref_cached = np.array([p.ref_lp for p in self.ft_pairs], np.float32).view(np.int32)
+        else:
+            ref_cached = np.zeros((0, 2), np.int32)
         parts = [
             ("tokens", self.tokens), ("pos", self.pos), ("row_seq", self.row_seq), ("row_kvi", self.row_kvi),
             ("seqs", self.seqs), ("tc_items", self.tc_items), ("dec_items", self.dec_items),
@@ -84,6 +89,7 @@ class TickBatch:
             ("ft_logit_rows", self.ft_logit_rows), ("ft_targets", self.ft_targets), ("pair_rows", self.pair_rows),
             ("row_ps", self.row_ps), ("ft_seqs", self.ft_seqs), ("ft_tc_items", self.ft_tc_items),
             ("ft_row_seq", self.ft_row_seq), ("bwd_items", self.bwd_items),
+            ("ft_local_rows", local_rows), ("ref_cached", ref_cached),  # fp32 bits of cached pi_ref log-probs
         ]
         layout = {}
         off = 0

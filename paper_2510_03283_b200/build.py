@@ -27,24 +27,26 @@ def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+def _stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = sources() + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [PKG.parent / "include" / "mace_b200.h"]
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
-    objdir = PKG / "build"
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines: tuple[str, ...] = ()) -> Path:
+    """variant "": the product library; otherwise libmace_b200_<variant>.so built with extra -D defines."""
+    lib = LIB if not variant else PKG / f"libmace_b200_{variant}.so"
+    if not force and not _stale(lib):
+        return lib
+    objdir = PKG / ("build" if not variant else f"build_{variant}")
     objdir.mkdir(exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = objdir / (src.stem + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, "-I", str(CSRC), "-I", str(PKG.parent / "include"), "-c", str(src), "-o", str(obj)]
+        cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(CSRC), "-I", str(PKG.parent / "include"), "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
@@ -58,13 +60,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             print(out)
     if failed:
         raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *map(str, objs)]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -1,6 +1,7 @@
 // Shared sm_100a device helpers: mbarrier, TMA (cp.async.bulk[.tensor]), tcgen05 / TMEM.
 // Everything here is raw PTX so the SASS is auditable (UTCHMMA / UTMALDG / LDTM / UBLKCP).
 #pragma once
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -53,6 +54,7 @@ MACE_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 MACE_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
+#ifdef MACE_MBAR_SUSPEND_HINT
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
@@ -62,6 +64,17 @@ MACE_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
       "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
       "r"(phase), "r"(0x989680)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+#endif
 }
 
 // named barrier among `count` threads (id 1..15; 0 is __syncthreads)
@@ -84,6 +97,32 @@ MACE_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// TMA stores / reductions from shared memory (bulk-group completion; see bulk_commit / bulk_wait_read)
+MACE_DEV void tma_store_2d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+MACE_DEV void tma_store_3d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+// global (+)= smem tile (fp32 add performed at L2; exact fp32 sum with one rounding per element)
+MACE_DEV void tma_reduce_add_2d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+MACE_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+MACE_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+template <int N>
+MACE_DEV void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+
 // 1-D bulk copy global -> shared (size multiple of 16, both 16-byte aligned)
 MACE_DEV void bulk_load(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -203,7 +242,16 @@ MACE_DEV uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// host: launch with the PDL attribute (cudaLaunchKernelEx)
+// host: launch with the PDL attribute (cudaLaunchKernelEx). MACE_NO_PDL=1 in the environment turns it
+// off (profiling: with PDL a kernel's measured duration includes its wait on the predecessor).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MACE_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                             Args&&... args) {
@@ -216,7 +264,7 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

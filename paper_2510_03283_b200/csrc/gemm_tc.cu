@@ -12,6 +12,9 @@
 //  * warps 4..7: epilogue, tcgen05.ld 32x32b -> registers -> fused bias / residual / convert
 //  * operands may be K-major (row-major [rows, K]) or MN-major (row-major [K, rows]); the MN-major
 //    form is what the fine-tune backward needs (dX = dY.W and dW = dY^T.X) without transposes.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "mace_internal.h"
 
@@ -25,28 +28,60 @@ struct GemmCfg {
   static constexpr int kABytes = kBM * kBK * 2;  // 16 KB
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  // epilogue staging for the TMA-store path: 4 warps x 2 buffers x (32 rows x 128 B)
+  static constexpr int kCBytes = 4 * 2 * 4096;
+  static constexpr int kBudget = 227 * 1024 - kCBytes - 1024 /*align*/ - 256 /*barriers*/;
+  static constexpr int kStages = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
   static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kCBytes + 1024 + 256;
 };
 
 struct GemmParams {
   int M, N, K;
   int num_m, num_n, splits, kb_total, kb_per_split;
+  int c_reduce;  // TMA epilogue: 1 -> global += tile (cp.reduce.async.bulk .add)
+  int c_slab;    // TMA epilogue: 1 -> per-split fp32 slabs through a 3-D map {N, M, splits}
+  int dbg;       // trace builds only (tools/gemm_trace.py probes); 0 otherwise
   GemmEpilogue ep;
 };
 
-template <int BN, bool A_MN, bool B_MN>
+// Epilogue chunk of one warp (32 rows) through smem and a TMA store: registers -> 128B-swizzled
+// [32 rows][128 B] staging (conflict-free: 16-byte chunk q of row r lives at q ^ (r & 7)) ->
+// cp.async.bulk.tensor store (or .add reduction) of a {cols, 32 rows} box. Coalesced, asynchronous,
+// bounds-clipped by the tensor map, so the epilogue no longer issues 32 row-strided stores per warp.
+MACE_DEV void stage_row_chunk16(uint8_t* st, uint32_t lane, int q, uint4 w) {
+  *reinterpret_cast<uint4*>(st + lane * 128 + ((q ^ (lane & 7)) << 4)) = w;
+}
+
+#ifdef MACE_GEMM_TRACE
+// phase timestamps (%globaltimer ns) per CTA, tools/gemm_trace.py: [cta][32]
+__device__ unsigned long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ void trace_at(int slot) {
+  if (g_gemm_trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gemm_trace[blockIdx.x * 64 + slot] = t;
+    g_gemm_trace[blockIdx.x * 64 + 32 + slot] = clock64();  // SM cycles (same-CTA differences)
+  }
+}
+#define TRACE(slot) trace_at(slot)
+static int g_gemm_dbg_host = 0;  // 1: TMA only for the first ring pass (MMA-rate probe), 2: no MMA (TMA-rate probe)
+#else
+#define TRACE(slot)
+#endif
+
+template <int BN, bool A_MN, bool B_MN, bool TMA_EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   const GemmParams p) {
+                   const __grid_constant__ CUtensorMap map_c, const GemmParams p) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + S * Cfg::kABytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint8_t* smem_c = smem + S * Cfg::kStageBytes;  // epilogue staging (TMA_EPI)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_c + Cfg::kCBytes);
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -55,10 +90,12 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int num_tiles = p.num_m * p.num_n * p.splits;
+  if (threadIdx.x == 0) TRACE(0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
+    if (TMA_EPI) tma_prefetch_desc(&map_c);
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -74,22 +111,33 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(1);
   pdl_wait();
   pdl_trigger();
+  if (threadIdx.x == 0) TRACE(2);
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------ TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m_blk = t % p.num_m;
-        const int n_blk = (t / p.num_m) % p.num_n;
-        const int split = t / (p.num_m * p.num_n);
-        const int kb0 = split * p.kb_per_split;
-        const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+    // ------------------------------------------------ TMA producer (whole warp walks the schedule so
+    // every index is warp-uniform and lives in uniform registers; one elected lane issues)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m_blk = t % p.num_m;
+      const int n_blk = (t / p.num_m) % p.num_n;
+      const int split = t / (p.num_m * p.num_n);
+      const int kb0 = split * p.kb_per_split;
+      const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
+#ifdef MACE_GEMM_TRACE
+        if (p.dbg == 4 && (kb - kb0) >= S) break;
+#endif
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (elect_one()) {
+#ifdef MACE_GEMM_TRACE
+          if ((p.dbg == 1 || p.dbg == 3) && (kb - kb0) >= S) {
+            mbar_arrive(&full_bar[stage]);
+          } else {
+#endif
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           uint8_t* sa = smem_a + stage * Cfg::kABytes;
           uint8_t* sb = smem_b + stage * Cfg::kBBytes;
@@ -100,6 +148,9 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < kBM / 64; ++j)
               tma_load_2d(sa + j * (64 * kBK * 2), &map_a, &full_bar[stage], m_blk * kBM + j * 64, kb * kBK);
           }
+#ifdef MACE_GEMM_TRACE
+          if (t == (int)blockIdx.x && kb == kb0) TRACE(3);
+#endif
           if (!B_MN) {
             tma_load_2d(sb, &map_b, &full_bar[stage], kb * kBK, n_blk * BN);
           } else {
@@ -107,33 +158,44 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < BN / 64; ++j)
               tma_load_2d(sb + j * (64 * kBK * 2), &map_b, &full_bar[stage], n_blk * BN + j * 64, kb * kBK);
           }
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
+#ifdef MACE_GEMM_TRACE
           }
+#endif
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer (single thread)
-      constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN, A_MN, B_MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int split = t / (p.num_m * p.num_n);
-        const int kb0 = split * p.kb_per_split;
-        const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+    // ------------------------------------------------ MMA issuer (whole warp; one elected lane issues)
+    constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const uint32_t a_base = smem_u32(smem_a), b_base = smem_u32(smem_b);
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int split = t / (p.num_m * p.num_n);
+      const int kb0 = split * p.kb_per_split;
+      const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+#ifdef MACE_GEMM_TRACE
+        if (!(p.dbg == 4 && (kb - kb0) >= S))
+#endif
+        mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::kABytes);
-          const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
+#ifdef MACE_GEMM_TRACE
+        if (lane == 0 && t == (int)blockIdx.x && kb == kb0) TRACE(4);
+#endif
+        const uint32_t a_addr = a_base + stage * Cfg::kABytes;
+        const uint32_t b_addr = b_base + stage * Cfg::kBBytes;
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             // K-major: advance 16 elems = 32 B inside the swizzle atom; SBO = 8 rows * 128 B.
@@ -142,19 +204,34 @@ __global__ void __launch_bounds__(256, 1)
                                      : smem_desc_sw128(a_addr + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
                                      : smem_desc_sw128(b_addr + k * 32, 16, 1024);
+#ifdef MACE_GEMM_TRACE
+            if (p.dbg == 2) continue;
+            if (p.dbg == 3) {  // independent accumulators for odd k (dependency-latency probe)
+              umma_bf16(d_tmem + ((k & 1) ? ((acc ^ 1) - acc) * BN : 0), ad, bd, idesc, (kb > kb0 || k > 1) ? 1u : 0u);
+              continue;
+            }
+#endif
             umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
+#ifdef MACE_GEMM_TRACE
+          if (!(p.dbg == 4))
+#endif
           umma_commit(&empty_bar[stage]);
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        umma_commit(&tfull_bar[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
         }
+      }
+#ifdef MACE_GEMM_TRACE
+      { const int ti = (t - (int)blockIdx.x) / (int)gridDim.x; if (lane == 0 && ti < 5) TRACE(8 + ti * 4); }
+#endif
+      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
       }
     }
   } else if (warp >= 4) {
@@ -162,6 +239,7 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t quarter = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int stage_buf = 0;
     const GemmEpilogue& ep = p.ep;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int m_blk = t % p.num_m;
@@ -169,6 +247,81 @@ __global__ void __launch_bounds__(256, 1)
       const int split = t / (p.num_m * p.num_n);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+#ifdef MACE_GEMM_TRACE
+      const int ti_ = (t - (int)blockIdx.x) / (int)gridDim.x;
+      if (warp == 4 && lane == 0 && ti_ < 5) TRACE(8 + ti_ * 4 + 1);
+#endif
+      if constexpr (TMA_EPI) {
+        const bool bf16_out = ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU;
+        const int cw = bf16_out ? 64 : 32;  // columns per 128-byte staged row
+        const int row0 = m_blk * kBM + quarter * 32;
+        const bool add_bias = ep.bias != nullptr && split == 0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += cw) {
+          const int col0 = n_blk * BN + c0;
+          if (col0 >= p.N) break;
+          uint32_t r[64];
+          tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + acc * BN + c0, *reinterpret_cast<uint32_t(*)[32]>(r));
+          if (bf16_out)
+            tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + acc * BN + c0 + 32,
+                               *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+          tmem_ld_wait();
+          if (lane == 0) bulk_wait_read<1>();  // staging buffer used two chunks ago has been read
+          __syncwarp();
+          uint8_t* st = smem_c + (quarter * 2 + stage_buf) * 4096;
+          if (bf16_out) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float v[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int c = q * 8 + j;
+                v[j] = __uint_as_float(r[c]) * ep.alpha;
+                if (add_bias && col0 + c < p.N) v[j] += __bfloat162float(ep.bias[col0 + c]);
+                if (ep.mode == EPI_BF16_GELU) v[j] = gelu_tanh(v[j]);
+              }
+              stage_row_chunk16(st, lane, q, make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                                                        pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7])));
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float v[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int c = q * 4 + j;
+                v[j] = __uint_as_float(r[c]) * ep.alpha;
+                if (add_bias && col0 + c < p.N) v[j] += __bfloat162float(ep.bias[col0 + c]);
+              }
+              stage_row_chunk16(st, lane, q, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
+                                                        __float_as_uint(v[2]), __float_as_uint(v[3])));
+            }
+          }
+          fence_proxy_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            if (p.c_slab)
+              tma_store_3d(&map_c, st, col0, row0, split);
+            else if (p.c_reduce)
+              tma_reduce_add_2d(&map_c, st, col0, row0);
+            else
+              tma_store_2d(&map_c, st, col0, row0);
+            bulk_commit();
+          }
+          stage_buf ^= 1;
+        }
+        tc_fence_before();
+        __syncwarp();
+#ifdef MACE_GEMM_TRACE
+        if (warp == 4 && lane == 0 && ti_ < 5) TRACE(8 + ti_ * 4 + 2);
+#endif
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
       const int row = m_blk * kBM + quarter * 32 + lane;
       const bool row_ok = row < p.M;
       const bool add_bias = ep.bias != nullptr && split == 0;
@@ -235,6 +388,9 @@ __global__ void __launch_bounds__(256, 1)
       }
       tc_fence_before();
       __syncwarp();
+#ifdef MACE_GEMM_TRACE
+      if (warp == 4 && lane == 0 && ti_ < 5) TRACE(8 + ti_ * 4 + 2);
+#endif
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {
         acc = 0;
@@ -242,12 +398,14 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   }
+  if (TMA_EPI && warp >= 4 && lane == 0) bulk_wait<0>();  // staged stores complete before exit
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   }
+  if (threadIdx.x == 0) TRACE(31);
 }
 
 // split-K finalize: out (op)= sum_s ws[s][M][N] in fixed split order (deterministic, no atomics).
@@ -286,10 +444,33 @@ static int make_map(MaceCtx* ctx, CUtensorMap* map, const void* ptr, uint64_t in
   return r == CUDA_SUCCESS ? 0 : -1;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+// output map of the TMA-store epilogue: {cols, rows} (or {cols, rows, splits} for split-K slabs),
+// box = {128 bytes of columns, 32 rows}, 128B swizzle (matches stage_row_chunk16)
+static int make_map_c(MaceCtx* ctx, CUtensorMap* map, const GemmEpilogue& ep, int M, int N, int splits) {
+  const bool bf16 = ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU;
+  const uint64_t es = bf16 ? 2 : 4;
+  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)splits};
+  cuuint64_t strides[2] = {(cuuint64_t)ep.ldo * es, (cuuint64_t)ep.split_stride * es};
+  cuuint32_t box[3] = {(cuuint32_t)(128 / es), 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const int rank = ep.split_stride ? 3 : 2;
+  CUresult r = ctx->encode_tiled(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank,
+                                 ep.out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -1;
+}
+
+// the TMA-store epilogue needs 16-byte aligned output rows (and slabs)
+static bool tma_epi_ok(const GemmEpilogue& ep) {
+  const size_t es = (ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU) ? 2 : 4;
+  return ((uintptr_t)ep.out & 15) == 0 && ((size_t)ep.ldo * es) % 16 == 0 && (ep.split_stride * es) % 16 == 0;
+}
+
+template <int BN, bool A_MN, bool B_MN, bool TMA_EPI>
 static int launch_gemm(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStream_t stream, const GemmEpilogue& ep) {
   using Cfg = GemmCfg<BN>;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   // A logical [M,K]; K-major storage [M, lda>=K], MN-major storage [K, lda>=M]
   int rc = A_MN ? make_map(ctx, &ma, g->a, g->M, g->K, g->lda, 64, kBK) : make_map(ctx, &ma, g->a, g->K, g->M, g->lda, kBK, kBM);
   if (rc) return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm: tensor map A encode failed");
@@ -305,7 +486,20 @@ static int launch_gemm(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStre
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
   p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
   p.ep = ep;
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+  p.c_slab = ep.split_stride != 0;
+  p.c_reduce = ep.mode == EPI_F32_ADD || ep.mode == EPI_F32_ATOMIC;
+#ifdef MACE_GEMM_TRACE
+  p.dbg = g_gemm_dbg_host;
+#else
+  p.dbg = 0;
+#endif
+  if (TMA_EPI) {
+    if (make_map_c(ctx, &mc, ep, g->M, g->N, p.c_slab ? p.splits : 1))
+      return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm: tensor map C encode failed");
+  } else {
+    mc = ma;  // unused
+  }
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, TMA_EPI>;
   static bool attr_set = false;  // per-instantiation; attribute is process-wide and idempotent
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -313,22 +507,36 @@ static int launch_gemm(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStre
   }
   const int tiles = p.num_m * p.num_n * p.splits;
   const int grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
-  launch_k(kern, grid, 256, Cfg::kSmemBytes, stream, ma, mb, p);
+  launch_k(kern, grid, 256, Cfg::kSmemBytes, stream, ma, mb, mc, p);
   ctx->launches++;
   return 0;
 }
 
+template <int BN, bool T>
+static int dispatch_major_t(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStream_t s, const GemmEpilogue& ep) {
+  if (!g->a_mn_major && !g->b_mn_major) return launch_gemm<BN, false, false, T>(ctx, g, splits, s, ep);
+  if (!g->a_mn_major && g->b_mn_major) return launch_gemm<BN, false, true, T>(ctx, g, splits, s, ep);
+  if (g->a_mn_major && !g->b_mn_major) return launch_gemm<BN, true, false, T>(ctx, g, splits, s, ep);
+  return launch_gemm<BN, true, true, T>(ctx, g, splits, s, ep);
+}
+
 template <int BN>
 static int dispatch_major(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStream_t s, const GemmEpilogue& ep) {
-  if (!g->a_mn_major && !g->b_mn_major) return launch_gemm<BN, false, false>(ctx, g, splits, s, ep);
-  if (!g->a_mn_major && g->b_mn_major) return launch_gemm<BN, false, true>(ctx, g, splits, s, ep);
-  if (g->a_mn_major && !g->b_mn_major) return launch_gemm<BN, true, false>(ctx, g, splits, s, ep);
-  return launch_gemm<BN, true, true>(ctx, g, splits, s, ep);
+  static const bool no_tma_epi = getenv("MACE_GEMM_NO_TMA_EPI") != nullptr;  // A/B comparisons only
+  if (tma_epi_ok(ep) && !no_tma_epi) return dispatch_major_t<BN, true>(ctx, g, splits, s, ep);
+  return dispatch_major_t<BN, false>(ctx, g, splits, s, ep);
 }
 
 }  // namespace mace
 
 using namespace mace;
+
+#ifdef MACE_GEMM_TRACE
+extern "C" int mace_debug_gemm_trace(void* buf, int dbg) {
+  g_gemm_dbg_host = dbg;
+  return cudaMemcpyToSymbol(g_gemm_trace, &buf, sizeof(buf)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* stream_) {
   MaceCtx* ctx = ctx_;
@@ -352,6 +560,14 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     int max_split = kb_total / 4;  // keep >= 4 k-blocks per split
     if (splits > max_split) splits = max_split;
     if (splits < 1) splits = 1;
+  }
+  // tuning override (tools/gemm_bench.py sweeps): MACE_GEMM_FORCE="<bn>,<splits>"
+  if (const char* f = getenv("MACE_GEMM_FORCE")) {
+    int fb = 0, fs = 0;
+    if (sscanf(f, "%d,%d", &fb, &fs) == 2) {
+      if (fb == 64 || fb == 128 || fb == 256) bn = fb;
+      if (fs >= 1) splits = fs;
+    }
   }
   GemmEpilogue ep;
   ep.out = g->out;

@@ -374,7 +374,7 @@ class GpuEngine(Engine):
             rec = dict(tick=self.tick_index - 1, batch=batch,
                        kept_post={self.slot_of[r.id]: list(self.state[r.id].kept) for r in live_dec if self.pruning},
                        dec_tokens=None if out.dec_tokens is None else out.dec_tokens.cpu().numpy().copy(),
-                       dec_logits=None if out.dec_tokens is None else m.dec_logits[: batch.n_dec].cpu().clone())
+                       dec_logits=None if out.dec_tokens is None else m.dec_logits[: batch.n_dec, : self.mcfg.vocab].cpu().clone())
             if fts:
                 rec.update(ft_loss=out.ft_loss.cpu().numpy().copy(), ft_margin=out.ft_margin.cpu().numpy().copy(),
                            ft_lp=out.ft_lp.cpu().numpy().copy(), ref_lp=out.ref_lp.cpu().numpy().copy(),

@@ -20,8 +20,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import ops
-from ._lib import Ctx, MaceKvLayout
+from ._lib import (Ctx, MaceKvLayout, MaceLayerGrads, MaceLayerWeights, MaceModelDesc, MaceSavedActs,
+                   MaceTickBuffers, MaceTickDesc)
 from .batch import PAGE, TickBatch
 from .config import ModelConfig, TrainConfig, selected_param_names
 
@@ -121,15 +121,80 @@ class HybridModel:
         self._ft_cap = 0
         self._R_cap = 0
         self._ndec_cap = 0
+        self._P_cap = 0
+        # padded vocab row stride (16-byte aligned fp32/bf16 rows: TMA operand / TMA-store epilogue)
+        self.vpad = (cfg.vocab + 7) // 8 * 8
         self.ws = torch.empty(16 << 20, dtype=torch.float32, device=self.dev)  # 64 MB split-K / reduction scratch
         self.tape: list | None = None   # when a list: every device-side call is appended (bench replay)
         self.instrument: list | None = None  # when a list: (ev0, ev1, bytes) per decode-attention launch
         self._attn_bytes = 0
         self.idx = torch.empty(1 << 16, dtype=torch.int32, device=self.dev)
+        self._bufs = MaceTickBuffers()
+        self.mh = self._create_native()
+
+    def _create_native(self):
+        """mace_model_create: weight / gradient / KV pointers of the native tick executor (csrc/tick.cu)."""
+        c = self.cfg
+        w = self.w
+        fields = [f for f, _ in MaceLayerWeights._fields_]
+
+        def lw(get, l, cls):
+            return cls(**{f: get(f"layers.{l}.{f[:-2]}.{f[-1]}") for f in fields})
+
+        def wptr(n):
+            t = w.get(n)
+            return None if t is None else t.data_ptr()
+
+        def refptr(n):
+            t = self.ref_w.get(n, w.get(n))
+            return None if t is None else t.data_ptr()
+
+        def gptr(n):
+            t = self.gview.get(n)
+            return None if t is None else t.data_ptr()
+
+        L = c.n_layers
+        self._layers_arr = (MaceLayerWeights * L)(*[lw(wptr, l, MaceLayerWeights) for l in range(L)])
+        nsel = len(self.sel_layers)
+        self._sel_arr = (C.c_int * max(nsel, 1))(*self.sel_layers)
+        self._ref_arr = (MaceLayerWeights * max(nsel, 1))(*[lw(refptr, l, MaceLayerWeights) for l in self.sel_layers])
+        self._grad_arr = (MaceLayerGrads * max(nsel, 1))(*[lw(gptr, l, MaceLayerGrads) for l in self.sel_layers])
+        desc = MaceModelDesc(
+            family=int(c.family == "gpt2"), n_layers=L, d_model=c.d_model, n_heads=c.n_heads,
+            n_kv_heads=c.n_kv_heads, head_dim=c.head_dim, ffn=c.ffn, up_dim=c.up_dim, vocab=c.vocab,
+            norm_eps=c.norm_eps, dpo_beta=self.tcfg.dpo_beta,
+            embed=wptr("embed"), pos_embed=wptr("pos_embed"), final_norm_w=wptr("final_norm.w"),
+            final_norm_b=wptr("final_norm.b"), layers=self._layers_arr, n_sel=nsel, sel_layers=self._sel_arr,
+            ref_layers=self._ref_arr, ref_final_norm_w=refptr("final_norm.w"), ref_final_norm_b=refptr("final_norm.b"),
+            grads=self._grad_arr, grad_final_norm_w=gptr("final_norm.w"), grad_final_norm_b=gptr("final_norm.b"),
+            grad_flat=self.grad.data_ptr(), n_grad=self.n_sel, cos_t=self.cos_t.data_ptr(),
+            sin_t=self.sin_t.data_ptr(), kv=self.kv, k_pool=self.k_pool.data_ptr(), v_pool=self.v_pool.data_ptr(),
+            pages_per_layer=self.pages_per_layer, last_token=self.last_token.data_ptr(),
+            dec_counters=self.dec_counters.data_ptr(), dec_work=self.dec_work.data_ptr(),
+            decode_impl=int(self.decode_impl),
+        )
+        h = C.c_void_p()
+        self.ctx.check(self.ctx.L.mace_model_create(self.ctx.h, C.byref(desc), C.byref(h)), "mace_model_create")
+        return h
+
+    def set_decode_impl(self, impl: int) -> None:
+        """0 auto, 1 CUDA-core streaming decode attention, 2 tcgen05 swap-AB (re-creates the executor)."""
+        self.decode_impl = impl
+        self.ctx.L.mace_model_destroy(self.mh)
+        self.mh = self._create_native()
+
+    def __del__(self):
+        try:
+            if getattr(self, "mh", None):
+                self.ctx.L.mace_model_destroy(self.mh)
+                self.mh = None
+        except Exception:
+            pass
 
     # ------------------------------------------------------------------ buffers
-    def _ensure(self, T: int, n_ft: int, R: int, n_dec: int) -> None:
+    def _ensure(self, T: int, n_ft: int, R: int, n_dec: int, P: int = 1) -> None:
         c, dev = self.cfg, self.dev
+        grew = False
         bf, f32 = dict(dtype=torch.bfloat16, device=dev), dict(dtype=torch.float32, device=dev)
         if T > self._cap:
             cap = max(T, int(self._cap * 1.5), 256)
@@ -142,6 +207,7 @@ class HybridModel:
             self.u = torch.empty(cap, c.up_dim, **bf)
             self.a = torch.empty(cap, c.ffn, **bf)
             self._cap = cap
+            grew = True
         if n_ft > self._ft_cap:
             cap = max(n_ft, int(self._ft_cap * 1.5), 128)
             self.sav = {}
@@ -173,23 +239,64 @@ class HybridModel:
             self.dqkv16 = torch.empty(cap, c.qkv_dim, **bf)
             self.Dbuf = torch.empty(cap, c.n_heads, **f32)
             self._ft_cap = cap
+            grew = True
         if R > self._R_cap:
             cap = max(R, int(self._R_cap * 1.5), 64)
             self.ft_h = torch.empty(cap, c.d_model, **bf)
-            self.ft_logits = torch.empty(cap, c.vocab, **f32)
-            self.vpad = (c.vocab + 7) // 8 * 8  # 16-byte aligned rows for the TMA operand of dX = dlogits . E
+            self.ft_logits = torch.empty(cap, self.vpad, **f32)
             self.dlogits = torch.empty(cap, self.vpad, **bf)
             self.dh = torch.empty(cap, c.d_model, **f32)
             self.row_lse = torch.empty(cap, **f32)
             self.row_lp = torch.empty(cap, **f32)
             self._R_cap = cap
+            grew = True
         if n_dec > self._ndec_cap:
             cap = max(n_dec, int(self._ndec_cap * 1.5), 64)
             self.dec_h = torch.empty(cap, c.d_model, **bf)
-            self.dec_logits = torch.empty(cap, c.vocab, **f32)
+            self.dec_logits = torch.empty(cap, self.vpad, **f32)
             self.dec_tok = torch.empty(cap, dtype=torch.int32, device=dev)
             self.dec_ws = torch.empty(cap * c.n_kv_heads * 4 * (2 * c.group + c.group * c.head_dim), **f32)
             self._ndec_cap = cap
+            grew = True
+        if P > self._P_cap:
+            cap = max(P, 2 * self._P_cap, 16)
+            self.dpo_lp = torch.empty(cap, 2, **f32)
+            self.dpo_ref_lp = torch.empty(cap, 2, **f32)
+            self.dpo_loss = torch.empty(cap, **f32)
+            self.dpo_margin = torch.empty(cap, **f32)
+            self.dpo_coef = torch.empty(cap, 2, **f32)
+            self._P_cap = cap
+            grew = True
+        if grew:
+            self._fill_bufs()
+
+    def _fill_bufs(self) -> None:
+        """(Re)point the native executor's MaceTickBuffers at the current scratch tensors."""
+        b = MaceTickBuffers()
+        for n in ("x", "h", "qkv", "o", "lse", "hn", "u", "a"):
+            setattr(b, n, getattr(self, n).data_ptr())
+        if self._ft_cap:
+            sav = [MaceSavedActs(**{k: t.data_ptr() for k, t in self.sav[l].items()}) for l in self.sel_layers]
+            self._sav_arr = (MaceSavedActs * max(len(sav), 1))(*sav)
+            b.sav = self._sav_arr
+            for n in ("rx", "rx2", "x_lmin", "rlse", "rh", "rqkv", "ro", "ru", "ra", "dx", "dy16", "df", "da16",
+                      "du16", "do16", "dqkv", "dqkv16", "Dbuf"):
+                setattr(b, n, getattr(self, n).data_ptr())
+            b.ld_df = self.df.shape[1]
+        if self._R_cap:
+            for n in ("ft_h", "ft_logits", "dlogits", "dh", "row_lse", "row_lp"):
+                setattr(b, n, getattr(self, n).data_ptr())
+            b.ld_vocab = self.vpad
+        b.ld_vocab = self.vpad
+        if self._ndec_cap:
+            for n in ("dec_h", "dec_logits", "dec_tok", "dec_ws"):
+                setattr(b, n, getattr(self, n).data_ptr())
+            b.dec_ws_bytes = self.dec_ws.numel() * 4
+        if self._P_cap:
+            b.lp, b.ref_lp, b.loss = self.dpo_lp.data_ptr(), self.dpo_ref_lp.data_ptr(), self.dpo_loss.data_ptr()
+            b.margin, b.coef = self.dpo_margin.data_ptr(), self.dpo_coef.data_ptr()
+        b.ws, b.ws_bytes = self.ws.data_ptr(), self.ws.numel() * 4
+        self._bufs = b
 
     def replay(self, tape) -> None:
         """Re-issue a recorded sequence of device calls (bench: device-only throughput)."""
@@ -219,159 +326,71 @@ class HybridModel:
             views[name] = self.idx[off: off + cnt].view(*shape) if cnt else None
         return views
 
-    # ------------------------------------------------------------------ primitive wrappers
-    def _chk(self, rc, what):
-        self.ctx.check(rc, what)
-
-    @property
-    def _s(self) -> int:
-        return torch.cuda.current_stream(self.dev).cuda_stream
-
-    def _norm(self, x, ldx, rows, n, wname, W, out, ldo):
-        c = self.cfg
-        ln = c.family == "gpt2"
-        b = W.get(wname[:-2] + ".b") if ln else None
-        self._chk(self.ctx.L.mace_norm(self.ctx.h, x.data_ptr(), ldx, _p(rows), n, c.d_model, W[wname].data_ptr(),
-                                       _p(b), int(ln), c.norm_eps, out.data_ptr(), ldo, None, self._s), "norm")
-
-    def _gemm(self, a, b, out, mode, bias=None, a_mn=False, b_mn=False):
-        ops.gemm(self.ctx, a, b, out, mode=mode, bias=bias, a_mn=a_mn, b_mn=b_mn, workspace=self.ws)
-
-    # ------------------------------------------------------------------ one decoder layer (forward)
-    def _layer(self, l, W, T, x, h, qkv, o, u, a, seqs, tc_items, dec_items, row_seq, row_pos, row_kvi,
-               paged: bool, lse=None, hn=None, save=None, ft0=0):
-        c = self.cfg
-        p = f"layers.{l}."
-        bias = (lambda n: W[p + n + ".b"]) if c.has_bias else (lambda n: None)
-        if save is not None:
-            save["x_in"][: T - ft0].copy_(x[ft0:T])
-        self._norm(x, c.d_model, None, T, p + "attn_norm.w", W, h, c.d_model)
-        self._gemm(h[:T], W[p + "qkv.w"], qkv[:T], "bf16", bias("qkv"))
-        lay = self.kv
-        kp = self.k_pool[l] if paged else None
-        vp = self.v_pool[l] if paged else None
-        self._chk(self.ctx.L.mace_rope_kv(self.ctx.h, qkv.data_ptr(), T, c.n_heads, c.n_kv_heads, c.head_dim,
-                                          row_pos.data_ptr(), row_seq.data_ptr(), _p(row_kvi), seqs.data_ptr(),
-                                          self.cos_t.data_ptr(), self.sin_t.data_ptr(), int(c.family == "llama"),
-                                          C.byref(lay), _p(kp), _p(vp), self._s), "rope_kv")
-        if self.instrument is not None and dec_items is not None:
-            if tc_items is not None:
-                ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, tc_items, None, lay,
-                             kp, vp, o[:T], lse=lse, head_norm=hn)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, None, dec_items, lay,
-                         kp, vp, o[:T], lse=lse, head_norm=hn, dec_workspace=self.dec_ws,
-                         dec_counters=self.dec_counters, dec_work=self.dec_work,
-                         decode_impl=self.decode_impl)
-            e1.record()
-            self.instrument.append((e0, e1, self._attn_bytes))
-        else:
-            ops.attn_fwd(self.ctx, qkv[:T], c.n_heads, c.n_kv_heads, c.head_dim, seqs, tc_items, dec_items, lay,
-                         kp, vp, o[:T], lse=lse, head_norm=hn, dec_workspace=self.dec_ws,
-                         dec_counters=self.dec_counters, dec_work=self.dec_work,
-                         decode_impl=self.decode_impl)
-        if save is not None:
-            n = T - ft0
-            save["h1"][:n].copy_(h[ft0:T])
-            save["qkv"][:n].copy_(qkv[ft0:T])
-            save["o"][:n].copy_(o[ft0:T])
-            save["lse"][:n].copy_(lse[ft0:T])
-        self._gemm(o[:T], W[p + "o.w"], x[:T], "f32_add", bias("o"))
-        if save is not None:
-            save["x_mid"][: T - ft0].copy_(x[ft0:T])
-        self._norm(x, c.d_model, None, T, p + "mlp_norm.w", W, h, c.d_model)
-        if c.family == "gpt2" and save is None:
-            # GELU fused into the up-projection epilogue (no pre-activation needed without a backward)
-            self._gemm(h[:T], W[p + "up.w"], a[:T], "bf16_gelu", bias("up"))
-        else:
-            self._gemm(h[:T], W[p + "up.w"], u[:T], "bf16", bias("up"))
-            self._chk(self.ctx.L.mace_act(self.ctx.h, u.data_ptr(), T, c.ffn, int(c.family == "llama"),
-                                          a.data_ptr(), self._s), "act")
-        if save is not None:
-            n = T - ft0
-            save["h2"][:n].copy_(h[ft0:T])
-            save["u"][:n].copy_(u[ft0:T])
-            save["a"][:n].copy_(a[ft0:T])
-        self._gemm(a[:T], W[p + "down.w"], x[:T], "f32_add", bias("down"))
-
     # ------------------------------------------------------------------ tick
     @torch.no_grad()
     def step(self, batch: TickBatch, trim: tuple[np.ndarray, np.ndarray] | None = None,
              ft_global: bool | None = None) -> StepOutputs:
         """Run one hybrid tick on the device (asynchronous; outputs are device tensors).
 
+        Every launch of the tick is issued by ONE native call (mace_tick_run, csrc/tick.cu); this
+        method only sizes the buffers, uploads the packed row tables and fills the descriptor.
         ``ft_global``: whether ANY replica has fine-tune rows this tick (lockstep multi-GPU); defaults to
         this replica's own rows."""
         if self.tape is not None:
             self.tape.append(("step", batch, ft_global))
-        c = self.cfg
         T, ft0 = batch.T, batch.ft0
         n_ft = T - ft0
         R = int(batch.ft_logit_rows.shape[0])
         n_dec = batch.n_dec
-        self._ensure(max(T, 1), max(n_ft, 1), max(R, 1), max(n_dec, 1))
+        P = len(batch.ft_pairs)
+        self._ensure(max(T, 1), max(n_ft, 1), max(R, 1), max(n_dec, 1), max(P, 1))
         v = self._upload(batch)
-        L = self.ctx.L
-        s = self._s
-        # ---- page-table maintenance (host page manager decisions -> device)
-        if v["ptab_slots"] is not None:
-            self._chk(L.mace_kv_set_prompt_tables(self.ctx.h, C.byref(self.kv), v["ptab_slots"].data_ptr(),
-                                                  v["ptab_rows"].data_ptr(), batch.ptab_slots.shape[0],
-                                                  batch.ptab_rows.shape[1], s), "set_tables")
-        if v["page_copies"] is not None:
-            self._chk(L.mace_kv_page_copy(self.ctx.h, v["page_copies"].data_ptr(), batch.page_copies.shape[0],
-                                          c.n_kv_heads, c.head_dim, self.pages_per_layer, c.n_layers,
-                                          self.k_pool.data_ptr(), self.v_pool.data_ptr(), s), "page_copy")
-        if n_dec:
-            self._chk(L.mace_kv_decode_alloc(self.ctx.h, C.byref(self.kv), v["dec_slots"].data_ptr(), n_dec, s),
-                      "decode_alloc")
+        has_ft = n_ft > 0 and P > 0
         if self.instrument is not None and n_dec:
             self._attn_bytes = self.decode_attn_bytes(batch)
+        d = MaceTickDesc(T=T, ft0=ft0, n_dec=n_dec, R=R, n_pairs=P,
+                         need_ref=int(any(p.ref_lp is None for p in batch.ft_pairs)))
+        for name in ("tokens", "pos", "row_seq", "row_kvi", "seqs", "dec_slots", "dec_rows", "ptab_slots",
+                     "ptab_rows", "page_copies", "ft_local_rows", "ft_targets", "pair_rows", "row_ps", "ref_cached",
+                     "ft_seqs", "ft_row_seq"):
+            setattr(d, name, _p(v[name]))
+        d.tc_items, d.n_tc = _p(v["tc_items"]), batch.tc_items.shape[0]
+        d.n_tc_inference = int(batch.meta.get("n_tc_inference", d.n_tc))
+        d.dec_items, d.n_dec_items = _p(v["dec_items"]), batch.dec_items.shape[0]
+        d.n_ptab, d.ptab_cols = batch.ptab_slots.shape[0], batch.ptab_rows.shape[1] if batch.ptab_rows.ndim == 2 else 0
+        d.n_copies = batch.page_copies.shape[0]
+        d.ft_tc_items, d.n_ft_tc = _p(v["ft_tc_items"]), batch.ft_tc_items.shape[0]
+        d.bwd_items, d.n_bwd = _p(v["bwd_items"]), batch.bwd_items.shape[0]
+        events = None
+        if self.instrument is not None and n_dec and T:
+            events = [torch.cuda.Event(enable_timing=True) for _ in range(2 * self.cfg.n_layers)]
+            for e in events:
+                e.record()  # materialise the cudaEvent_t handles
+            arr = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
+            d.attn_events = C.cast(arr, C.c_void_p)
+            self._ev_keep = arr
+        self.ctx.check(self.ctx.L.mace_tick_run(self.mh, C.byref(self._bufs), C.byref(d), self._s), "mace_tick_run")
+        if events is not None:
+            for l in range(self.cfg.n_layers):
+                self.instrument.append((events[2 * l], events[2 * l + 1], self._attn_bytes))
         out = StepOutputs(None, None, None, None, None, None)
-        if T == 0:
-            if ft_global:
-                self.apply_update(False)
-            return out
-        # ---- forward through all layers (one ragged batch)
-        self._chk(L.mace_embed(self.ctx.h, v["tokens"].data_ptr(), v["pos"].data_ptr(), self.last_token.data_ptr(),
-                               self.w["embed"].data_ptr(), _p(self.w.get("pos_embed")), T, c.d_model,
-                               self.x.data_ptr(), s), "embed")
-        has_ft = n_ft > 0 and len(batch.ft_pairs) > 0
-        n_tc_all = 0 if v["tc_items"] is None else v["tc_items"].shape[0]
-        n_tc_inf = int(batch.meta.get("n_tc_inference", n_tc_all))
-        for l in range(c.n_layers):
-            # FT rows ride in the shared ragged batch below the lowest selected layer; from there on they
-            # run as their own sub-batch (policy with saved activations + the pi_ref pass) so the two
-            # log-prob paths are kernel-for-kernel identical (margin exactly 0 while pi_theta = pi_ref)
-            top = has_ft and l >= self.l_min
-            T_l = ft0 if top else T
-            if has_ft and l == self.l_min:
-                self.x_lmin[:n_ft].copy_(self.x[ft0:T])
-            if T_l == 0:
-                continue
-            tci = v["tc_items"][:n_tc_inf] if top else v["tc_items"]
-            if tci is not None and tci.shape[0] == 0:
-                tci = None
-            hn = self.hn if l == c.n_layers - 1 else None
-            self._layer(l, self.w, T_l, self.x, self.h, self.qkv, self.o, self.u, self.a, v["seqs"], tci,
-                        v["dec_items"], v["row_seq"], v["pos"], v["row_kvi"], paged=True, hn=hn)
-        # ---- decode rows: final norm on gathered rows -> lm_head -> greedy token
-        if n_dec:
-            self._norm(self.x, c.d_model, v["dec_rows"], n_dec, "final_norm.w", self.w, self.dec_h, c.d_model)
-            self._gemm(self.dec_h[:n_dec], self.w["embed"], self.dec_logits[:n_dec], "f32")
-            self._chk(L.mace_argmax(self.ctx.h, self.dec_logits.data_ptr(), n_dec, c.vocab, c.vocab,
-                                    self.dec_tok.data_ptr(), s), "argmax")
-            self._chk(L.mace_scatter_tokens(self.ctx.h, self.dec_tok.data_ptr(), v["dec_slots"].data_ptr(), n_dec,
-                                            self.last_token.data_ptr(), s), "scatter_tokens")
+        if n_dec and T:
             out.dec_tokens = self.dec_tok[:n_dec]
         if trim is not None and trim[0].size:
             self.apply_trim(*trim)
         if has_ft:
-            self._ft_step(batch, v, out)
+            out.ft_loss, out.ft_margin = self.dpo_loss[:P], self.dpo_margin[:P]
+            out.ft_lp, out.ref_lp = self.dpo_lp[:P], self.dpo_ref_lp[:P]
         if has_ft or ft_global:
             self.apply_update(has_ft)
         return out
+
+    @property
+    def _s(self) -> int:
+        return torch.cuda.current_stream(self.dev).cuda_stream
+
+    def _chk(self, rc, what):
+        self.ctx.check(rc, what)
 
     def decode_attn_bytes(self, batch: TickBatch) -> int:
         """Algorithmic bytes of ONE decode-attention launch (one layer) of this tick: every visible K and
@@ -407,62 +426,7 @@ class HybridModel:
         self._chk(self.ctx.L.mace_kv_release(self.ctx.h, C.byref(self.kv), t_s.data_ptr(), len(slots), self._s),
                   "kv_release")
 
-    # ------------------------------------------------------------------ fine-tune rows
-    def _lm_rows(self, x, rows, R, W, out_h, logits):
-        c = self.cfg
-        self._norm(x, c.d_model, rows, R, "final_norm.w", W, out_h, c.d_model)
-        self._gemm(out_h[:R], self.w["embed"], logits[:R], "f32")
-
-    def _ft_step(self, batch: TickBatch, v, out: StepOutputs) -> None:
-        c, L, s = self.cfg, self.ctx.L, self._s
-        T, ft0 = batch.T, batch.ft0
-        n = T - ft0
-        R = int(batch.ft_logit_rows.shape[0])
-        P = len(batch.ft_pairs)
-        f32 = dict(dtype=torch.float32, device=self.dev)
-        lp = torch.empty(P, 2, **f32)
-        ref_lp = torch.empty(P, 2, **f32)
-        loss = torch.empty(P, **f32)
-        margin = torch.empty(P, **f32)
-        coef = torch.empty(P, 2, **f32)
-        local_rows = v["ft_logit_rows"] - ft0
-        ft_pos = v["pos"][ft0:T]
-
-        def sub_pass(W, x, save: bool):
-            x[:n].copy_(self.x_lmin[:n])
-            for l in self.sel_layers:
-                self._layer(l, W, n, x, self.rh, self.rqkv, self.ro, self.ru, self.ra, v["ft_seqs"], v["ft_tc_items"],
-                            None, v["ft_row_seq"], ft_pos, None, paged=False, lse=self.rlse if save else None,
-                            save=self.sav[l] if save else None, ft0=0)
-            self._lm_rows(x, local_rows, R, W, self.ft_h, self.ft_logits)
-
-        # ---- pi_ref log-probs (once per pair): selected layers with the frozen weights from the shared input
-        if any(p.ref_lp is None for p in batch.ft_pairs):
-            Wref = dict(self.w)
-            Wref.update(self.ref_w)
-            sub_pass(Wref, self.rx2, save=False)
-            self._chk(L.mace_dpo_fused(self.ctx.h, self.ft_logits.data_ptr(), R, c.vocab, c.vocab,
-                                       v["ft_targets"].data_ptr(), v["pair_rows"].data_ptr(), P, v["row_ps"].data_ptr(),
-                                       None, 0.0, self.row_lse.data_ptr(), self.row_lp.data_ptr(), ref_lp.data_ptr(),
-                                       None, None, None, None, 0, s), "dpo_ref")
-        else:
-            ref_lp.copy_(torch.tensor([p.ref_lp for p in batch.ft_pairs], dtype=torch.float32), non_blocking=True)
-        # ---- policy log-probs (saving activations), DPO loss and dlogits
-        sub_pass(self.w, self.rx, save=True)
-        self._chk(L.mace_dpo_fused(self.ctx.h, self.ft_logits.data_ptr(), R, c.vocab, c.vocab,
-                                   v["ft_targets"].data_ptr(), v["pair_rows"].data_ptr(), P, v["row_ps"].data_ptr(),
-                                   ref_lp.data_ptr(), self.tcfg.dpo_beta, self.row_lse.data_ptr(),
-                                   self.row_lp.data_ptr(), lp.data_ptr(), loss.data_ptr(), margin.data_ptr(),
-                                   coef.data_ptr(), self.dlogits.data_ptr(), self.vpad, s), "dpo")
-        out.ft_loss, out.ft_margin, out.ft_lp, out.ref_lp = loss, margin, lp, ref_lp
-        # ---- backward: lm_head (tied, frozen) -> final norm -> selected layers top-down
-        self.grad.zero_()
-        self._gemm(self.dlogits[:R, : c.vocab], self.w["embed"], self.dh[:R], "f32", b_mn=True)
-        self.dx[:n].zero_()
-        self._norm_bwd(self.rx, local_rows, self.dh, R, "final_norm", self.dx, local_rows)
-        for l in reversed(self.sel_layers):
-            self._layer_bwd(l, n, v, ft_pos)
-
+    # ------------------------------------------------------------------ fine-tune update
     def apply_update(self, local_ft: bool) -> None:
         """Gradient exchange (NCCL all-reduce over the request-stream replicas) and the
         masked AdamW. A replica without FT rows this tick contributes zeros and applies the same
@@ -478,72 +442,3 @@ class HybridModel:
                                       self.grad.data_ptr(), self.n_sel, self.seg_offsets.data_ptr(),
                                       self.seg_ptrs.data_ptr(), len(self.sel), t.lr, t.beta1, t.beta2, t.eps,
                                       t.weight_decay, self.adam_step, s), "adamw")
-
-    def _norm_bwd(self, x, xrows, dy, n, name, dx, dxrows):
-        c = self.cfg
-        ln = c.family == "gpt2"
-        self._chk(self.ctx.L.mace_norm_bwd(self.ctx.h, x.data_ptr(), c.d_model, _p(xrows), dy.data_ptr(), c.d_model, n,
-                                           c.d_model, self.w[name + ".w"].data_ptr(), int(ln), c.norm_eps,
-                                           dx.data_ptr(), c.d_model, _p(dxrows), self.gview[name + ".w"].data_ptr(),
-                                           _p(self.gview.get(name + ".b")), self.ws.data_ptr(),
-                                           self.ws.numel() * 4, self._s), "norm_bwd")
-
-    def _colsum(self, y16, n, N, name):
-        if name not in self.gview:
-            return
-        self._chk(self.ctx.L.mace_colsum_bf16(self.ctx.h, y16.data_ptr(), n, N, N, self.gview[name].data_ptr(),
-                                              self.ws.data_ptr(), self.ws.numel() * 4, self._s), "colsum")
-
-    def _to16(self, x, n_elems, y):
-        self._chk(self.ctx.L.mace_f32_to_bf16(self.ctx.h, x.data_ptr(), n_elems, y.data_ptr(), self._s), "to_bf16")
-
-    def _layer_bwd(self, l, n, v, ft_pos):
-        """dx (grad wrt this layer's output, FT rows) -> grad wrt its input; dW of the layer's params."""
-        c, L = self.cfg, self.ctx.L
-        sv = self.sav[l]
-        p = f"layers.{l}."
-        d, F, up, W, HO = c.d_model, c.ffn, c.up_dim, c.qkv_dim, c.n_heads * c.head_dim
-        g = self.gview
-        # MLP: down
-        self._to16(self.dx, n * d, self.dy16)
-        self._gemm(self.dy16[:n], sv["a"][:n], g[p + "down.w"], "f32_add", a_mn=True, b_mn=True)
-        self._colsum(self.dy16, n, d, p + "down.b")
-        self._gemm(self.dy16[:n], self.w[p + "down.w"], self.da16[:n], "bf16", b_mn=True)
-        self._chk(L.mace_act_bwd(self.ctx.h, sv["u"].data_ptr(), self.da16.data_ptr(), n, F,
-                                 int(c.family == "llama"), self.du16.data_ptr(), self._s), "act_bwd")
-        # MLP: up
-        self._gemm(self.du16[:n], sv["h2"][:n], g[p + "up.w"], "f32_add", a_mn=True, b_mn=True)
-        self._colsum(self.du16, n, up, p + "up.b")
-        dh = self.df[:n, :d]
-        self._gemm(self.du16[:n], self.w[p + "up.w"], self.df[:n, :d], "f32", b_mn=True)
-        self._norm_bwd_local(sv["x_mid"], self.df, n, p + "mlp_norm")
-        # attention: o projection
-        self._to16(self.dx, n * d, self.dy16)
-        self._gemm(self.dy16[:n], sv["o"][:n], g[p + "o.w"], "f32_add", a_mn=True, b_mn=True)
-        self._colsum(self.dy16, n, d, p + "o.b")
-        self._gemm(self.dy16[:n], self.w[p + "o.w"], self.do16[:n], "bf16", b_mn=True)
-        # attention core
-        self.dqkv[:n].zero_()
-        self._chk(L.mace_attn_bwd(self.ctx.h, sv["qkv"].data_ptr(), sv["o"].data_ptr(), self.do16.data_ptr(),
-                                  sv["lse"].data_ptr(), n, c.n_heads, c.n_kv_heads, c.head_dim,
-                                  v["ft_seqs"].data_ptr(), v["bwd_items"].data_ptr(), v["bwd_items"].shape[0], 0,
-                                  self.Dbuf.data_ptr(), self.dqkv.data_ptr(), self._s), "attn_bwd")
-        if c.family == "llama":
-            self._chk(L.mace_rope_bwd(self.ctx.h, self.dqkv.data_ptr(), n, c.n_heads, c.n_kv_heads, c.head_dim,
-                                      ft_pos.data_ptr(), self.cos_t.data_ptr(), self.sin_t.data_ptr(), self._s),
-                      "rope_bwd")
-        self._to16(self.dqkv, n * W, self.dqkv16)
-        self._gemm(self.dqkv16[:n], sv["h1"][:n], g[p + "qkv.w"], "f32_add", a_mn=True, b_mn=True)
-        self._colsum(self.dqkv16, n, W, p + "qkv.b")
-        self._gemm(self.dqkv16[:n], self.w[p + "qkv.w"], self.df[:n, :d], "f32", b_mn=True)
-        self._norm_bwd_local(sv["x_in"], self.df, n, p + "attn_norm")
-
-    def _norm_bwd_local(self, x, dyf, n, name):
-        """dx += norm_bwd(x, dy) for FT-local rows; dy rows live in dyf[:, :d] (row stride = dyf.shape[1])."""
-        c = self.cfg
-        ln = c.family == "gpt2"
-        self._chk(self.ctx.L.mace_norm_bwd(self.ctx.h, x.data_ptr(), c.d_model, None, dyf.data_ptr(), dyf.shape[1], n,
-                                           c.d_model, self.w[name + ".w"].data_ptr(), int(ln), c.norm_eps,
-                                           self.dx.data_ptr(), c.d_model, None, self.gview[name + ".w"].data_ptr(),
-                                           _p(self.gview.get(name + ".b")), self.ws.data_ptr(),
-                                           self.ws.numel() * 4, self._s), "norm_bwd")

@@ -43,3 +43,29 @@ def test_no_gpu_means_loud_failure():
 def test_product_never_imports_oracle():
     for p in (ROOT / "paper_2510_03283_b200").glob("*.py"):
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", p.read_text(), re.M), p
+
+
+def test_ctypes_struct_layouts_match_the_header(tmp_path):
+    """Every ctypes mirror of a header struct has the C compiler's size and field offsets (gcc here)."""
+    import subprocess
+
+    from paper_2510_03283_b200 import _lib
+
+    structs = [_lib.MaceGemmArgs, _lib.MaceKvLayout, _lib.MaceAttnArgs, _lib.MaceLayerWeights, _lib.MaceLayerGrads,
+               _lib.MaceModelDesc, _lib.MaceSavedActs, _lib.MaceTickBuffers, _lib.MaceTickDesc]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "mace_b200.h"', "int main(void) {"]
+    expect = []
+    for st in structs:
+        n = st.__name__
+        lines.append(f'  printf("%zu\\n", sizeof({n}));')
+        expect.append(ctypes.sizeof(st))
+        for f, _ in st._fields_:
+            lines.append(f'  printf("%zu\\n", offsetof({n}, {f}));')
+            expect.append(getattr(st, f).offset)
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got == expect
