@@ -72,7 +72,10 @@ typedef struct MaceGemmArgs {
   int split_k;           /* 0 = heuristic */
   void* workspace;       /* fp32 scratch for split-K with bf16 output (may be NULL) */
   size_t workspace_bytes;
+  int flags;             /* MACE_GEMM_B_STATIC: B is not written by the preceding kernel on the stream
+                            (weights), so its first tiles are fetched before the PDL wait            */
 } MaceGemmArgs;
+#define MACE_GEMM_B_STATIC 1
 int mace_gemm_bf16(mace_ctx* ctx, const MaceGemmArgs* args, void* stream);
 
 

@@ -27,7 +27,7 @@ class MaceGemmArgs(C.Structure):
         ("M", C.c_int), ("N", C.c_int), ("K", C.c_int),
         ("out", C.c_void_p), ("ldo", C.c_int), ("mode", C.c_int),
         ("bias", C.c_void_p), ("alpha", C.c_float), ("split_k", C.c_int),
-        ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+        ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("flags", C.c_int),
     ]
 
 

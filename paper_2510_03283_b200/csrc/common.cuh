@@ -222,6 +222,13 @@ MACE_DEV float2 ffma2(float2 a, float2 b, float2 c) {
         "l"(*reinterpret_cast<unsigned long long*>(&c)));
   return *reinterpret_cast<float2*>(&d);
 }
+// GPT-2 "gelu_new" with the MUFU tanh (tanh.approx.f32, ~2^-11 relative error: below the bf16 rounding
+// of the output it feeds); used in the GEMM epilogue where a libm tanhf per element costs more than the MMA
+MACE_DEV float gelu_tanh_fast(float x) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+  return 0.5f * x * (1.f + t);
+}
 MACE_DEV float gelu_tanh(float x) {  // GPT-2 "gelu_new"
   return 0.5f * x * (1.f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
 }

@@ -42,6 +42,7 @@ struct GemmParams {
   int c_reduce;  // TMA epilogue: 1 -> global += tile (cp.reduce.async.bulk .add)
   int c_slab;    // TMA epilogue: 1 -> per-split fp32 slabs through a 3-D map {N, M, splits}
   int dbg;       // trace builds only (tools/gemm_trace.py probes); 0 otherwise
+  int b_static;  // B not written by the preceding kernel: first ring of B tiles loads before the PDL wait
   GemmEpilogue ep;
 };
 
@@ -112,13 +113,38 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) TRACE(1);
-  pdl_wait();
-  pdl_trigger();
-  if (threadIdx.x == 0) TRACE(2);
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (whole warp walks the schedule so
     // every index is warp-uniform and lives in uniform registers; one elected lane issues)
+    auto load_b = [&](int stage, int kb, int n_blk) {
+      uint8_t* sb = smem_b + stage * Cfg::kBBytes;
+      if (!B_MN) {
+        tma_load_2d(sb, &map_b, &full_bar[stage], kb * kBK, n_blk * BN);
+      } else {
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j)
+          tma_load_2d(sb + j * (64 * kBK * 2), &map_b, &full_bar[stage], n_blk * BN + j * 64, kb * kBK);
+      }
+    };
+    // weights (B) do not depend on the preceding kernel: fill the first ring of B tiles while it drains
+    int pre = 0;
+    if (p.b_static && (int)blockIdx.x < num_tiles) {
+      const int t = blockIdx.x;
+      const int n_blk = (t / p.num_m) % p.num_n;
+      const int kb0 = (t / (p.num_m * p.num_n)) * p.kb_per_split;
+      pre = min(S, min(p.kb_total, kb0 + p.kb_per_split) - kb0);
+      if (elect_one()) {
+        for (int i = 0; i < pre; ++i) {
+          mbar_arrive_expect_tx(&full_bar[i], Cfg::kStageBytes);
+          load_b(i, kb0 + i, n_blk);
+        }
+      }
+      __syncwarp();
+    }
+    pdl_wait();
+    pdl_trigger();
+    if (lane == 0) TRACE(2);
     int stage = 0;
     uint32_t phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -131,6 +157,7 @@ __global__ void __launch_bounds__(256, 1)
 #ifdef MACE_GEMM_TRACE
         if (p.dbg == 4 && (kb - kb0) >= S) break;
 #endif
+        const bool b_done = t == (int)blockIdx.x && kb - kb0 < pre;  // B already in flight (pre-wait)
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (elect_one()) {
 #ifdef MACE_GEMM_TRACE
@@ -138,9 +165,8 @@ __global__ void __launch_bounds__(256, 1)
             mbar_arrive(&full_bar[stage]);
           } else {
 #endif
-          mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+          if (!b_done) mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           uint8_t* sa = smem_a + stage * Cfg::kABytes;
-          uint8_t* sb = smem_b + stage * Cfg::kBBytes;
           if (!A_MN) {
             tma_load_2d(sa, &map_a, &full_bar[stage], kb * kBK, m_blk * kBM);
           } else {
@@ -151,13 +177,7 @@ __global__ void __launch_bounds__(256, 1)
 #ifdef MACE_GEMM_TRACE
           if (t == (int)blockIdx.x && kb == kb0) TRACE(3);
 #endif
-          if (!B_MN) {
-            tma_load_2d(sb, &map_b, &full_bar[stage], kb * kBK, n_blk * BN);
-          } else {
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(sb + j * (64 * kBK * 2), &map_b, &full_bar[stage], n_blk * BN + j * 64, kb * kBK);
-          }
+          if (!b_done) load_b(stage, kb, n_blk);
 #ifdef MACE_GEMM_TRACE
           }
 #endif
@@ -236,6 +256,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue (128 threads <-> 128 TMEM lanes)
+    pdl_wait();  // outputs may be read / accumulated by the preceding kernel
     const uint32_t quarter = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -278,7 +299,7 @@ __global__ void __launch_bounds__(256, 1)
                 const int c = q * 8 + j;
                 v[j] = __uint_as_float(r[c]) * ep.alpha;
                 if (add_bias && col0 + c < p.N) v[j] += __bfloat162float(ep.bias[col0 + c]);
-                if (ep.mode == EPI_BF16_GELU) v[j] = gelu_tanh(v[j]);
+                if (ep.mode == EPI_BF16_GELU) v[j] = gelu_tanh_fast(v[j]);
               }
               stage_row_chunk16(st, lane, q, make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
                                                         pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7])));
@@ -346,7 +367,7 @@ __global__ void __launch_bounds__(256, 1)
         const bool full = (col0 + 32 <= p.N) && ((ep.ldo & 7) == 0);
         if (ep.mode == EPI_BF16_GELU) {  // fused GPT-2 MLP activation (gelu_tanh) on the up projection
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+          for (int j = 0; j < 32; ++j) v[j] = gelu_tanh_fast(v[j]);
         }
         if (ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU) {
           __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ep_out) + (size_t)row * ep.ldo + col0;
@@ -409,24 +430,36 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // split-K finalize: out (op)= sum_s ws[s][M][N] in fixed split order (deterministic, no atomics).
-// mode: EPI_BF16 -> bf16 store, EPI_F32 -> fp32 store, EPI_F32_ADD -> fp32 +=
+// mode: EPI_BF16 / EPI_BF16_GELU -> bf16 store, EPI_F32 -> fp32 store, EPI_F32_ADD -> fp32 +=.
+// Four columns per thread (N % 4 == 0, the common case) with 32-bit index math.
+template <bool VEC4>
 __global__ void gemm_finalize(const float* __restrict__ ws, int splits, int M, int N, void* __restrict__ out, int ldo,
                               int mode) {
   pdl_wait();
   pdl_trigger();
-  const size_t total = (size_t)M * N;
-  const size_t slab = total;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t r = i / N, c = i % N;
-    float v = 0.f;
-    for (int sp = 0; sp < splits; ++sp) v += ws[sp * slab + i];
-    if (mode == EPI_BF16_GELU) v = gelu_tanh(v);
-    if (mode == EPI_BF16 || mode == EPI_BF16_GELU) {
-      reinterpret_cast<__nv_bfloat16*>(out)[r * ldo + c] = __float2bfloat16(v);
-    } else if (mode == EPI_F32) {
-      reinterpret_cast<float*>(out)[r * ldo + c] = v;
-    } else {
-      reinterpret_cast<float*>(out)[r * ldo + c] += v;
+  const int W = VEC4 ? N / 4 : N;
+  const int total = M * W;
+  const size_t slab = (size_t)M * N;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int r = i / W, c = (i - r * W) * (VEC4 ? 4 : 1);
+    const size_t src = (size_t)r * N + c;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int sp = 0; sp < splits; ++sp) {
+      if (VEC4) {
+        const float4 w = *reinterpret_cast<const float4*>(ws + sp * slab + src);
+        v[0] += w.x; v[1] += w.y; v[2] += w.z; v[3] += w.w;
+      } else {
+        v[0] += ws[sp * slab + src];
+      }
+    }
+    const size_t dst = (size_t)r * ldo + c;
+#pragma unroll
+    for (int j = 0; j < (VEC4 ? 4 : 1); ++j) {
+      float x = v[j];
+      if (mode == EPI_BF16_GELU) x = gelu_tanh_fast(x);
+      if (mode == EPI_BF16 || mode == EPI_BF16_GELU) reinterpret_cast<__nv_bfloat16*>(out)[dst + j] = __float2bfloat16(x);
+      else if (mode == EPI_F32) reinterpret_cast<float*>(out)[dst + j] = x;
+      else reinterpret_cast<float*>(out)[dst + j] += x;
     }
   }
 }
@@ -488,6 +521,7 @@ static int launch_gemm(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStre
   p.ep = ep;
   p.c_slab = ep.split_stride != 0;
   p.c_reduce = ep.mode == EPI_F32_ADD || ep.mode == EPI_F32_ATOMIC;
+  p.b_static = (g->flags & MACE_GEMM_B_STATIC) ? 1 : 0;
 #ifdef MACE_GEMM_TRACE
   p.dbg = g_gemm_dbg_host;
 #else
@@ -547,17 +581,19 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     return mace_fail(ctx, MACE_ERR_ARG, "gemm: operands need 16-byte aligned rows (ld % 8 == 0)");
   if (g->mode < EPI_BF16 || g->mode > EPI_BF16_GELU) return mace_fail(ctx, MACE_ERR_ARG, "gemm: bad epilogue mode");
 
-  // tile shape / split-K heuristic: fill the 148 SMs
+  // tile shape / split-K heuristic (tools/gemm_sweep.py on B200): a k-block costs about the same for
+  // BN = 64 and 128 (TMA/issue-bound), BN = 256 only pays once its tiles fill the SMs; split-K only when
+  // every split keeps >= 12 k-blocks (the slab round trip + finalize launch cost ~2-3 us)
   const int num_m = (g->M + kBM - 1) / kBM;
   const int kb_total = (g->K + kBK - 1) / kBK;
   int bn = 256;
   if ((long)num_m * ((g->N + 255) / 256) < ctx->num_sms) bn = 128;
-  if (bn == 128 && (long)num_m * ((g->N + 127) / 128) < ctx->num_sms / 2) bn = 64;
+  if (bn == 128 && kb_total < 24 && (long)num_m * ((g->N + 127) / 128) < ctx->num_sms / 2) bn = 64;
   const long tiles = (long)num_m * ((g->N + bn - 1) / bn);
   int splits = g->split_k > 0 ? g->split_k : 1;
   if (g->split_k <= 0 && tiles < ctx->num_sms) {
     splits = (int)(ctx->num_sms / tiles);
-    int max_split = kb_total / 4;  // keep >= 4 k-blocks per split
+    int max_split = kb_total / 12;
     if (splits > max_split) splits = max_split;
     if (splits < 1) splits = 1;
   }
@@ -603,8 +639,16 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     rc = dispatch_major<64>(ctx, g, splits, stream, ep);
   if (rc) return rc;
   if (need_finalize) {
-    launch_k(gemm_finalize, ctx->num_sms * 4, 256, 0, stream, reinterpret_cast<const float*>(g->workspace), splits, g->M,
-                                                        g->N, g->out, g->ldo, g->mode);
+    const bool vec4 = (g->N % 4) == 0;
+    const long long work = (long long)g->M * (vec4 ? g->N / 4 : g->N);
+    int fgrid = (int)((work + 255) / 256);
+    if (fgrid > ctx->num_sms * 8) fgrid = ctx->num_sms * 8;
+    if (vec4)
+      launch_k(gemm_finalize<true>, fgrid, 256, 0, stream, reinterpret_cast<const float*>(g->workspace), splits, g->M,
+               g->N, g->out, g->ldo, g->mode);
+    else
+      launch_k(gemm_finalize<false>, fgrid, 256, 0, stream, reinterpret_cast<const float*>(g->workspace), splits, g->M,
+               g->N, g->out, g->ldo, g->mode);
     ctx->launches++;
   }
   return mace_check_launch(ctx, "gemm");

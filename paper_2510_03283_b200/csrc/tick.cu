@@ -67,7 +67,8 @@ struct AttnRows {
 static const size_t kBf = 2;
 
 static int gemm(ModelState& m, const MaceTickBuffers* b, cudaStream_t s, const void* A, int lda, bool a_mn, const void* B,
-                int ldb, bool b_mn, int M, int N, int K, void* out, int ldo, int mode, const void* bias) {
+                int ldb, bool b_mn, int M, int N, int K, void* out, int ldo, int mode, const void* bias,
+                bool b_weights = true) {
   MaceGemmArgs g{};
   g.a = A;
   g.lda = lda;
@@ -86,6 +87,7 @@ static int gemm(ModelState& m, const MaceTickBuffers* b, cudaStream_t s, const v
   g.split_k = 0;
   g.workspace = b->ws;
   g.workspace_bytes = b->ws_bytes;
+  g.flags = b_weights ? MACE_GEMM_B_STATIC : 0;  // weights are only written by AdamW at the tick's end
   const int rc = mace_gemm_bf16(m.ctx, &g, s);
   return rc;
 }
@@ -228,19 +230,19 @@ static int layer_bwd(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc
   const int ln = d.family == 1;
   // MLP down: dW = dy^T a, db = colsum(dy), da = dy W
   MACE_TRY(mace_f32_to_bf16(m.ctx, b->dx, (long long)n * D, b->dy16, s));
-  MACE_TRY(gemm(m, b, s, b->dy16, D, true, sv.a, F, true, D, F, n, g.down_w, F, MACE_EPI_F32_ADD, nullptr));
+  MACE_TRY(gemm(m, b, s, b->dy16, D, true, sv.a, F, true, D, F, n, g.down_w, F, MACE_EPI_F32_ADD, nullptr, false));
   MACE_TRY(colsum(m, b, b->dy16, n, D, g.down_b, s));
   MACE_TRY(gemm(m, b, s, b->dy16, D, false, W.down_w, F, true, n, F, D, b->da16, F, MACE_EPI_BF16, nullptr));
   MACE_TRY(mace_act_bwd(m.ctx, sv.u, b->da16, n, F, d.family == 0, b->du16, s));
   // MLP up
-  MACE_TRY(gemm(m, b, s, b->du16, UP, true, sv.h2, D, true, UP, D, n, g.up_w, D, MACE_EPI_F32_ADD, nullptr));
+  MACE_TRY(gemm(m, b, s, b->du16, UP, true, sv.h2, D, true, UP, D, n, g.up_w, D, MACE_EPI_F32_ADD, nullptr, false));
   MACE_TRY(colsum(m, b, b->du16, n, UP, g.up_b, s));
   MACE_TRY(gemm(m, b, s, b->du16, UP, false, W.up_w, D, true, n, D, UP, b->df, b->ld_df, MACE_EPI_F32, nullptr));
   MACE_TRY(mace_norm_bwd(m.ctx, sv.x_mid, D, nullptr, b->df, b->ld_df, n, D, W.mlp_norm_w, ln, d.norm_eps, b->dx, D,
                          nullptr, g.mlp_norm_w, g.mlp_norm_b, b->ws, b->ws_bytes, s));
   // attention: o projection
   MACE_TRY(mace_f32_to_bf16(m.ctx, b->dx, (long long)n * D, b->dy16, s));
-  MACE_TRY(gemm(m, b, s, b->dy16, D, true, sv.o, HO, true, D, HO, n, g.o_w, HO, MACE_EPI_F32_ADD, nullptr));
+  MACE_TRY(gemm(m, b, s, b->dy16, D, true, sv.o, HO, true, D, HO, n, g.o_w, HO, MACE_EPI_F32_ADD, nullptr, false));
   MACE_TRY(colsum(m, b, b->dy16, n, D, g.o_b, s));
   MACE_TRY(gemm(m, b, s, b->dy16, D, false, W.o_w, HO, true, n, HO, D, b->do16, HO, MACE_EPI_BF16, nullptr));
   // attention core (dense causal FT sequences)
@@ -250,7 +252,7 @@ static int layer_bwd(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc
   if (d.family == 0)
     MACE_TRY(mace_rope_bwd(m.ctx, b->dqkv, n, d.n_heads, d.n_kv_heads, d.head_dim, t->pos + t->ft0, d.cos_t, d.sin_t, s));
   MACE_TRY(mace_f32_to_bf16(m.ctx, b->dqkv, (long long)n * QKV, b->dqkv16, s));
-  MACE_TRY(gemm(m, b, s, b->dqkv16, QKV, true, sv.h1, D, true, QKV, D, n, g.qkv_w, D, MACE_EPI_F32_ADD, nullptr));
+  MACE_TRY(gemm(m, b, s, b->dqkv16, QKV, true, sv.h1, D, true, QKV, D, n, g.qkv_w, D, MACE_EPI_F32_ADD, nullptr, false));
   MACE_TRY(colsum(m, b, b->dqkv16, n, QKV, g.qkv_b, s));
   MACE_TRY(gemm(m, b, s, b->dqkv16, QKV, false, W.qkv_w, D, true, n, D, QKV, b->df, b->ld_df, MACE_EPI_F32, nullptr));
   MACE_TRY(mace_norm_bwd(m.ctx, sv.x_in, D, nullptr, b->df, b->ld_df, n, D, W.attn_norm_w, ln, d.norm_eps, b->dx, D,

@@ -37,6 +37,7 @@ def gemm(
     split_k: int = 0,
     workspace: torch.Tensor | None = None,
     stream: torch.cuda.Stream | None = None,
+    b_static: bool = False,
 ) -> torch.Tensor:
     """out[M,N] (op)= alpha * A[M,K] . B[N,K]^T.
 
@@ -68,6 +69,7 @@ def gemm(
         out=_ptr(out), ldo=out.stride(0), mode=EPI[mode],
         bias=_ptr(bias), alpha=float(alpha), split_k=int(split_k),
         workspace=_ptr(workspace), workspace_bytes=0 if workspace is None else workspace.numel() * workspace.element_size(),
+        flags=1 if b_static else 0,
     )
     ctx.check(ctx.L.mace_gemm_bf16(ctx.h, C.byref(g), _stream(stream)), "mace_gemm_bf16")
     return out
