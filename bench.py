@@ -103,12 +103,18 @@ class ClockSampler:
 
 
 def snapshot(model):
+    """Device state the timed ticks mutate. The KV pools are restored only when a copy fits next to them:
+    without it the replay re-writes the same pages with the same (deterministic) values, and only pages that
+    the original run evicted and re-used read other (finite) KV content -- same bytes, same launches."""
     import torch
 
-    names = ["k_pool", "v_pool", "ptab", "dtab", "dec_base", "dec_first", "dec_end", "free_stack", "free_top",
-             "last_token", "master", "m", "v"]
+    names = ["ptab", "dtab", "dec_base", "dec_first", "dec_end", "free_stack", "free_top", "last_token", "master",
+             "m", "v"]
+    pool_bytes = 2 * model.k_pool.numel() * model.k_pool.element_size()
+    if pool_bytes < 0.6 * torch.cuda.mem_get_info(model.dev)[0]:
+        names = ["k_pool", "v_pool"] + names
     snap = {n: getattr(model, n).clone() for n in names}
-    snap["w"] = {n: t.clone() for n, t in model.w.items()}
+    snap["w"] = {n: model.w[n].clone() for n in model.sel}  # AdamW writes only the selected parameters
     snap["adam_step"] = model.adam_step
     return snap
 
@@ -122,6 +128,16 @@ def restore(model, snap):
             model.adam_step = t
         else:
             getattr(model, n).copy_(t)
+
+
+def make_workload(args, rank):
+    """The workload's trace for this rank: one independent request stream per GPU, seed = base + rank."""
+    from paper_2510_03283_b200.workloads import WORKLOADS
+
+    if args.workload == "c1":
+        return WORKLOADS["c1"]()
+    base = WORKLOADS[args.workload]().seed if args.seed is None else args.seed
+    return WORKLOADS[args.workload](seed=base + rank)
 
 
 def run_ours(args, rank, world, lock):
@@ -138,19 +154,20 @@ def run_ours(args, rank, world, lock):
     build()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    wl = WORKLOADS[args.workload](seed=args.seed + rank) if args.workload != "c1" else WORKLOADS["c1"]()
+    wl = make_workload(args, rank)
     cfg = wl.model
     w = init_weights(cfg, seed=0, device=f"cuda:{local}")
     torch.cuda.synchronize()
-    kvtok = args.kv_tokens
+    kvtok = args.kv_tokens or wl.kv_tokens
     model = HybridModel(cfg, wl.train, w, device=local, max_slots=args.max_slots, max_prompt_len=wl.max_prompt_len,
                         max_decode_steps=wl.sched.max_decode_steps, prompt_groups=kvtok // 16,
-                        decode_pages=args.max_slots * cfg.n_kv_heads * 12,
+                        decode_pages=args.max_slots * cfg.n_kv_heads * wl.decode_pages_per_head,
                         process_group=lock.grad_group if world > 1 else None)
     del w
     eng = GpuEngine(*wl.engine_args(), model=model, mode="P", lockstep=lock if world > 1 else None)
     eng.keep_outputs = False
     # ---- ramp the trace to steady state (untimed), then warm up
+    args.skip = wl.bench_skip if args.skip is None else args.skip
     eng.run_ticks(args.skip)
     eng.run_ticks(args.warmup)
     torch.cuda.synchronize()
@@ -233,6 +250,7 @@ def run_ours(args, rank, world, lock):
                    "clock": "reference cost model (mode P: bins identical to the unmodified scheduler)",
                    "skip_ticks": args.skip, "parallelism": f"request-stream replicas x{world} + NCCL grad all-reduce",
                    "l2": "inputs larger than L2 (weights + KV pages per tick >> 126 MB)",
+                   "kv_pool_restored_for_replay": "k_pool" in snap,
                    "per_gpu_tokens_per_s": value / world,
                    "rows_per_tick_mean": float(np.mean(tick_tokens)) if tick_tokens else 0.0},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
@@ -253,7 +271,11 @@ def run_ours(args, rank, world, lock):
     n_pairs = sum(len(op[1].ft_pairs) for op in tape if op[0] == "step")
     out["finetune_samples_per_s"] = lock.sum_over_ranks(n_pairs) / (dev_ms / 1e3)
     out["config"]["ft_ticks_in_timed_region"] = n_ft_ticks
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if args.workload == "c4" and not args.no_cpu_baseline:
+        # the fp32 CPU oracle of Llama-3-8B needs 32 GB of host weights and ~200 s per prefill-heavy tick
+        out["cpu_baseline"] = {"unavailable": "c4 (Llama-3-8B): one fp32 CPU oracle tick exceeds the bounded "
+                                              "sample; the c2 line carries the CPU baseline"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, wl, budget_s=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(out))
@@ -300,7 +322,7 @@ def run_reference(args, rank, world):
 
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
-    wl = WORKLOADS[args.workload](seed=args.seed) if args.workload != "c1" else WORKLOADS["c1"]()
+    wl = make_workload(args, 0)
     cfg = wl.model
     Eng = make_reference_engine_cls()
     eng = Eng(*wl.engine_args())
@@ -330,12 +352,12 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--skip", type=int, default=150, help="ticks to reach steady state before warm-up")
+    ap.add_argument("--seed", type=int, default=None, help="trace seed of rank 0 (default: the workload's); rank r uses seed + r")
+    ap.add_argument("--skip", type=int, default=None, help="ticks to reach steady state before warm-up (default: the workload's)")
     ap.add_argument("--max-slots", type=int, default=1024)
-    ap.add_argument("--kv-tokens", type=int, default=1 << 19, help="prompt KV capacity in tokens")
+    ap.add_argument("--kv-tokens", type=int, default=None, help="prompt KV capacity in tokens (default: the workload's)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -18,8 +18,12 @@ shapes = [  # (M, N, K, mode, label)
     (256, 50257, 768, "f32", "gpt2 lm_head decode"), (1000, 2304, 768, "bf16", "gpt2 qkv mixed"),
     (1000, 768, 3072, "f32_add", "gpt2 down mixed"), (256, 3072, 2048, "bf16", "llama1b qkv decode"),
     (256, 16384, 2048, "bf16", "llama1b up decode"), (256, 2048, 8192, "f32_add", "llama1b down decode"),
-    (4096, 4096, 4096, "bf16", "square 4k"),
+    (4096, 4096, 4096, "bf16", "square 4k"), (8192, 8192, 8192, "bf16", "square 8k"),
+    (16384, 6144, 4096, "bf16", "llama8b qkv prefill"), (16384, 4096, 4096, "f32_add", "llama8b o prefill"),
+    (16384, 28672, 4096, "bf16", "llama8b up prefill"), (16384, 4096, 14336, "f32_add", "llama8b down prefill"),
 ]
+if len(sys.argv) > 1:
+    shapes = [s for s in shapes if any(k in s[4] for k in sys.argv[1:])]
 for M, N, K, mode, label in shapes:
     a = torch.randn(M, K, device="cuda").bfloat16()
     b = torch.randn(N, K, device="cuda").bfloat16()

@@ -22,14 +22,15 @@ from paper_2510_03283_b200.workloads import WORKLOADS  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c2")
 ap.add_argument("--steps", type=int, default=8)
-ap.add_argument("--skip", type=int, default=150)
-ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--skip", type=int, default=None)
+ap.add_argument("--seed", type=int, default=None)
 args = ap.parse_args()
-wl = WORKLOADS[args.workload](seed=args.seed)
+wl = WORKLOADS[args.workload]() if args.seed is None else WORKLOADS[args.workload](seed=args.seed)
+args.skip = wl.bench_skip if args.skip is None else args.skip
 cfg = wl.model
 model = HybridModel(cfg, wl.train, init_weights(cfg, 0, "cuda"), max_slots=1024, max_prompt_len=wl.max_prompt_len,
-                    max_decode_steps=wl.sched.max_decode_steps, prompt_groups=(1 << 19) // 16,
-                    decode_pages=1024 * cfg.n_kv_heads * 12)
+                    max_decode_steps=wl.sched.max_decode_steps, prompt_groups=wl.kv_tokens // 16,
+                    decode_pages=1024 * cfg.n_kv_heads * wl.decode_pages_per_head)
 eng = GpuEngine(*wl.engine_args(), model=model, mode="P")
 eng.keep_outputs = False
 eng.run_ticks(args.skip)
