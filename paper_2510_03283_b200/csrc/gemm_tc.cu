@@ -429,6 +429,252 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) TRACE(31);
 }
 
+// ====================================================================================================
+// CTA-pair GEMM (cta_group::2) for the large prefill / fine-tune projections.
+//
+// A single-CTA 128 x 256 tile is shared-memory-bound on B200: per K=16 step the MMA reads 12 KB of operands
+// from smem while TMA writes the next 12 KB, ~192 B/clk against ~128 B/clk of smem bandwidth, which caps it
+// near 65% of the tensor peak. A CTA pair (two SMs of one TPC, cluster of 2) computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 issued by the leader: each CTA stages only its 128 rows of A and its BN/2 rows of
+// B, so per-SM operand traffic halves at the same MMA rate. Roles (256 threads per CTA):
+//   warp 0 (both CTAs): TMA producer; both CTAs' loads complete on the LEADER's full barrier
+//   warp 1 (leader):    single-thread MMA issue; commits multicast to both CTAs' empty / tmem-full barriers
+//   warp 2 (both):      TMEM allocation (cta_group::2: one warp of each CTA)
+//   warps 4..7 (both):  epilogue of the CTA's 128 accumulator rows (TMA-store), then a cluster-scope arrive
+//                       on the leader's tmem-empty barrier (8 arrivals = 4 warps x 2 CTAs)
+// Tiles are walked in groups of kGroupM m-tiles (n outer within a group) so the ~74 tiles in flight share
+// A and B panels through L2.
+// ====================================================================================================
+template <int BN>
+struct Gemm2Cfg {
+  static constexpr int kABytes = 128 * kBK * 2;           // this CTA's 128 rows of A
+  static constexpr int kBBytes = (BN / 2) * kBK * 2;      // this CTA's BN/2 rows of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kCBytes = 4 * 2 * 4096;
+  static constexpr int kBudget = 227 * 1024 - kCBytes - 1024 - 256;
+  static constexpr int kStages = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kCBytes + 1024 + 256;
+};
+constexpr int kGroupM = 16;
+
+MACE_DEV void tile2_coords(int t, int num_m, int num_n, int& m_blk, int& n_blk) {
+  const int group = t / (kGroupM * num_n);
+  const int first_m = group * kGroupM;
+  const int gm = min(kGroupM, num_m - first_m);
+  const int r = t - group * kGroupM * num_n;
+  m_blk = first_m + r % gm;
+  n_blk = r / gm;
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ CUtensorMap map_c, const GemmParams p) {
+  using Cfg = Gemm2Cfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + S * Cfg::kABytes;
+  uint8_t* smem_c = smem + S * Cfg::kStageBytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_c + Cfg::kCBytes);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int num_tiles = p.num_m * p.num_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    tma_prefetch_desc(&map_c);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised before any cross-CTA arrive / complete_tx
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (both CTAs)
+    auto load_b = [&](int stage, int kb, int n_blk, uint32_t bar) {
+      tma_load_2d_pair(smem_b + stage * Cfg::kBBytes, &map_b, bar, kb * kBK, n_blk * BN + rank * (BN / 2));
+    };
+    const uint32_t full0 = mapa_shared(smem_u32(&full_bar[0]), 0);  // leader's full barriers
+    int pre = 0;
+    if (p.b_static && cid < num_tiles) {
+      int m_blk, n_blk;
+      tile2_coords(cid, p.num_m, p.num_n, m_blk, n_blk);
+      pre = min(S, p.kb_total);
+      if (elect_one()) {
+        for (int i = 0; i < pre; ++i) {
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[i], 2 * Cfg::kStageBytes);
+          load_b(i, i, n_blk, full0 + i * 8);
+        }
+      }
+      __syncwarp();
+    }
+    pdl_wait();
+    pdl_trigger();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = cid; t < num_tiles; t += ncl) {
+      int m_blk, n_blk;
+      tile2_coords(t, p.num_m, p.num_n, m_blk, n_blk);
+      for (int kb = 0; kb < p.kb_total; ++kb) {
+        const bool b_done = t == cid && kb < pre;
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (elect_one()) {
+          const uint32_t bar = full0 + stage * 8;
+          if (rank == 0 && !b_done) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+          tma_load_2d_pair(smem_a + stage * Cfg::kABytes, &map_a, bar, kb * kBK, m_blk * 256 + rank * 128);
+          if (!b_done) load_b(stage, kb, n_blk, bar);
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && rank == 0) {
+    // ------------------------------------------------ MMA issuer (leader only)
+    constexpr uint32_t idesc = idesc_bf16_f32(256, BN, false, false);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const uint32_t a_base = smem_u32(smem_a), b_base = smem_u32(smem_b);
+    for (int t = cid; t < num_tiles; t += ncl) {
+      mbar_wait_cluster(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < p.kb_total; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        const uint32_t a_addr = a_base + stage * Cfg::kABytes;
+        const uint32_t b_addr = b_base + stage * Cfg::kBBytes;
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_bf16_pair(d_tmem, smem_desc_sw128(a_addr + k * 32, 16, 1024),
+                           smem_desc_sw128(b_addr + k * 32, 16, 1024), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          umma_commit_pair(&empty_bar[stage], 0x3);
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (elect_one()) umma_commit_pair(&tfull_bar[acc], 0x3);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue (both CTAs: this CTA's 128 rows)
+    pdl_wait();
+    const uint32_t quarter = warp & 3;
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int stage_buf = 0;
+    const GemmEpilogue& ep = p.ep;
+    const bool bf16_out = ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU;
+    const int cw = bf16_out ? 64 : 32;
+    for (int t = cid; t < num_tiles; t += ncl) {
+      int m_blk, n_blk;
+      tile2_coords(t, p.num_m, p.num_n, m_blk, n_blk);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row0 = m_blk * 256 + rank * 128 + quarter * 32;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += cw) {
+        const int col0 = n_blk * BN + c0;
+        if (col0 >= p.N) break;
+        uint32_t r[64];
+        const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN + c0;
+        tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+        if (bf16_out) tmem_ld_32x32b_x32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        tmem_ld_wait();
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* st = smem_c + (quarter * 2 + stage_buf) * 4096;
+        if (bf16_out) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int c = q * 8 + j;
+              v[j] = __uint_as_float(r[c]) * ep.alpha;
+              if (ep.bias != nullptr && col0 + c < p.N) v[j] += __bfloat162float(ep.bias[col0 + c]);
+              if (ep.mode == EPI_BF16_GELU) v[j] = gelu_tanh_fast(v[j]);
+            }
+            stage_row_chunk16(st, lane, q, make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                                                      pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7])));
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int c = q * 4 + j;
+              v[j] = __uint_as_float(r[c]) * ep.alpha;
+              if (ep.bias != nullptr && col0 + c < p.N) v[j] += __bfloat162float(ep.bias[col0 + c]);
+            }
+            stage_row_chunk16(st, lane, q, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
+                                                      __float_as_uint(v[2]), __float_as_uint(v[3])));
+          }
+        }
+        fence_proxy_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+          if (p.c_reduce)
+            tma_reduce_add_2d(&map_c, st, col0, row0);
+          else
+            tma_store_2d(&map_c, st, col0, row0);
+          bulk_commit();
+        }
+        stage_buf ^= 1;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  cluster_sync();  // the peer's epilogue arrivals and the leader's MMAs are done before TMEM is released
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
 // split-K finalize: out (op)= sum_s ws[s][M][N] in fixed split order (deterministic, no atomics).
 // mode: EPI_BF16 / EPI_BF16_GELU -> bf16 store, EPI_F32 -> fp32 store, EPI_F32_ADD -> fp32 +=.
 // Four columns per thread (N % 4 == 0, the common case) with 32-bit index math.
@@ -546,6 +792,43 @@ static int launch_gemm(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStre
   return 0;
 }
 
+template <int BN>
+static int launch_gemm2(MaceCtx* ctx, const MaceGemmArgs* g, cudaStream_t stream, const GemmEpilogue& ep) {
+  using Cfg = Gemm2Cfg<BN>;
+  CUtensorMap ma, mb, mc;
+  if (make_map(ctx, &ma, g->a, g->K, g->M, g->lda, kBK, 128))
+    return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm2: tensor map A encode failed");
+  if (make_map(ctx, &mb, g->b, g->K, g->N, g->ldb, kBK, BN / 2))
+    return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm2: tensor map B encode failed");
+  GemmParams p{};
+  p.M = g->M;
+  p.N = g->N;
+  p.K = g->K;
+  p.num_m = (g->M + 255) / 256;
+  p.num_n = (g->N + BN - 1) / BN;
+  p.kb_total = (g->K + kBK - 1) / kBK;
+  p.kb_per_split = p.kb_total;
+  p.splits = 1;
+  p.ep = ep;
+  p.c_slab = 0;
+  p.c_reduce = ep.mode == EPI_F32_ADD || ep.mode == EPI_F32_ATOMIC;
+  p.b_static = (g->flags & MACE_GEMM_B_STATIC) ? 1 : 0;
+  p.dbg = 0;
+  if (make_map_c(ctx, &mc, ep, g->M, g->N, 1)) return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm2: tensor map C encode failed");
+  auto kern = gemm_tc2_kernel<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    attr_set = true;
+  }
+  const int tiles = p.num_m * p.num_n;
+  const int pairs = ctx->num_sms / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  launch_k(kern, grid, 256, Cfg::kSmemBytes, stream, ma, mb, mc, p);
+  ctx->launches++;
+  return 0;
+}
+
 template <int BN, bool T>
 static int dispatch_major_t(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStream_t s, const GemmEpilogue& ep) {
   if (!g->a_mn_major && !g->b_mn_major) return launch_gemm<BN, false, false, T>(ctx, g, splits, s, ep);
@@ -612,6 +895,26 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   ep.alpha = g->alpha == 0.f ? 1.f : g->alpha;
   ep.mode = g->mode;
   ep.split_stride = 0;
+  // CTA-pair kernel: K-major operands, no split-K, TMA-store epilogue, and enough 256-row tiles to fill
+  // the 74 pairs (tools/gemm_sweep.py); MACE_GEMM_FORCE="pair,<bn>" / "single" override for sweeps
+  {
+    int pair_bn = 0;
+    const int num_m2 = (g->M + 255) / 256;
+    if (!g->a_mn_major && !g->b_mn_major && g->split_k <= 0 && g->mode != EPI_F32_ATOMIC && tma_epi_ok(ep)) {
+      if ((long)num_m2 * ((g->N + 255) / 256) >= ctx->num_sms) pair_bn = 256;
+      else if ((long)num_m2 * ((g->N + 127) / 128) >= ctx->num_sms) pair_bn = 128;
+      if (const char* f = getenv("MACE_GEMM_FORCE")) {
+        int fb = 0;
+        if (sscanf(f, "pair,%d", &fb) == 1 && (fb == 128 || fb == 256)) pair_bn = fb;
+        else pair_bn = 0;
+      }
+    }
+    if (pair_bn) {
+      const int rc2 = pair_bn == 256 ? launch_gemm2<256>(ctx, g, stream, ep) : launch_gemm2<128>(ctx, g, stream, ep);
+      if (rc2) return rc2;
+      return mace_check_launch(ctx, "gemm2");
+    }
+  }
   bool need_finalize = false;
   if (splits > 1 && g->mode != EPI_F32_ATOMIC) {
     // keep the per-split slabs inside the caller's workspace

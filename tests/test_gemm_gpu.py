@@ -75,3 +75,36 @@ def test_gemm_splitk_bf16_workspace(ctx):
     y = ops.gemm(ctx, a, b, mode="bf16", split_k=8, workspace=ws)
     ref = a.float() @ b.float().t()
     assert torch.allclose(y.float(), ref, atol=0.5, rtol=1e-2)
+
+
+@pytest.mark.parametrize("M,N,K,force", [
+    (2048, 6144, 1024, None),        # auto -> CTA-pair, BN 256 (8 x 24 pair tiles)
+    (1100, 8200, 512, None),         # ragged M (last pair tile straddles M) and N
+    (777, 2056, 640, "pair,128"),    # pair BN 128, ragged everywhere, K % 64 != 0
+    (4096, 1024, 4160, "pair,256"),  # long K
+])
+def test_gemm_cta_pair(ctx, M, N, K, force, monkeypatch):
+    """cta_group::2 GEMM (256-row pair tiles, leader-issued MMA) against the fp32 reference, every epilogue."""
+    if force:
+        monkeypatch.setenv("MACE_GEMM_FORCE", force)
+    torch.manual_seed(M + N + K)
+    a = torch.randn(M, K, device="cuda").bfloat16()
+    b = torch.randn(N, K, device="cuda").bfloat16()
+    bias = torch.randn(N, device="cuda").bfloat16()
+    ref = a.float() @ b.float().t()
+    tol = 1e-3 * K ** 0.5 + 1e-2
+    out = ops.gemm(ctx, a, b, mode="f32")
+    assert (out - ref).abs().max().item() <= tol
+    y = ops.gemm(ctx, a, b, mode="bf16", bias=bias)
+    assert torch.allclose(y.float(), ref + bias.float(), atol=0.1, rtol=1e-2)
+    g = ops.gemm(ctx, a, b, mode="bf16_gelu", bias=bias)
+    assert torch.allclose(g.float(), torch.nn.functional.gelu(ref + bias.float(), approximate="tanh"), atol=0.1,
+                          rtol=1e-2)
+    acc0 = torch.randn(M, N, device="cuda")
+    acc = acc0.clone()
+    ops.gemm(ctx, a, b, acc, mode="f32_add", alpha=0.5)
+    assert torch.allclose(acc, acc0 + 0.5 * ref, atol=2e-2, rtol=1e-3)
+    # same numbers as the single-CTA kernel (both accumulate K in the same 16-wide MMA order in fp32)
+    monkeypatch.setenv("MACE_GEMM_FORCE", "single")
+    out1 = ops.gemm(ctx, a, b, mode="f32")
+    assert torch.equal(out, out1)
