@@ -162,14 +162,20 @@ class GpuEngine(Engine):
         self._planned_shared = {}
         hq_grid = np.arange(Hq, dtype=i32)
 
-        def tc_block(si, q_len):
+        def tc_block(si, q_len, kv_len):
+            """(seq, q head, q block, KV tiles the block visits): one CTA of the tensor-core attention each."""
             nb = (q_len + 127) // 128
             g = np.empty((Hq * nb, 4), i32)
             g[:, 0] = si
             g[:, 1] = np.repeat(hq_grid, nb)
-            g[:, 2] = np.tile(np.arange(nb, dtype=i32), Hq)
-            g[:, 3] = 0
+            qb = np.tile(np.arange(nb, dtype=i32), Hq)
+            g[:, 2] = qb
+            g[:, 3] = (kv_len - q_len + np.minimum(qb * 128 + 127, q_len - 1)) // 128 + 1
             return g
+
+        def lpt(items):
+            """longest-first launch order (causal blocks differ in KV tiles): the grid tail is short blocks"""
+            return items[np.argsort(-items[:, 3], kind="stable")] if items.shape[0] > 1 else items
 
         # ---- prefill rows (trie-DFS order): uncached suffix of each prompt
         for req in prefills:
@@ -187,7 +193,7 @@ class GpuEngine(Engine):
                 continue
             si = len(seqs)
             seqs.append((KIND_PREFILL, n_rows, q, slot, P, P, -1, 0))
-            tc_seg.append(tc_block(si, q))
+            tc_seg.append(tc_block(si, q, P))
             tok_seg.append(np.asarray(req.prompt_tokens[start:], i32))
             r = np.arange(start, P, dtype=i32)
             pos_seg.append(r)
@@ -263,10 +269,10 @@ class GpuEngine(Engine):
                 si = len(seqs)
                 q0 = n_rows
                 seqs.append((KIND_FT, q0, n, -1, 0, n, -1, 0))
-                tc_seg.append(tc_block(si, n))
+                tc_seg.append(tc_block(si, n, n))
                 fs = len(ft_seqs)
                 ft_seqs.append((KIND_FT, q0 - ft0, n, -1, 0, n, -1, 0))
-                ft_tc_seg.append(tc_block(fs, n))
+                ft_tc_seg.append(tc_block(fs, n, n))
                 nkb = (n + 63) // 64
                 bw = np.zeros((Hkv * nkb, 4), i32)
                 bw[:, 0] = fs
@@ -307,13 +313,15 @@ class GpuEngine(Engine):
             if len(t) > maxpp:
                 raise RuntimeError("prompt longer than max_prompt_len")
             pt[i, : len(t)] = t
+        tc_all = cat(tc_seg, 4)
+        tc_all = np.concatenate([lpt(tc_all[:n_tc_inference]), lpt(tc_all[n_tc_inference:])])
         return TickBatch(
             tokens=tokens, pos=cat(pos_seg), row_seq=cat(seq_seg), row_kvi=cat(kvi_seg),
-            seqs=arr(seqs, 8), tc_items=cat(tc_seg, 4), dec_items=dec_items,
+            seqs=arr(seqs, 8), tc_items=tc_all, dec_items=dec_items,
             dec_slots=dec_slots.astype(i32), dec_rows=dec_rows, ptab_slots=np.asarray(ptab_slots, i32), ptab_rows=pt,
             page_copies=arr(copies, 4), ft0=ft0, ft_pairs=pairs, ft_logit_rows=cat(lr_seg),
             ft_targets=cat(tg_seg), pair_rows=arr(pair_rows, 4), row_ps=cat(ps_seg),
-            ft_seqs=arr(ft_seqs, 8), ft_tc_items=cat(ft_tc_seg, 4), ft_row_seq=cat(ft_seq_seg),
+            ft_seqs=arr(ft_seqs, 8), ft_tc_items=lpt(cat(ft_tc_seg, 4)), ft_row_seq=cat(ft_seq_seg),
             bwd_items=cat(bwd_seg, 4), n_prefill_tokens=n_pre, n_decode_tokens=n_dec, n_ft_tokens=n_ft,
             meta={"n_tc_inference": n_tc_inference},
         )
