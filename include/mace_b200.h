@@ -254,6 +254,8 @@ typedef struct MaceTickDesc {              /* device row tables of one tick (see
   const MaceSeq* ft_seqs; const int* ft_tc_items; int n_ft_tc; const int* ft_row_seq;
   const int* bwd_items; int n_bwd;
   void** attn_events;                      /* optional cudaEvent_t[2*n_layers] around decode attention */
+  void** gemm_events; int gemm_events_cap; /* optional cudaEvent_t[2*cap] around every GEMM launch     */
+  long long* gemm_flops; int* gemm_count;  /* host: 2*M*N*K per instrumented GEMM, number recorded    */
 } MaceTickDesc;
 int mace_model_create(mace_ctx* ctx, const MaceModelDesc* desc, mace_model** out);
 int mace_model_destroy(mace_model* model);

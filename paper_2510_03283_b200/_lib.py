@@ -122,6 +122,8 @@ class MaceTickDesc(C.Structure):
         ("n_ft_tc", C.c_int),
         ("ft_row_seq", C.c_void_p), ("bwd_items", C.c_void_p), ("n_bwd", C.c_int),
         ("attn_events", C.c_void_p),
+        ("gemm_events", C.c_void_p), ("gemm_events_cap", C.c_int), ("gemm_flops", C.c_void_p),
+        ("gemm_count", C.c_void_p),
     ]
 
 

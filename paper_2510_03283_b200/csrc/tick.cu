@@ -28,6 +28,7 @@ struct ModelState {
   std::vector<MaceLayerWeights> layers, ref_layers;
   std::vector<MaceLayerGrads> grads;
   std::vector<int> sel;
+  const MaceTickDesc* tick = nullptr;  // the tick being issued (optional GEMM event instrumentation)
 };
 
 // activation buffers of one forward pass through a layer (FT sub-pass with save: the saved slots)
@@ -88,7 +89,15 @@ static int gemm(ModelState& m, const MaceTickBuffers* b, cudaStream_t s, const v
   g.workspace = b->ws;
   g.workspace_bytes = b->ws_bytes;
   g.flags = b_weights ? MACE_GEMM_B_STATIC : 0;  // weights are only written by AdamW at the tick's end
+  const MaceTickDesc* t = m.tick;
+  const bool ev = t && t->gemm_events && t->gemm_count && *t->gemm_count < t->gemm_events_cap;
+  if (ev) cudaEventRecord((cudaEvent_t)t->gemm_events[2 * *t->gemm_count], s);
   const int rc = mace_gemm_bf16(m.ctx, &g, s);
+  if (ev) {
+    cudaEventRecord((cudaEvent_t)t->gemm_events[2 * *t->gemm_count + 1], s);
+    t->gemm_flops[*t->gemm_count] = 2ll * M * N * K;
+    ++*t->gemm_count;
+  }
   return rc;
 }
 
@@ -377,5 +386,8 @@ extern "C" int mace_tick_run(mace_model* model, const MaceTickBuffers* bufs, con
     return mace_fail(model->ctx, MACE_ERR_ARG, "tick: missing activation buffers");
   if (tick->T - tick->ft0 > 0 && tick->n_pairs > 0 && !bufs->sav && model->sel.size())
     return mace_fail(model->ctx, MACE_ERR_ARG, "tick: FT rows need saved-activation buffers");
-  return tick_run(*model, bufs, tick, (cudaStream_t)stream);
+  model->tick = tick;
+  const int rc = tick_run(*model, bufs, tick, (cudaStream_t)stream);
+  model->tick = nullptr;
+  return rc;
 }

@@ -28,13 +28,15 @@ import torch
 
 from .batch import KIND_DECODE, KIND_FT, KIND_PREFILL, PAGE, FtPair, TickBatch
 from .config import ModelConfig, TrainConfig
+from .hostfast import FastPriorityQueue, NormStream
 from .hoststats import BatchedHeadStats
 from .kvmanager import GpuPrefixTrie, GroupPool, plan_prefill_pages
 from .model import HybridModel
 from .refpath import ensure_macesim
 
 ensure_macesim()
-from macesim.cache import dfs_order  # noqa: E402
+import macesim.engine as _ref_engine  # noqa: E402
+from macesim.cache import dfs_order as _ref_dfs_order  # noqa: E402
 from macesim.cost_model import CostProfile  # noqa: E402
 from macesim.engine import Engine  # noqa: E402
 from macesim.workload import WorkloadType  # noqa: E402
@@ -87,7 +89,7 @@ class TickBudgetReached(Exception):
 class GpuEngine(Engine):
     def __init__(self, trace, profile, sched_cfg, priority_params, cache_cfg, env, engine_cfg, metrics_horizon=None,
                  *, model: HybridModel, mode: str = "P", seed: int | None = None, record: bool = False,
-                 lockstep=None):
+                 lockstep=None, fast_host: bool = True):
         if mode not in ("P", "M"):
             raise ValueError("mode must be 'P' (parity clock) or 'M' (measured clock)")
         if mode == "M":
@@ -96,6 +98,9 @@ class GpuEngine(Engine):
         super().__init__(trace, profile, sched_cfg, priority_params, cache_cfg, env, engine_cfg, metrics_horizon)
         if model.cfg.n_kv_heads != cache_cfg.num_heads:
             raise ValueError("CacheConfig.num_heads must equal the model's KV heads (per-head KV windows)")
+        if fast_host and self.queue is not None:  # vectorised re-keying, identical pop order (hostfast.py)
+            self.queue = FastPriorityQueue(priority_params, loss_fn=self._loss_of)
+        self.norm_stream = NormStream(self)
         self.model = model
         self.mcfg: ModelConfig = model.cfg
         self.mode = mode
@@ -122,12 +127,13 @@ class GpuEngine(Engine):
         self.keep_outputs = True
         self.time_ticks = False
         # batched bit-exact head-stats/prune bookkeeping (engine.py:482-532 restated over all rows)
-        self.fast_host = True
+        self.fast_host = fast_host
         cc = cache_cfg
         self.hstats = BatchedHeadStats(model.max_slots, cc.num_heads, cc.norm_window, cc.c_total, cc.prune_window,
                                        cc.norm_tau)
         self._dec_list: list = []
         self._dec_pending: dict | None = None
+        self._dec_est = None
 
     # ------------------------------------------------------------------ helpers
     def _slot(self, rid: int) -> int:
@@ -354,7 +360,15 @@ class GpuEngine(Engine):
             ev1.synchronize()
             self.profile._clock[0] = ev0.elapsed_time(ev1)
         # ---- the reference's own bookkeeping for this bin (timeline, metrics, KV MB, prune, ft_step)
-        super()._execute(plan)
+        # the reference orders this bin's prefills with dfs_order, a walk of the WHOLE trie (cache.py:253-273);
+        # the order is already known (path_dfs_order, equal by construction and by tests/test_host_cpu.py)
+        # (thread-safe: another engine's trie, e.g. a concurrent sweep thread, falls through to the reference)
+        _ref_engine.dfs_order = lambda trie, pending, _o=prefills, _t=self.trie: (
+            list(_o) if trie is _t else _ref_dfs_order(trie, pending))
+        try:
+            super()._execute(plan)
+        finally:
+            _ref_engine.dfs_order = _ref_dfs_order
         # ---- mirror post-tick KV decisions onto the device (retired requests were released already)
         live_dec = [r for r in decodes if r.id in self.slot_of]
         if self.pruning and live_dec:
@@ -461,7 +475,7 @@ class GpuEngine(Engine):
         if first.any():
             self.hstats.reset(slots[first])
         steps = np.fromiter((r.decode_pos + 1 for r in rows), np.int64, len(rows))
-        norms = np.array([self._synth_norms(r, self.state[r.id]) for r in rows], dtype=np.float64)
+        norms = np.stack([self.norm_stream.norms(r, self.state[r.id]) for r in rows])
         kept, released = self.hstats.step(slots, steps, norms)
         kl = kept.tolist()
         rl = released.tolist()
@@ -469,7 +483,19 @@ class GpuEngine(Engine):
             out[r.id] = (kl[i], rl[i])
         return out
 
+    def _synth_norms(self, req, rs):  # engine.py:433 — same draws, served from the per-request block stream
+        return self.norm_stream.norms(req, rs).tolist()
+
+    def _estimate(self, req):  # engine.py:262 — decode estimates are constants (cost_model.py:101-102)
+        if req.workload is WorkloadType.DECODE:
+            est = self._dec_est
+            if est is None:
+                est = self._dec_est = super()._estimate(req)
+            return est
+        return super()._estimate(req)
+
     def _retire(self, req, t_end_ms, rejected=False):  # engine.py:538
+        self.norm_stream.drop(req.id)
         super()._retire(req, t_end_ms, rejected)
         slot = self.slot_of.pop(req.id, None)
         table = self.table_of.pop(req.id, None)

@@ -1,0 +1,186 @@
+"""Vectorised host bookkeeping for the reference loop, decision-for-decision identical.
+
+The hybrid iteration's end-to-end rate is bound by the reference's per-tick Python, not by the B200: at C2
+the queue holds ~1.8k requests and every tick re-keys all of them (priority.py:121-127), and every decode
+row draws its synthetic head norms through its own numpy Generator (engine.py:433-442). Both are restated
+here without changing a single decision:
+
+* ``FastPriorityQueue`` keeps the reference's key ``(-p, arrival, id)`` per queued request (priority.py:112-116)
+  in column arrays; push keys a request with the reference's own ``_key``; ``refresh`` recomputes every p
+  with numpy in the same IEEE-754 operation order as ``dynamic_priority`` / ``ft_total_priority``
+  (priority.py:67-81: base + growth * (t - arrival), then + gamma * loss for fine-tunes) and sorts the keys
+  once. Keys are unique (they contain the request id), so the pop / peek sequence equals heappop on the
+  reference heap. ``priority_state`` (priority.py:114-115, written but never read by the reference) holds
+  the refreshed value for every popped request.
+* ``NormStream`` draws a request's head-norm jitter ``normal(1, 0.1)`` in blocks from the same Generator
+  (seed ``[seed, 211, id]``); numpy's Generator fills an array with the same sequence as repeated
+  ``size=num_heads`` calls, so the per-step values equal the reference's (checked in tests/test_host_cpu.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .refpath import ensure_macesim
+
+ensure_macesim()
+from macesim.priority import PriorityContractError, PriorityQueue  # noqa: E402
+from macesim.workload import WorkloadType  # noqa: E402
+
+_FT = WorkloadType.FINETUNE
+
+
+class FastPriorityQueue(PriorityQueue):
+    """The reference PriorityQueue's semantics on column arrays: a key (-p, arrival, id) per live entry, computed
+    by the reference's own ``_key`` at push time (priority.py:112-119) and re-computed for all entries by a
+    vectorised ``refresh``; ``pop`` / ``peek`` return the entry with the smallest key, exactly like heappop on
+    the reference heap (keys are unique: they contain the request id)."""
+
+    def __init__(self, params, loss_fn=None):
+        super().__init__(params, loss_fn)
+        cap = 1024
+        self._neg = np.empty(cap, np.float64)   # -p of the current key
+        self._arr = np.empty(cap, np.float64)   # arrival time
+        self._bg = np.empty((cap, 2), np.float64)  # base, growth of the workload type
+        self._id = np.empty(cap, np.int64)
+        self._ft = np.zeros(cap, bool)
+        self._alive = np.zeros(cap, bool)
+        self._req: list = [None] * cap
+        self._n = 0          # slots used (live + dead)
+        self._live = 0
+        self._order: list[int] | None = None  # pop order of live slots after refresh (None: stale)
+        self._cur = 0
+
+    def __len__(self) -> int:
+        return self._live
+
+    def __bool__(self) -> bool:
+        return self._live > 0
+
+    def _grow(self) -> None:
+        cap = 2 * self._neg.shape[0]
+        for name in ("_neg", "_arr", "_id", "_ft", "_alive"):
+            a = getattr(self, name)
+            b = np.zeros(cap, a.dtype)
+            b[: a.shape[0]] = a
+            setattr(self, name, b)
+        bg = np.zeros((cap, 2), np.float64)
+        bg[: self._bg.shape[0]] = self._bg
+        self._bg = bg
+        self._req += [None] * (cap - len(self._req))
+
+    def _compact(self) -> None:
+        idx = np.flatnonzero(self._alive[: self._n])
+        n = idx.shape[0]
+        for name in ("_neg", "_arr", "_id", "_ft", "_alive"):
+            a = getattr(self, name)
+            a[:n] = a[idx]
+        self._bg[:n] = self._bg[idx]
+        reqs = [self._req[i] for i in idx.tolist()]
+        self._req[:n] = reqs
+        for k in range(n, self._n):
+            self._req[k] = None
+        self._alive[n: self._n] = False
+        self._n = n
+        self._order = None
+
+    def push(self, req, t=None) -> None:  # priority.py:118-119
+        key = self._key(req, self._last_refresh if t is None else t)
+        if self._n == self._neg.shape[0]:
+            if self._live < self._n // 2:
+                self._compact()
+            else:
+                self._grow()
+        k = self._n
+        self._n += 1
+        w = req.workload
+        self._neg[k] = key[0]
+        self._arr[k] = key[1]
+        self._bg[k, 0] = self.params.base[w]
+        self._bg[k, 1] = self.params.growth[w]
+        self._id[k] = req.id
+        self._ft[k] = w is _FT
+        self._alive[k] = True
+        self._req[k] = req
+        self._live += 1
+        self._order = None
+
+    def refresh(self, t: float) -> None:  # priority.py:121-127
+        self._last_refresh = t
+        if self._live == 0:
+            return
+        if self._live < self._n // 2:
+            self._compact()
+        n = self._n
+        alive = self._alive[:n]
+        arr = self._arr[:n]
+        if ((t < arr) & alive).any():
+            bad = self._req[int(np.argmax((t < arr) & alive))]
+            raise PriorityContractError(
+                f"priority query at t={t} before arrival of request {bad.id} at {bad.arrival_time}")
+        p = self._bg[:n, 0] + self._bg[:n, 1] * (t - arr)  # dynamic_priority (priority.py:73), no FMA
+        if self.loss_fn is not None:
+            gamma = self.params.gamma
+            for k in np.flatnonzero(self._ft[:n] & alive).tolist():  # ft_total_priority (priority.py:76-81)
+                loss = self.loss_fn(self._req[k])
+                if loss < 0:
+                    raise PriorityContractError("loss must be >= 0 under the positive-loss convention")
+                p[k] = p[k] + gamma * loss
+        self._neg[:n] = -p
+        self._sort()
+
+    def _sort(self) -> None:
+        n = self._n
+        live = np.flatnonzero(self._alive[:n])
+        o = np.lexsort((self._id[live], self._arr[live], self._neg[live]))  # heappop order of (-p, arrival, id)
+        self._order = live[o].tolist()
+        self._cur = 0
+
+    def _front(self) -> int:
+        if self._live == 0:
+            raise IndexError("pop from empty priority queue")
+        if self._order is None:
+            self._sort()
+        while not self._alive[self._order[self._cur]]:
+            self._cur += 1
+        return self._order[self._cur]
+
+    def pop(self):
+        k = self._front()
+        self._alive[k] = False
+        self._live -= 1
+        self._cur += 1
+        req = self._req[k]
+        self._req[k] = None
+        req.priority_state.value = -float(self._neg[k])
+        req.priority_state.refreshed_at = self._last_refresh
+        return req
+
+    def peek(self):
+        return self._req[self._front()]
+
+
+class NormStream:
+    """Per-request synthetic head-norm jitter in blocks (engine.py:433-442)."""
+
+    BLOCK = 64  # steps per draw
+
+    def __init__(self, engine):
+        self.eng = engine
+        self.buf: dict[int, tuple[np.ndarray, int]] = {}
+
+    def norms(self, req, rs) -> np.ndarray:
+        eng = self.eng
+        H = eng.cache_cfg.num_heads
+        if rs.head_rng is None:
+            rs.head_rng = np.random.default_rng([eng.ecfg.seed, 211, req.id])
+            rs.head_scales = [eng.cache_cfg.weak_scale if h in eng.weak_heads else 1.0 for h in range(H)]
+        ent = self.buf.get(req.id)
+        if ent is None or ent[1] >= ent[0].shape[0]:
+            block = rs.head_rng.normal(1.0, 0.1, size=H * self.BLOCK).reshape(self.BLOCK, H)
+            ent = (np.maximum(0.0, np.asarray(rs.head_scales, np.float64) * block), 0)
+        row = ent[0][ent[1]]
+        self.buf[req.id] = (ent[0], ent[1] + 1)
+        return row
+
+    def drop(self, rid: int) -> None:
+        self.buf.pop(rid, None)

@@ -72,6 +72,23 @@ def page_range(a: int, b: int) -> range:
     return range(a // PAGE, (b - 1) // PAGE + 1) if b > a else range(0)
 
 
+def _common_prefix(label: list[int], toks: list[int], idx: int, limit: int) -> int:
+    """Length of the common prefix of label[:limit] and toks[idx:idx+limit] (the reference's element loop,
+    cache.py:176-178, as C-speed slice comparisons plus a bisection to the first mismatch)."""
+    if label[:limit] == toks[idx: idx + limit]:
+        return limit
+    lo, hi = 0, limit  # the first mismatch lies in [lo, hi)
+    while hi - lo > 8:
+        mid = (lo + hi) // 2
+        if label[lo:mid] == toks[idx + lo: idx + mid]:
+            lo = mid
+        else:
+            hi = mid
+    while lo < hi and label[lo] == toks[idx + lo]:
+        lo += 1
+    return lo
+
+
 class GpuPrefixTrie(PrefixTrie):
     """Reference trie + page-group ownership mirror (decisions unchanged)."""
 
@@ -80,6 +97,25 @@ class GpuPrefixTrie(PrefixTrie):
         self.pool = pool
         self.node_pages: dict[int, dict[int, int]] = {}
         self.pending: dict[int, dict[int, int]] = {}   # pages a tick's prefill will hand to newly cached nodes
+
+    def cached_prefix_len(self, prompt_tokens):  # cache.py:164-184, same walk; label matches compared by slices
+        node = self.root
+        idx = 0
+        shared = 0
+        n = len(prompt_tokens)
+        while idx < n:
+            child = node.children.get(prompt_tokens[idx])
+            if child is None or not child.cached:
+                break
+            label = child.label
+            limit = min(len(label), n - idx)
+            match = _common_prefix(label, prompt_tokens, idx, limit)
+            shared += match
+            idx += match
+            if match < len(label):
+                break
+            node = child
+        return shared
 
     # -- decisions stay the reference's; ownership follows
     def _split(self, node, at):

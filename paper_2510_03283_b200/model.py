@@ -127,6 +127,7 @@ class HybridModel:
         self.ws = torch.empty(16 << 20, dtype=torch.float32, device=self.dev)  # 64 MB split-K / reduction scratch
         self.tape: list | None = None   # when a list: every device-side call is appended (bench replay)
         self.instrument: list | None = None  # when a list: (ev0, ev1, bytes) per decode-attention launch
+        self.gemm_instrument: list | None = None  # when a list: (ms, flops, launches) of the GEMMs of each tick
         self._attn_bytes = 0
         self.idx = torch.empty(1 << 16, dtype=torch.int32, device=self.dev)
         self._bufs = MaceTickBuffers()
@@ -369,7 +370,24 @@ class HybridModel:
             arr = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
             d.attn_events = C.cast(arr, C.c_void_p)
             self._ev_keep = arr
+        gcount = None
+        if self.gemm_instrument is not None:  # CUDA events around every GEMM of the tick (bench roofline pass)
+            cap = 4096
+            if getattr(self, "_gev", None) is None:
+                self._gev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * cap)]
+                for e in self._gev:
+                    e.record()
+                self._gev_arr = (C.c_void_p * (2 * cap))(*[e.cuda_event for e in self._gev])
+                self._gflops = np.zeros(cap, np.int64)
+            gcount = np.zeros(1, np.int32)
+            d.gemm_events, d.gemm_events_cap = C.cast(self._gev_arr, C.c_void_p), cap
+            d.gemm_flops, d.gemm_count = self._gflops.ctypes.data, gcount.ctypes.data
         self.ctx.check(self.ctx.L.mace_tick_run(self.mh, C.byref(self._bufs), C.byref(d), self._s), "mace_tick_run")
+        if gcount is not None:
+            torch.cuda.synchronize(self.dev)
+            n = int(gcount[0])
+            ms = sum(self._gev[2 * i].elapsed_time(self._gev[2 * i + 1]) for i in range(n))
+            self.gemm_instrument.append((ms, int(self._gflops[:n].sum()), n))
         if events is not None:
             for l in range(self.cfg.n_layers):
                 self.instrument.append((events[2 * l], events[2 * l + 1], self._attn_bytes))

@@ -11,11 +11,11 @@ from fakes import FakeModel
 GOLD = Path(__file__).parent / "golden" / "c1_reference.json"
 
 
-def _engine(wl, **kw):
+def _engine(wl, fast_host=True, **kw):
     from paper_2510_03283_b200.engine import GpuEngine
 
     fm = FakeModel(wl.model, wl.train, max_prompt_len=wl.max_prompt_len, **kw)
-    eng = GpuEngine(*wl.engine_args(), model=fm, mode="P")
+    eng = GpuEngine(*wl.engine_args(), model=fm, mode="P", fast_host=fast_host)
     eng.keep_outputs = False
     return eng, fm
 
@@ -142,14 +142,14 @@ def test_path_dfs_order_matches_reference():
 
 @pytest.mark.parametrize("wl_name,ticks", [("c1", None), ("c2", 260)])
 def test_batched_head_stats_bit_identical(wl_name, ticks):
-    """The batched head-stats/prune bookkeeping (hoststats.py) reproduces the reference's per-row
-    _exec_decode exactly: same timeline (prune events carry MB deltas), kept[] and metrics."""
+    """The host fast paths (hoststats.py batched head-stats/prune, hostfast.py column priority queue and
+    block-drawn head norms) reproduce the reference's per-row _exec_decode and PriorityQueue exactly: same
+    timeline (decisions, prune events with MB deltas), kept[] and metrics."""
     from paper_2510_03283_b200.workloads import WORKLOADS
 
     def run(fast):
         wl = WORKLOADS[wl_name]()
-        eng, fm = _engine(wl, prompt_groups=1 << 15, max_slots=1024)
-        eng.fast_host = fast
+        eng, fm = _engine(wl, fast_host=fast, prompt_groups=1 << 15, max_slots=1024)
         if ticks is None:
             res = eng.run()
             return res.timeline, res.metrics.tbt_ms, {k: list(v.kept) for k, v in eng.state.items()}
@@ -178,3 +178,82 @@ def test_batched_allocate_matches_reference_fuzz():
         got = hs._allocate(means)
         want = np.array([allocate_capacity(m.tolist(), C) for m in means])
         assert (got == want).all()
+
+
+def test_fast_priority_queue_matches_reference_heap():
+    """FastPriorityQueue pops in exactly the reference heap's order under interleaved push / refresh / pop /
+    peek, including fine-tune keys with a loss term and equal priorities (arrival / id tie-breaks)."""
+    import numpy as np
+
+    from macesim.priority import PriorityParams, PriorityQueue
+    from macesim.workload import PreferencePair, Request, WorkloadType
+    from paper_2510_03283_b200.hostfast import FastPriorityQueue
+
+    rng = np.random.default_rng(3)
+    kinds = [WorkloadType.PREFILL, WorkloadType.DECODE, WorkloadType.FINETUNE]
+    losses = {}
+
+    def loss_fn(r):
+        return losses[r.id]
+
+    ref, fast = PriorityQueue(PriorityParams(), loss_fn), FastPriorityQueue(PriorityParams(), loss_fn)
+    t, rid = 0.0, 0
+    for step in range(300):
+        for _ in range(int(rng.integers(0, 12))):
+            w = kinds[int(rng.integers(0, 3))]
+            arr = t if rng.random() < 0.3 else min(t, round(t - rng.random(), 1))  # ties on arrival time
+            pair = PreferencePair(0.5, 4, 4) if w is WorkloadType.FINETUNE else None
+            mk = lambda: Request(id=rid, tenant=0, workload=w, arrival_time=max(0.0, arr), prompt_tokens=[1, 2],
+                                 target_output_len=4, pair=pair)
+            losses[rid] = float(rng.choice([0.0, 0.3, rng.random()]))
+            ref.push(mk(), t)
+            fast.push(mk(), t)
+            rid += 1
+        if rng.random() < 0.5:
+            t += float(rng.choice([0.0, 0.05, rng.random()]))
+            for k in list(losses):
+                losses[k] = float(rng.random())
+            ref.refresh(t)
+            fast.refresh(t)
+        assert len(ref) == len(fast)
+        if ref:
+            assert ref.peek().id == fast.peek().id
+        for _ in range(int(rng.integers(0, 10))):
+            if not ref:
+                break
+            assert ref.pop().id == fast.pop().id
+
+
+def test_cached_prefix_len_matches_reference():
+    """GpuPrefixTrie.cached_prefix_len (slice compare + bisection) equals the reference's element loop on
+    random tries with shared prefixes, partial label matches and uncached nodes."""
+    import numpy as np
+
+    from macesim.cache import PrefixTrie
+    from paper_2510_03283_b200.kvmanager import GpuPrefixTrie, GroupPool, _common_prefix
+
+    rng = np.random.default_rng(7)
+    for _ in range(2000):
+        a = rng.integers(0, 5, int(rng.integers(1, 80))).tolist()
+        b = a[: int(rng.integers(0, len(a) + 1))] + rng.integers(0, 5, int(rng.integers(0, 40))).tolist()
+        i = int(rng.integers(0, len(b) + 1))
+        lim = min(len(a), len(b) - i)
+        ref = 0
+        while ref < lim and a[ref] == b[i + ref]:
+            ref += 1
+        assert _common_prefix(a, b, i, lim) == ref
+    ref_t, gpu_t = PrefixTrie(0.1), GpuPrefixTrie(0.1, GroupPool(1))
+    prompts = []
+    for k in range(300):
+        base = prompts[int(rng.integers(0, len(prompts)))] if prompts and rng.random() < 0.7 else []
+        p = base[: int(rng.integers(0, len(base) + 1))] + rng.integers(0, 6, int(rng.integers(1, 60))).tolist()
+        prompts.append(p)
+        r1, r2 = ref_t.insert(p, float(k)), gpu_t.insert(p, float(k))
+        if rng.random() < 0.6:  # cache the path (no pages needed for the query)
+            for n in r1.leaf.path_nodes():
+                n.cached = True
+            for n in r2.leaf.path_nodes():
+                n.cached = True
+        q = prompts[int(rng.integers(0, len(prompts)))]
+        q = q[: int(rng.integers(1, len(q) + 1))] + rng.integers(0, 6, int(rng.integers(0, 5))).tolist()
+        assert gpu_t.cached_prefix_len(q) == ref_t.cached_prefix_len(q)

@@ -11,11 +11,11 @@ import torch  # noqa: E402
 from paper_2510_03283_b200 import ops  # noqa: E402
 from paper_2510_03283_b200._lib import Ctx  # noqa: E402
 
-SHAPES = [(1200, 2304, 768, "bf16"), (1200, 768, 768, "f32_add"), (1200, 3072, 768, "bf16_gelu"),
-          (1200, 768, 3072, "f32_add"), (256, 50264, 768, "f32"), (260, 2304, 768, "bf16"), (260, 768, 768, "f32_add"),
-          (260, 3072, 768, "bf16_gelu"), (260, 768, 3072, "f32_add"), (256, 3072, 2048, "bf16"),
-          (256, 2048, 2048, "f32_add"), (256, 16384, 2048, "bf16"), (256, 2048, 8192, "f32_add"),
-          (2000, 3072, 2048, "bf16"), (2000, 2048, 8192, "f32_add")]
+SHAPES = [(1215, 2304, 768, "bf16"), (1215, 768, 768, "f32_add"), (1215, 3072, 768, "bf16_gelu"),
+          (1215, 768, 3072, "f32_add"), (256, 50264, 768, "f32"), (600, 2304, 768, "bf16"), (600, 768, 3072, "f32_add"),
+          (256, 3072, 2048, "bf16"), (256, 2048, 2048, "f32_add"), (256, 16384, 2048, "bf16"),
+          (256, 2048, 8192, "f32_add"), (256, 128256, 2048, "f32"), (2000, 3072, 2048, "bf16"),
+          (2000, 2048, 8192, "f32_add")]
 if len(sys.argv) > 2 and sys.argv[1] == "--shapes":
     SHAPES = [(int(a), int(b), int(c), d) for a, b, c, d in (x.split(",") for x in sys.argv[2:])]
 ctx = Ctx(0)
@@ -52,8 +52,8 @@ def timed(M, N, K, mode, cfg, n=30):
 
 
 for M, N, K, mode in SHAPES:
-    row = [(c, timed(M, N, K, mode, c)) for c in ["auto"] + [f"{bn},{sp}" for bn in (64, 128, 256)
-                                                             for sp in (1, 2, 3, 4, 6)]]
+    row = [(c, timed(M, N, K, mode, c)) for c in ["auto", "pair,128", "pair,256"] +
+           [f"{bn},{sp}" for bn in (64, 128, 256) for sp in (1, 2, 3, 4)]]
     best = min((t, c) for c, t in row)
     print(f"M={M} N={N} K={K} {mode}: auto {row[0][1]:.2f} | best {best[1]} {best[0]:.2f} | "
           + " ".join(f"{c}:{t:.1f}" for c, t in row[1:]), flush=True)
