@@ -192,6 +192,19 @@ class HybridModel:
         except Exception:
             pass
 
+    def ft_bytes_per_token(self) -> int:
+        """Device bytes one fine-tune token occupies (the per-row buffers _ensure sizes for FT rows: saved
+        activations of every selected layer + the pi_ref / backward scratch). This is what the reference's
+        ft_mem_per_token (cost_model.py:40-41) stands for on a B200 (C5 sizes the cost model with it)."""
+        c = self.cfg
+        qo = c.n_heads * c.head_dim
+        sav = 4 * c.d_model + 2 * c.d_model + 2 * c.qkv_dim + 2 * qo + 4 * c.n_heads + 4 * c.d_model + 2 * c.d_model \
+            + 2 * c.up_dim + 2 * c.ffn
+        scratch = (3 * 4 * c.d_model + 4 * c.n_heads + 2 * c.d_model + 2 * c.qkv_dim + 2 * qo + 2 * c.up_dim + 2 * c.ffn
+                   + 4 * c.d_model + 2 * c.d_model + 4 * max(c.ffn, c.up_dim, c.qkv_dim, qo) + 2 * c.ffn + 2 * c.up_dim
+                   + 2 * qo + 4 * c.qkv_dim + 2 * c.qkv_dim)
+        return len(self.sel_layers) * sav + scratch
+
     # ------------------------------------------------------------------ buffers
     def _ensure(self, T: int, n_ft: int, R: int, n_dec: int, P: int = 1) -> None:
         c, dev = self.cfg, self.dev

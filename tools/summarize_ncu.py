@@ -7,6 +7,7 @@ import sys
 from pathlib import Path
 
 OUT = Path(sys.argv[1] if len(sys.argv) > 1 else "profiles")
+TAG = sys.argv[2] if len(sys.argv) > 2 else "r1"
 SRC = Path("gpurun_out")
 M = {
     "gpu__time_duration.sum": "duration_us",
@@ -44,7 +45,7 @@ def raw(rep):
                 if name in ("dram_read", "dram_write") and isinstance(v, float):
                     v = v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
                 if name == "duration_us" and isinstance(v, float):
-                    v = v * {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(u, 1)
+                    v = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3}.get(u, 1)
                 d[name] = v
         out.append(d)
     return out
@@ -53,25 +54,30 @@ def raw(rep):
 def main():
     OUT.mkdir(exist_ok=True)
     summary = {}
-    for name in ("attn_decode", "gemm", "attn_tc"):
+    for name in ("attn_decode", "gemm", "attn_fa", "attn_decode_tc", "gemm_pair", "attn_fa_c4"):
         rep = SRC / f"{name}.ncu-rep"
         if rep.exists():
             summary[name] = raw(rep)
-    algo = json.loads((SRC / "decode_attn_bytes.json").read_text()) if (SRC / "decode_attn_bytes.json").exists() else []
+    # algorithmic bytes per decode-attention launch of the C2 replay (the launch-list run: same snapshot, so its
+    # first ticks are the ones the --set full capture replays; later profile_tick runs overwrite the plain file)
+    src = SRC / "decode_attn_bytes_launchlist.json"
+    if not src.exists():
+        src = SRC / "decode_attn_bytes.json"
+    algo = json.loads(src.read_text()) if src.exists() else []
     if "attn_decode" in summary and algo:
         for j, d in enumerate(summary["attn_decode"]):
             a = algo[12 + j]  # ncu -s 12: launches 13.. of the 2-tick replay
             d["algorithmic_bytes"] = a
             d["traffic_bytes"] = d["dram_read"] + d["dram_write"]
             d["traffic_over_algorithmic"] = d["traffic_bytes"] / a
-    (OUT / "r1_ncu_full_summary.json").write_text(json.dumps(summary, indent=1))
-    lines = ["# r1 ncu --set full captures (C2 steady state, tools/ncu_capture.sh; cold-cache, serialised)", ""]
+    (OUT / f"{TAG}_ncu_full_summary.json").write_text(json.dumps(summary, indent=1))
+    lines = [f"# {TAG} ncu --set full captures (C2 / C3 / C4 steady state, tools/ncu_capture.sh; cold-cache, serialised)", ""]
     for name, rows in summary.items():
         lines.append(f"## {name}")
         for d in rows:
             lines.append("- " + ", ".join(f"{k}={v:.4g}" if isinstance(v, float) else f"{k}={v}" for k, v in d.items()))
         lines.append("")
-    (OUT / "r1_ncu_full_summary.md").write_text("\n".join(lines))
+    (OUT / f"{TAG}_ncu_full_summary.md").write_text("\n".join(lines))
     print("\n".join(lines))
 
 
