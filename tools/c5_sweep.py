@@ -9,6 +9,7 @@ evictions and prune trims), TPOT p50/p99 (reference clock), device tokens/s over
     python tools/c5_sweep.py [--ticks 48] [--caps 40960,61440,81920,122880,184320]
 """
 import argparse
+import gc
 import json
 import sys
 import time
@@ -80,6 +81,7 @@ for cap in caps:
     rows.append(row)
     print(json.dumps(row), flush=True)
     del eng, model
+    gc.collect()  # the engine holds reference cycles (norm stream, trie); free the device pools now
     torch.cuda.empty_cache()
 Path("gpurun_out").mkdir(exist_ok=True)
 Path("gpurun_out/c5_sweep.json").write_text(json.dumps(rows, indent=1))

@@ -8,6 +8,7 @@ alignment win rate / CLPD, utilisation, rejections.
     python tools/policy_compare.py [--duration 3] [--rate 100] [--policies Hybrid,Periodic,Sync]
 """
 import argparse
+import gc
 import json
 import sys
 import time
@@ -62,6 +63,7 @@ for name in args.policies.split(","):
     rows.append(row)
     print(json.dumps(row), flush=True)
     del eng, model
+    gc.collect()  # the engine holds reference cycles (norm stream, trie); free the device pools now
     torch.cuda.empty_cache()
 Path(args.out).parent.mkdir(exist_ok=True)
 Path(args.out).write_text(json.dumps(rows, indent=1))
