@@ -177,6 +177,9 @@ int mace_act_bwd(mace_ctx* ctx, const void* u, const void* da, int n, int F, int
 int mace_rope_bwd(mace_ctx* ctx, float* dqkv, int n, int Hq, int Hkv, int hd, const int* pos, const float* cos_t,
                   const float* sin_t, void* stream);
 int mace_f32_to_bf16(mace_ctx* ctx, const float* x, long long n, void* y, void* stream);
+/* attention backward of the dense causal FT sequences: items int4 [n_items] = (seq, kv_head, key_block, steps),
+ * key blocks of 128 keys for head_dim 64 / 128 (tcgen05 kernel), 64 keys for head_dim 32; dqkv fp32 [n_rows, W]
+ * zeroed by the caller (dQ accumulates across key blocks and GQA heads), dK / dV written.                     */
 int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, const void* dout, const float* lse, int n_rows, int Hq,
                   int Hkv, int hd, const MaceSeq* seqs, const int* items, int n_items, int row_offset, float* Dbuf,
                   float* dqkv, void* stream);

@@ -6,7 +6,7 @@
 //   col_reduce  deterministic column sums of per-block partials (dw, db, bias grads)
 //   act_bwd     SwiGLU / GELU(tanh)
 //   rope_bwd    inverse rotation of dq/dk
-//   attn_bwd    dense causal attention backward for FT sequences (dQ via fp32 atomics, dK/dV owned)
+//   attn_bwd    dense causal attention backward for FT sequences, head_dim 32 (head_dim 64 / 128: attention_bwd_tc.cu)
 #include "common.cuh"
 #include "mace_internal.h"
 
@@ -420,7 +420,15 @@ extern "C" int mace_f32_to_bf16(mace_ctx* ctx, const float* x, long long n, void
   return mace_check_launch(ctx, "f32_to_bf16");
 }
 
-// items int4 [n_items] = (seq, kv_head, key_block, 0); rows of qkv/dout/lse/dqkv are local to the FT
+namespace mace {
+int attn_bwd_tc(MaceCtx* ctx, const void* qkv, const void* dout, const float* lse, int n_rows, int Hq, int Hkv, int hd,
+                const MaceSeq* seqs, const int* items, int n_items, int row_offset, const float* Dbuf, float* dqkv,
+                cudaStream_t s);  // attention_bwd_tc.cu
+}  // namespace mace
+
+// items int4 [n_items] = (seq, kv_head, key_block, steps); key blocks of 128 keys (head_dim 64 / 128: the tcgen05
+// kernel of attention_bwd_tc.cu) or 64 keys (head_dim 32: the CUDA-core kernel below). Rows of qkv/dout/lse/dqkv
+// are local to the FT
 // block starting at global row `row_offset`. dqkv must be zeroed by the caller (dq accumulates).
 extern "C" int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, const void* dout, const float* lse, int n_rows,
                              int Hq, int Hkv, int hd, const MaceSeq* seqs, const int* items, int n_items, int row_offset,
@@ -429,6 +437,12 @@ extern "C" int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, cons
   cudaStream_t s = (cudaStream_t)stream;
   launch_k(attn_bwd_prep_kernel, (n_rows * Hq + 7) / 8, 256, 0, s, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, n_rows,
                                                              Hq, hd, Dbuf);
+  if (hd == 64 || hd == 128) {  // tcgen05 path (128-key blocks)
+    const int rc = attn_bwd_tc(ctx, qkv, dout, lse, n_rows, Hq, Hkv, hd, seqs, items, n_items, row_offset, Dbuf, dqkv, s);
+    if (rc) return rc;
+    ctx->launches++;  // the prep kernel
+    return mace_check_launch(ctx, "attn_bwd");
+  }
   const float scale = 1.f / sqrtf((float)hd);
   auto go = [&](auto kern, int HD) {
     const size_t sh = (4 * 64 * (HD + 1) + 2 * 64 * 65 + 128) * sizeof(float);

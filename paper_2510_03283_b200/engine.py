@@ -279,11 +279,13 @@ class GpuEngine(Engine):
                 fs = len(ft_seqs)
                 ft_seqs.append((KIND_FT, q0 - ft0, n, -1, 0, n, -1, 0))
                 ft_tc_seg.append(tc_block(fs, n, n))
-                nkb = (n + 63) // 64
+                kblk = 128 if c.head_dim >= 64 else 64  # key block of the backward kernel (csrc/backward.cu)
+                nkb = (n + kblk - 1) // kblk
                 bw = np.zeros((Hkv * nkb, 4), i32)
                 bw[:, 0] = fs
                 bw[:, 1] = np.repeat(np.arange(Hkv, dtype=i32), nkb)
                 bw[:, 2] = np.tile(np.arange(nkb, dtype=i32), Hkv)
+                bw[:, 3] = nkb - bw[:, 2]  # query blocks the key block walks (LPT key)
                 bwd_seg.append(bw)
                 tok_seg.append(np.asarray(list(req.prompt_tokens) + list(resp), i32))
                 pos_seg.append(np.arange(n, dtype=i32))
@@ -328,7 +330,7 @@ class GpuEngine(Engine):
             page_copies=arr(copies, 4), ft0=ft0, ft_pairs=pairs, ft_logit_rows=cat(lr_seg),
             ft_targets=cat(tg_seg), pair_rows=arr(pair_rows, 4), row_ps=cat(ps_seg),
             ft_seqs=arr(ft_seqs, 8), ft_tc_items=lpt(cat(ft_tc_seg, 4)), ft_row_seq=cat(ft_seq_seg),
-            bwd_items=cat(bwd_seg, 4), n_prefill_tokens=n_pre, n_decode_tokens=n_dec, n_ft_tokens=n_ft,
+            bwd_items=lpt(cat(bwd_seg, 4)), n_prefill_tokens=n_pre, n_decode_tokens=n_dec, n_ft_tokens=n_ft,
             meta={"n_tc_inference": n_tc_inference},
         )
 

@@ -115,3 +115,28 @@ def attn_fwd(
     )
     ctx.check(ctx.L.mace_attn_fwd(ctx.h, C.byref(a), _stream(stream)), "mace_attn_fwd")
     return out
+
+
+def attn_bwd(
+    ctx: Ctx,
+    qkv: torch.Tensor,
+    o: torch.Tensor,
+    dout: torch.Tensor,
+    lse: torch.Tensor,
+    Hq: int,
+    Hkv: int,
+    hd: int,
+    seqs: torch.Tensor,
+    items: torch.Tensor,
+    dqkv: torch.Tensor | None = None,
+    stream: torch.cuda.Stream | None = None,
+) -> torch.Tensor:
+    """Attention backward of dense causal sequences: dqkv fp32 [T, (Hq+2Hkv)*hd] (dQ, dK, dV in the qkv layout).
+    ``items`` int32 [n, 4] = (seq, kv_head, key_block, steps) with 128-key blocks (hd 64/128) or 64 (hd 32)."""
+    T = qkv.shape[0]
+    if dqkv is None:
+        dqkv = torch.zeros(T, qkv.shape[1], dtype=torch.float32, device=qkv.device)
+    Dbuf = torch.empty(T, Hq, dtype=torch.float32, device=qkv.device)
+    ctx.check(ctx.L.mace_attn_bwd(ctx.h, _ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), T, Hq, Hkv, hd, _ptr(seqs),
+                                  _ptr(items), items.shape[0], 0, _ptr(Dbuf), _ptr(dqkv), _stream(stream)), "attn_bwd")
+    return dqkv

@@ -20,17 +20,18 @@ model = HybridModel(cfg, wl.train, init_weights(cfg, 0, "cuda"), max_slots=1024,
                     decode_pages=1024 * cfg.n_kv_heads * 12)
 eng = GpuEngine(*wl.engine_args(), model=model, mode="P")
 eng.keep_outputs = False
-eng.run_ticks(120)
+eng.run_ticks(150)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
-eng.run_ticks(20)
+eng.run_ticks(64)
 t1 = time.perf_counter()
 torch.cuda.synchronize()
 t2 = time.perf_counter()
-print(f"host submit {1e3 * (t1 - t0) / 20:.2f} ms/tick, wall incl. drain {1e3 * (t2 - t0) / 20:.2f} ms/tick")
+print(f"host submit {1e3 * (t1 - t0) / 64:.2f} ms/tick, wall incl. drain {1e3 * (t2 - t0) / 64:.2f} ms/tick")
 pr = cProfile.Profile()
 pr.enable()
-eng.run_ticks(20)
+eng.run_ticks(64)
 torch.cuda.synchronize()
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+pstats.Stats(pr).sort_stats("tottime").print_stats(40)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(40)
