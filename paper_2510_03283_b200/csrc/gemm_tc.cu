@@ -43,6 +43,7 @@ struct GemmParams {
   int c_slab;    // TMA epilogue: 1 -> per-split fp32 slabs through a 3-D map {N, M, splits}
   int dbg;       // trace builds only (tools/gemm_trace.py probes); 0 otherwise
   int b_static;  // B not written by the preceding kernel: first ring of B tiles loads before the PDL wait
+  int stages;    // smem ring depth of the single-CTA kernel
   GemmEpilogue ep;
 };
 
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, const GemmParams p) {
   using Cfg = GemmCfg<BN>;
-  constexpr int S = Cfg::kStages;
+  const int S = p.stages;  // ring depth (<= Cfg::kStages; small-K GEMMs use fewer to leave smem for the next kernel)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -273,70 +274,87 @@ __global__ void __launch_bounds__(256, 1)
       if (warp == 4 && lane == 0 && ti_ < 5) TRACE(8 + ti_ * 4 + 1);
 #endif
       if constexpr (TMA_EPI) {
+        // per group of two staged chunks (bf16: 2 x 64 columns, fp32: 2 x 32): every TMEM load of the group is
+        // issued before one wait, the accumulator is handed back to the MMA warp as soon as the tile's last
+        // group is in registers, and one proxy fence + one commit cover both staging buffers
         const bool bf16_out = ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU;
+        const bool gelu = ep.mode == EPI_BF16_GELU;
         const int cw = bf16_out ? 64 : 32;  // columns per 128-byte staged row
         const int row0 = m_blk * kBM + quarter * 32;
         const bool add_bias = ep.bias != nullptr && split == 0;
+        const uint32_t t_row = tmem_base + ((quarter * 32u) << 16) + acc * BN;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += cw) {
-          const int col0 = n_blk * BN + c0;
-          if (col0 >= p.N) break;
-          uint32_t r[64];
-          tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + acc * BN + c0, *reinterpret_cast<uint32_t(*)[32]>(r));
-          if (bf16_out)
-            tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + acc * BN + c0 + 32,
-                               *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        for (int g0 = 0; g0 < BN; g0 += 2 * cw) {
+          uint32_t r[128];
+          tmem_ld_32x32b_x32(t_row + g0, *reinterpret_cast<uint32_t(*)[32]>(r));
+          tmem_ld_32x32b_x32(t_row + g0 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+          if (bf16_out && g0 + 64 < BN) {  // BN 64: one bf16 chunk per tile
+            tmem_ld_32x32b_x32(t_row + g0 + 64, *reinterpret_cast<uint32_t(*)[32]>(r + 64));
+            tmem_ld_32x32b_x32(t_row + g0 + 96, *reinterpret_cast<uint32_t(*)[32]>(r + 96));
+          }
           tmem_ld_wait();
-          if (lane == 0) bulk_wait_read<1>();  // staging buffer used two chunks ago has been read
+          if (g0 + 2 * cw >= BN) {  // the whole tile is in registers: release the accumulator
+            tc_fence_before();
+            __syncwarp();
+#ifdef MACE_GEMM_TRACE
+            if (warp == 4 && lane == 0 && ti_ < 5) TRACE(8 + ti_ * 4 + 2);
+#endif
+            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+          }
+          if (lane == 0) bulk_wait_read<0>();  // both staging buffers have been read by the previous group's stores
           __syncwarp();
-          uint8_t* st = smem_c + (quarter * 2 + stage_buf) * 4096;
-          if (bf16_out) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float v[8];
+          for (int b = 0; b < 2; ++b) {
+            const int col0 = n_blk * BN + g0 + b * cw;
+            if (g0 + b * cw >= BN || col0 >= p.N) break;
+            uint8_t* st = smem_c + (quarter * 2 + b) * 4096;
+            if (bf16_out) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const int c = q * 8 + j;
-                v[j] = __uint_as_float(r[c]) * ep.alpha;
-                if (add_bias && col0 + c < p.N) v[j] += __bfloat162float(ep.bias[col0 + c]);
-                if (ep.mode == EPI_BF16_GELU) v[j] = gelu_tanh_fast(v[j]);
+              for (int q = 0; q < 8; ++q) {
+                float v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const int c = q * 8 + j;
+                  v[j] = __uint_as_float(r[b * 64 + c]) * ep.alpha;
+                  if (add_bias && col0 + c < p.N) v[j] += __bfloat162float(ep.bias[col0 + c]);
+                  if (gelu) v[j] = gelu_tanh_fast(v[j]);
+                }
+                stage_row_chunk16(st, lane, q, make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                                                          pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7])));
               }
-              stage_row_chunk16(st, lane, q, make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
-                                                        pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7])));
-            }
-          } else {
+            } else {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float v[4];
+              for (int q = 0; q < 8; ++q) {
+                float v[4];
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int c = q * 4 + j;
-                v[j] = __uint_as_float(r[c]) * ep.alpha;
-                if (add_bias && col0 + c < p.N) v[j] += __bfloat162float(ep.bias[col0 + c]);
+                for (int j = 0; j < 4; ++j) {
+                  const int c = q * 4 + j;
+                  v[j] = __uint_as_float(r[b * 32 + c]) * ep.alpha;
+                  if (add_bias && col0 + c < p.N) v[j] += __bfloat162float(ep.bias[col0 + c]);
+                }
+                stage_row_chunk16(st, lane, q, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
+                                                          __float_as_uint(v[2]), __float_as_uint(v[3])));
               }
-              stage_row_chunk16(st, lane, q, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
-                                                        __float_as_uint(v[2]), __float_as_uint(v[3])));
             }
           }
           fence_proxy_async_shared();
           __syncwarp();
           if (lane == 0) {
-            if (p.c_slab)
-              tma_store_3d(&map_c, st, col0, row0, split);
-            else if (p.c_reduce)
-              tma_reduce_add_2d(&map_c, st, col0, row0);
-            else
-              tma_store_2d(&map_c, st, col0, row0);
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              const int col0 = n_blk * BN + g0 + b * cw;
+              if (g0 + b * cw >= BN || col0 >= p.N) break;
+              uint8_t* st = smem_c + (quarter * 2 + b) * 4096;
+              if (p.c_slab)
+                tma_store_3d(&map_c, st, col0, row0, split);
+              else if (p.c_reduce)
+                tma_reduce_add_2d(&map_c, st, col0, row0);
+              else
+                tma_store_2d(&map_c, st, col0, row0);
+            }
             bulk_commit();
           }
-          stage_buf ^= 1;
         }
-        tc_fence_before();
-        __syncwarp();
-#ifdef MACE_GEMM_TRACE
-        if (warp == 4 && lane == 0 && ti_ < 5) TRACE(8 + ti_ * 4 + 2);
-#endif
-        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -785,9 +803,20 @@ static int launch_gemm(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStre
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     attr_set = true;
   }
+  // ring depth: never more stages than k-blocks per split; MACE_GEMM_STAGES caps it (sweeps)
+  static const int stage_cap = [] {
+    const char* e = getenv("MACE_GEMM_STAGES");
+    return e ? atoi(e) : 0;
+  }();
+  int stages = Cfg::kStages;
+  if (stages > p.kb_per_split) stages = p.kb_per_split;
+  if (stage_cap > 0 && stages > stage_cap) stages = stage_cap;
+  if (stages < 2) stages = 2;
+  p.stages = stages;
+  const int smem_bytes = stages * Cfg::kStageBytes + Cfg::kCBytes + 1024 + 256;
   const int tiles = p.num_m * p.num_n * p.splits;
   const int grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
-  launch_k(kern, grid, 256, Cfg::kSmemBytes, stream, ma, mb, mc, p);
+  launch_k(kern, grid, 256, smem_bytes, stream, ma, mb, mc, p);
   ctx->launches++;
   return 0;
 }
