@@ -348,10 +348,22 @@ def run_reference(args, rank, world):
     Eng = make_reference_engine_cls()
     eng = Eng(*wl.engine_args())
     eng.setup(cfg, init_weights(cfg, seed=0), wl.train, selected_param_names(cfg, wl.train), wl.seed)
-    eng.run_ticks(args.warmup)
+    # bounded sample: the fp32 CPU path needs ~10-80 s for one early (prefill / fine-tune heavy) C2 tick, so the
+    # warm-up is one tick (tick 0: oracle caches and threads warm) and the timed ticks stop at a wall-clock
+    # budget; the same ticks-from-0 sample as the cpu_baseline leg of the GPU arm (the whole arm ends in minutes)
+    t_w = time.perf_counter()
+    while eng._done < min(args.warmup, 1) and time.perf_counter() - t_w < args.ref_seconds / 6:
+        before = eng._done
+        eng.run_ticks(1)
+        if eng._done == before:
+            break
     n0 = len(eng.tick_tokens)
     t0 = time.perf_counter()
-    eng.run_ticks(args.steps)
+    while len(eng.tick_tokens) - n0 < args.steps and time.perf_counter() - t0 < args.ref_seconds:
+        before = eng._done
+        eng.run_ticks(1)
+        if eng._done == before:
+            break
     wall = time.perf_counter() - t0
     toks = sum(eng.tick_tokens[n0:])
     k = len(eng.tick_tokens) - n0
@@ -363,7 +375,8 @@ def run_reference(args, rank, world):
         "config": {"workload": f"{wl.name}: {cfg.name} hybrid serving + DPO ({args.workload})", "model": cfg.name,
                    "path": "unmodified macesim Engine bins + fp32 CPU oracle arithmetic (oracle/ref_arm.py)"},
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
-                         "sample": f"ticks {args.warmup}..{args.warmup + k} of the trace (from tick 0)"},
+                         "sample": f"ticks {n0}..{n0 + k} of the trace (from tick 0; warm-up and timed ticks "
+                                   f"bounded by {args.ref_seconds:.0f} s of wall clock), {toks} tokens"},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -381,6 +394,7 @@ def main():
     ap.add_argument("--kv-tokens", type=int, default=None, help="prompt KV capacity in tokens (default: the workload's)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=120.0, help="--impl reference: wall-clock bound of the timed ticks")
     args = ap.parse_args()
     from paper_2510_03283_b200.dist import init_from_env
 
