@@ -95,15 +95,28 @@ __global__ void norm_bwd_kernel(const float* __restrict__ x, int ldx, const int*
   for (int c = threadIdx.x; c < 2 * d; c += blockDim.x) part[(size_t)blockIdx.x * 2 * d + c] = sh[c];
 }
 
-// out[c] += sum_b part[b * ld + c]   (fixed order over b)
-__global__ void col_reduce_kernel(const float* __restrict__ part, int nb, int ld, int ncols, float* __restrict__ out) {
+// out[c] += sum_b part[b * ld + c], deterministic: CTA = 32 columns x 8 row groups; group g sums partials
+// b = g, g + 8, ... in order (4 independent chains), the 8 group sums are added in fixed order
+__global__ void __launch_bounds__(256) col_reduce_kernel(const float* __restrict__ part, int nb, int ld, int ncols,
+                                                         float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncols) return;
-  float s = 0.f;
-  for (int b = 0; b < nb; ++b) s += part[(size_t)b * ld + c];
-  out[c] += s;
+  __shared__ float red[8][33];
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+  if (c < ncols) {
+    int k = 0;
+    for (int b = g; b < nb; b += 8, ++k) s[k & 3] += part[(size_t)b * ld + c];
+  }
+  red[g][cl] = (s[0] + s[1]) + (s[2] + s[3]);
+  __syncthreads();
+  if (g == 0 && c < ncols) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][cl];
+    out[c] += t;
+  }
 }
 
 // column sums of a bf16 matrix (bias grads), partial per row-chunk then col_reduce
@@ -114,9 +127,14 @@ __global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ y, int n, i
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
   const int r0 = blockIdx.y * rows_per_block, r1 = min(n, r0 + rows_per_block);
-  float s = 0.f;
-  for (int r = r0; r < r1; ++r) s += __bfloat162float(y[(size_t)r * ld + c]);
-  part[(size_t)blockIdx.y * N + c] = s;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent chains: loads in flight
+  int r = r0;
+  for (; r + 8 <= r1; r += 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s[i] += __bfloat162float(y[(size_t)(r + i) * ld + c]);
+  }
+  for (int i = 0; r < r1; ++r, ++i) s[i] += __bfloat162float(y[(size_t)r * ld + c]);
+  part[(size_t)blockIdx.y * N + c] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
 // ------------------------------------------------------------------ activation backward
@@ -370,10 +388,10 @@ extern "C" int mace_norm_bwd(mace_ctx* ctx, const float* x, int ldx, const int* 
   else if (per_lane <= 128) MACE_NB(128);
   else return mace_fail(ctx, MACE_ERR_ARG, "norm_bwd: d too large");
 #undef MACE_NB
-  launch_k(col_reduce_kernel, (d + 255) / 256, 256, 0, s, workspace, nb, 2 * d, d, dw);
+  launch_k(col_reduce_kernel, (d + 31) / 32, 256, 0, s, workspace, nb, 2 * d, d, dw);
   ctx->launches += 2;
   if (layernorm && db) {
-    launch_k(col_reduce_kernel, (d + 255) / 256, 256, 0, s, workspace + d, nb, 2 * d, d, db);
+    launch_k(col_reduce_kernel, (d + 31) / 32, 256, 0, s, workspace + d, nb, 2 * d, d, db);
     ctx->launches++;
   }
   return mace_check_launch(ctx, "norm_bwd");
@@ -387,7 +405,7 @@ extern "C" int mace_colsum_bf16(mace_ctx* ctx, const void* y, int n, int N, int 
   const int nb = (n + rpb - 1) / rpb;
   if (workspace_bytes < (size_t)nb * N * 4) return mace_fail(ctx, MACE_ERR_ARG, "colsum: workspace too small");
   launch_k(colsum_bf16_kernel, dim3((N + 255) / 256, nb), 256, 0, s, (const __nv_bfloat16*)y, n, N, ld, rpb, workspace);
-  launch_k(col_reduce_kernel, (N + 255) / 256, 256, 0, s, workspace, nb, N, N, out);
+  launch_k(col_reduce_kernel, (N + 31) / 32, 256, 0, s, workspace, nb, N, N, out);
   ctx->launches += 2;
   return mace_check_launch(ctx, "colsum");
 }
