@@ -14,6 +14,7 @@ hand-written sm_100a kernel (see csrc/). Device state that persists across ticks
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass
 
@@ -110,7 +111,8 @@ class HybridModel:
         self.last_token = torch.zeros(max_slots, **i32)
         self.dec_counters = torch.zeros(max_slots * H, **i32)  # decode chunk-merge counters (self-cleaning)
         self.dec_work = torch.zeros(1, dtype=torch.int64, device=self.dev)  # decode ticket counter (monotonic)
-        self.decode_impl = 0  # 0 auto (tcgen05 swap-AB for GQA, CUDA-core streaming for MHA), 1, 2 forced
+        # 0 auto (tcgen05 swap-AB for GQA, CUDA-core streaming for MHA), 1 / 2 forced (MACE_DECODE_IMPL: sweeps)
+        self.decode_impl = int(os.environ.get("MACE_DECODE_IMPL", "0"))
         self.kv = MaceKvLayout(
             ptab=self.ptab.data_ptr(), max_prompt_pages=self.maxpp, dtab=self.dtab.data_ptr(),
             max_dec_pages=self.maxdp, dec_base=self.dec_base.data_ptr(), dec_first=self.dec_first.data_ptr(),
