@@ -20,6 +20,7 @@ Clock modes:
 """
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, replace
 
@@ -28,7 +29,7 @@ import torch
 
 from .batch import KIND_DECODE, KIND_FT, KIND_PREFILL, PAGE, FtPair, TickBatch
 from .config import ModelConfig, TrainConfig
-from .hostfast import FastPriorityQueue, NormStream
+from .hostfast import FastPriorityQueue, NormStream, fast_schedule_iteration
 from .hoststats import BatchedHeadStats
 from .kvmanager import GpuPrefixTrie, GroupPool, plan_prefill_pages
 from .model import HybridModel
@@ -37,11 +38,13 @@ from .refpath import ensure_macesim
 ensure_macesim()
 import macesim.engine as _ref_engine  # noqa: E402
 from macesim.cache import dfs_order as _ref_dfs_order  # noqa: E402
+from macesim.scheduler import schedule_iteration as _ref_schedule_iteration  # noqa: E402
 from macesim.cost_model import CostProfile  # noqa: E402
 from macesim.engine import Engine  # noqa: E402
 from macesim.workload import WorkloadType  # noqa: E402
 
 
+_FAST_ALG1 = os.environ.get("MACE_FAST_ALG1", "1") != "0"  # A/B switch for host profiling
 DECODE_CHUNK_PAGES = 128  # decode contexts longer than 2048 tokens are split into chunks (merged on device)
 
 
@@ -484,6 +487,16 @@ class GpuEngine(Engine):
         for i, r in enumerate(rows):
             out[r.id] = (kl[i], rl[i])
         return out
+
+    def _plan(self):  # engine.py:393 — the reference _plan with Alg. 1's inlined restatement (hostfast.py)
+        if not (self.fast_host and _FAST_ALG1 and isinstance(self.queue, FastPriorityQueue)):
+            return super()._plan()
+        _ref_engine.schedule_iteration = lambda q, *a, _q=self.queue, **k: (
+            fast_schedule_iteration(q, *a, **k) if q is _q else _ref_schedule_iteration(q, *a, **k))
+        try:
+            return super()._plan()
+        finally:
+            _ref_engine.schedule_iteration = _ref_schedule_iteration
 
     def _synth_norms(self, req, rs):  # engine.py:433 — same draws, served from the per-request block stream
         return self.norm_stream.norms(req, rs).tolist()

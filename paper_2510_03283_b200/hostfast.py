@@ -24,6 +24,7 @@ from .refpath import ensure_macesim
 
 ensure_macesim()
 from macesim.priority import PriorityContractError, PriorityQueue  # noqa: E402
+from macesim.scheduler import Bin, TickPlan  # noqa: E402
 from macesim.workload import WorkloadType  # noqa: E402
 
 _FT = WorkloadType.FINETUNE
@@ -49,6 +50,15 @@ class FastPriorityQueue(PriorityQueue):
         self._live = 0
         self._order: list[int] | None = None  # pop order of live slots after refresh (None: stale)
         self._cur = 0
+        # id -> (arrival, base, growth, is fine-tune, workload): a prefill turns into a decode in place
+        # (workload.py:64-66), so an entry is only reused while the request's workload is unchanged
+        self._meta: dict[int, tuple] = {}
+
+    def _meta_of(self, req) -> tuple:
+        w = req.workload
+        m = (req.arrival_time, self.params.base[w], self.params.growth[w], w is _FT, w)
+        self._meta[req.id] = m
+        return m
 
     def __len__(self) -> int:
         return self._live
@@ -83,8 +93,24 @@ class FastPriorityQueue(PriorityQueue):
         self._n = n
         self._order = None
 
-    def push(self, req, t=None) -> None:  # priority.py:118-119
-        key = self._key(req, self._last_refresh if t is None else t)
+    def push(self, req, t=None) -> None:  # priority.py:118-119 (key of _key / priority_of, same arithmetic)
+        t = self._last_refresh if t is None else t
+        m = self._meta.get(req.id)
+        if m is None or m[4] is not req.workload:
+            m = self._meta_of(req)
+        arrival, base, growth, is_ft, _ = m
+        if t < arrival:
+            raise PriorityContractError(
+                f"priority query at t={t} before arrival of request {req.id} at {arrival}")
+        p = base + growth * (t - arrival)  # dynamic_priority (priority.py:73)
+        if is_ft and self.loss_fn is not None:  # ft_total_priority (priority.py:76-81)
+            loss = self.loss_fn(req)
+            if loss < 0:
+                raise PriorityContractError("loss must be >= 0 under the positive-loss convention")
+            p = p + self.params.gamma * loss
+        req.priority_state.value = p
+        req.priority_state.refreshed_at = t
+        key = (-p, arrival, req.id)
         if self._n == self._neg.shape[0]:
             if self._live < self._n // 2:
                 self._compact()
@@ -92,13 +118,12 @@ class FastPriorityQueue(PriorityQueue):
                 self._grow()
         k = self._n
         self._n += 1
-        w = req.workload
         self._neg[k] = key[0]
-        self._arr[k] = key[1]
-        self._bg[k, 0] = self.params.base[w]
-        self._bg[k, 1] = self.params.growth[w]
+        self._arr[k] = arrival
+        self._bg[k, 0] = base
+        self._bg[k, 1] = growth
         self._id[k] = req.id
-        self._ft[k] = w is _FT
+        self._ft[k] = is_ft
         self._alive[k] = True
         self._req[k] = req
         self._live += 1
@@ -184,3 +209,74 @@ class NormStream:
 
     def drop(self, rid: int) -> None:
         self.buf.pop(rid, None)
+
+
+def fast_schedule_iteration(queue, capacity_budget, cfg, estimator, t, hard_limit=None):
+    """Alg. 1 exactly as scheduler.py:133-188 (same dequeue stop rule, same best-fit score arithmetic
+    lambda1*|free - mem| + lambda2*|maxlat - lat| with free = budget - used, same strict '<' tie rule,
+    same requeue / defer / reject lists), with the Bin methods (scheduler.py:81-117) inlined into local
+    arithmetic. Returns the reference TickPlan / Bin types; tests/test_host_cpu.py checks plan-for-plan
+    equality against the reference on randomized queues."""
+    if hard_limit is None:
+        hard_limit = capacity_budget
+    plan = TickPlan(bin=Bin(capacity_budget))
+    FT = _FT
+    max_ft, max_inf = cfg.max_ft_batch, cfg.max_decode_batch
+    l1, l2 = cfg.lambda1, cfg.lambda2
+    stop_mem = cfg.tau_mem * capacity_budget
+    tau_task = cfg.tau_task
+    # bin state: [used, maxlat, n_inf, n_ft, tasks, ests]
+    bins: list[list] = []
+    deferred: list = []
+    dequeued = plan.dequeued
+    rejected = plan.rejected
+    examined = 0
+    count = 0
+    while queue:
+        if bins and (bins[0][0] >= stop_mem or count >= tau_task):
+            break
+        task = queue.pop()
+        count += 1
+        dequeued.append(task)
+        est = estimator(task)
+        mem, lat = est.mem, est.lat
+        if mem > hard_limit:
+            rejected.append(task)
+            continue
+        if mem > capacity_budget:
+            deferred.append(task)
+            continue
+        is_ft = task.workload is FT
+        best = None
+        best_score = float("inf")
+        for b in bins:
+            examined += 1
+            free = capacity_budget - b[0]
+            if free < mem:
+                continue
+            if (b[3] < max_ft) if is_ft else (b[2] < max_inf):
+                score = l1 * abs(free - mem) + l2 * abs(b[1] - lat)
+                if score < best_score:
+                    best_score = score
+                    best = b
+        if best is None:
+            best = [0.0, 0.0, 0, 0, [], []]
+            bins.append(best)
+            plan.bins_opened += 1
+        best[4].append(task)
+        best[5].append(est)
+        best[0] += mem
+        best[1] = max(best[1], lat)
+        if is_ft:
+            best[3] += 1
+        else:
+            best[2] += 1
+    plan.bins_examined = examined
+    if bins:
+        b0 = bins[0]
+        plan.bin = Bin(capacity_budget, tasks=b0[4], estimates=b0[5], used_memory=b0[0], max_latency=b0[1],
+                       n_inference=b0[2], n_ft=b0[3])
+        for later in bins[1:]:
+            plan.requeued.extend(later[4])
+    plan.requeued.extend(deferred)
+    return plan

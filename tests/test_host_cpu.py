@@ -257,3 +257,47 @@ def test_cached_prefix_len_matches_reference():
         q = prompts[int(rng.integers(0, len(prompts)))]
         q = q[: int(rng.integers(1, len(q) + 1))] + rng.integers(0, 6, int(rng.integers(0, 5))).tolist()
         assert gpu_t.cached_prefix_len(q) == ref_t.cached_prefix_len(q)
+
+
+def test_fast_schedule_iteration_matches_reference():
+    """hostfast.fast_schedule_iteration returns the reference Alg. 1 plan (scheduler.py:133-188) task for task on
+    randomized queues: mixed workloads, tight budgets (reject / defer), bin caps, tau_mem / tau_task stops."""
+    import numpy as np
+
+    from macesim.cost_model import WorkloadEstimate
+    from macesim.priority import PriorityParams, PriorityQueue
+    from macesim.scheduler import SchedulerConfig, schedule_iteration
+    from macesim.workload import PreferencePair, Request, WorkloadType
+    from paper_2510_03283_b200.hostfast import FastPriorityQueue, fast_schedule_iteration
+
+    rng = np.random.default_rng(11)
+    kinds = [WorkloadType.PREFILL, WorkloadType.DECODE, WorkloadType.FINETUNE]
+    for trial in range(200):
+        cfg = SchedulerConfig(tau_task=int(rng.integers(1, 40)), max_decode_batch=int(rng.integers(1, 12)),
+                              max_ft_batch=int(rng.integers(1, 4)), tau_mem=float(rng.choice([0.5, 0.9, 1.0])))
+        budget = float(rng.choice([50.0, 200.0, 1000.0]))
+        hard = budget * float(rng.choice([1.0, 1.5]))
+        ests = {}
+        queues = (PriorityQueue(PriorityParams(), lambda r: 0.1), FastPriorityQueue(PriorityParams(), lambda r: 0.1))
+        for rid in range(int(rng.integers(0, 60))):
+            w = kinds[int(rng.integers(0, 3))]
+            pair = PreferencePair(0.5, 4, 4) if w is WorkloadType.FINETUNE else None
+            arr = float(rng.integers(0, 5))
+            ests[rid] = WorkloadEstimate(mem=float(rng.choice([1.0, 10.0, 60.0, 300.0, rng.random() * 100])),
+                                         lat=float(rng.choice([20.0, 120.0, rng.random() * 50])))
+            for q in queues:
+                q.push(Request(id=rid, tenant=0, workload=w, arrival_time=arr, prompt_tokens=[1], target_output_len=4,
+                               pair=pair), 5.0)
+        for q in queues:
+            q.refresh(5.0)
+        est = lambda r: ests[r.id]  # noqa: E731
+        a = schedule_iteration(queues[0], budget, cfg, est, 5.0, hard_limit=hard)
+        b = fast_schedule_iteration(queues[1], budget, cfg, est, 5.0, hard_limit=hard)
+        ids = lambda xs: [r.id for r in xs]  # noqa: E731
+        assert ids(a.bin.tasks) == ids(b.bin.tasks), trial
+        assert ids(a.requeued) == ids(b.requeued) and ids(a.rejected) == ids(b.rejected)
+        assert ids(a.dequeued) == ids(b.dequeued)
+        assert (a.bins_opened, a.bins_examined) == (b.bins_opened, b.bins_examined)
+        assert (a.bin.used_memory, a.bin.max_latency, a.bin.n_inference, a.bin.n_ft) == \
+            (b.bin.used_memory, b.bin.max_latency, b.bin.n_inference, b.bin.n_ft)
+        assert len(queues[0]) == len(queues[1])
