@@ -893,28 +893,64 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     return mace_fail(ctx, MACE_ERR_ARG, "gemm: operands need 16-byte aligned rows (ld % 8 == 0)");
   if (g->mode < EPI_BF16 || g->mode > EPI_BF16_GELU) return mace_fail(ctx, MACE_ERR_ARG, "gemm: bad epilogue mode");
 
-  // tile shape / split-K heuristic (tools/gemm_sweep.py on B200): a k-block costs about the same for
-  // BN = 64 and 128 (TMA/issue-bound), BN = 256 only pays once its tiles fill the SMs; split-K only when
-  // every split keeps >= 12 k-blocks (the slab round trip + finalize launch cost ~2-3 us)
+  // tile shape (tools/gemm_sweep.py on B200). Big GEMMs (>= one full wave of 256 x 256 pair tiles): the
+  // CTA-pair kernel (MN-major operands: single-CTA BN 256). Otherwise a per-k-block cost model fitted on the
+  // tick's shapes picks among single-CTA BN 64 / 128 / 192 / 256 and pair BN 128:
+  //   t ~ waves x k-blocks x c(BN),  c = 0.17 / 0.19 / 0.34 / 0.49 us (single), 0.155 us (pair 128)
+  // (a fixed ~4 us launch / fill / epilogue cost is common to all; pair only with >= 48 k-blocks). Split-K only
+  // for < 37 tiles with >= 24
+  // k-blocks per split: measured slower everywhere else (slab round trip + finalize launch).
   const int num_m = (g->M + kBM - 1) / kBM;
+  const int num_m2 = (g->M + 255) / 256;
   const int kb_total = (g->K + kBK - 1) / kBK;
-  int bn = 256;
-  if ((long)num_m * ((g->N + 255) / 256) < ctx->num_sms) bn = 128;
-  if (bn == 128 && kb_total < 24 && (long)num_m * ((g->N + 127) / 128) < ctx->num_sms / 2) bn = 64;
-  const long tiles = (long)num_m * ((g->N + bn - 1) / bn);
+  const bool pair_ok = !g->a_mn_major && !g->b_mn_major && g->split_k <= 0 && g->mode != EPI_F32_ATOMIC &&
+                       ((uintptr_t)g->out & 15) == 0 &&
+                       ((size_t)g->ldo * ((g->mode == EPI_BF16 || g->mode == EPI_BF16_GELU) ? 2 : 4)) % 16 == 0;
+  const long sms = ctx->num_sms, pairs = ctx->num_sms / 2;
+  int bn = 128, pair_bn = 0;
+  if (pair_ok && (long)num_m2 * ((g->N + 255) / 256) >= sms) {
+    pair_bn = 256;
+  } else if (!pair_ok && (long)num_m * ((g->N + 255) / 256) >= sms) {
+    bn = 256;
+  } else {
+    static const int kBn[4] = {64, 128, 192, 256};
+    static const double kCost[4] = {0.17, 0.19, 0.34, 0.49};
+    double best = 1e30;
+    for (int c = 0; c < 4; ++c) {
+      const long t = (long)num_m * ((g->N + kBn[c] - 1) / kBn[c]);
+      const double cost = (double)((t + sms - 1) / sms) * kb_total * kCost[c];
+      if (cost < best) {
+        best = cost;
+        bn = kBn[c];
+      }
+    }
+    if (pair_ok && kb_total >= 48) {  // the pair kernel's fill only pays off over long K loops
+      const long t2 = (long)num_m2 * ((g->N + 127) / 128);
+      if ((double)((t2 + pairs - 1) / pairs) * kb_total * 0.155 < best) pair_bn = 128;
+    }
+  }
   int splits = g->split_k > 0 ? g->split_k : 1;
-  if (g->split_k <= 0 && tiles < ctx->num_sms) {
-    splits = (int)(ctx->num_sms / tiles);
-    int max_split = kb_total / 12;
+  if (g->split_k <= 0 && kb_total >= 96 && (long)num_m * ((g->N + 127) / 128) < pairs) {
+    // long K over few tiles (decode-sized down projections, FT dW): split K across the idle SMs (BN 128)
+    bn = 128;
+    pair_bn = 0;
+    const long tiles = (long)num_m * ((g->N + bn - 1) / bn);
+    splits = (int)(sms / tiles);
+    const int max_split = kb_total / 12;
     if (splits > max_split) splits = max_split;
     if (splits < 1) splits = 1;
   }
-  // tuning override (tools/gemm_bench.py sweeps): MACE_GEMM_FORCE="<bn>,<splits>"
+  // tuning override (tools/gemm_sweep.py): MACE_GEMM_FORCE="<bn>,<splits>" | "pair,<bn>" | "single"
   if (const char* f = getenv("MACE_GEMM_FORCE")) {
     int fb = 0, fs = 0;
     if (sscanf(f, "%d,%d", &fb, &fs) == 2) {
-      if (fb == 64 || fb == 128 || fb == 256) bn = fb;
+      if (fb == 64 || fb == 128 || fb == 192 || fb == 256) bn = fb;
       if (fs >= 1) splits = fs;
+      pair_bn = 0;
+    } else if (sscanf(f, "pair,%d", &fb) == 1 && (fb == 128 || fb == 256) && pair_ok) {
+      pair_bn = fb;
+    } else {
+      pair_bn = 0;
     }
   }
   GemmEpilogue ep;
@@ -924,20 +960,7 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   ep.alpha = g->alpha == 0.f ? 1.f : g->alpha;
   ep.mode = g->mode;
   ep.split_stride = 0;
-  // CTA-pair kernel: K-major operands, no split-K, TMA-store epilogue, and enough 256-row tiles to fill
-  // the 74 pairs (tools/gemm_sweep.py); MACE_GEMM_FORCE="pair,<bn>" / "single" override for sweeps
   {
-    int pair_bn = 0;
-    const int num_m2 = (g->M + 255) / 256;
-    if (!g->a_mn_major && !g->b_mn_major && g->split_k <= 0 && g->mode != EPI_F32_ATOMIC && tma_epi_ok(ep)) {
-      if ((long)num_m2 * ((g->N + 255) / 256) >= ctx->num_sms) pair_bn = 256;
-      else if ((long)num_m2 * ((g->N + 127) / 128) >= ctx->num_sms) pair_bn = 128;
-      if (const char* f = getenv("MACE_GEMM_FORCE")) {
-        int fb = 0;
-        if (sscanf(f, "pair,%d", &fb) == 1 && (fb == 128 || fb == 256)) pair_bn = fb;
-        else pair_bn = 0;
-      }
-    }
     if (pair_bn) {
       const int rc2 = pair_bn == 256 ? launch_gemm2<256>(ctx, g, stream, ep) : launch_gemm2<128>(ctx, g, stream, ep);
       if (rc2) return rc2;
@@ -965,6 +988,8 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   int rc;
   if (bn == 256)
     rc = dispatch_major<256>(ctx, g, splits, stream, ep);
+  else if (bn == 192)
+    rc = dispatch_major<192>(ctx, g, splits, stream, ep);
   else if (bn == 128)
     rc = dispatch_major<128>(ctx, g, splits, stream, ep);
   else
