@@ -21,4 +21,6 @@ ncu --profile-from-start off --set full --clock-control none -k regex:gemm_tc2_k
     -o gpurun_out/gemm_pair python tools/profile_tick.py --workload c4 --steps 1 > gpurun_out/ncu_gemm2.log 2>&1
 ncu --profile-from-start off --set full --clock-control none -k regex:attn_fa_kernel -s 4 -c 1 \
     -o gpurun_out/attn_fa_c4 python tools/profile_tick.py --workload c4 --steps 1 > gpurun_out/ncu_attn_fa4.log 2>&1
+ncu --profile-from-start off --set full --clock-control none -k regex:attn_bwd_tc -s 0 -c 1 \
+    -o gpurun_out/attn_bwd_c4 python tools/profile_tick.py --workload c4 --steps 1 > gpurun_out/ncu_attn_bwd4.log 2>&1
 ls -la gpurun_out

@@ -54,7 +54,7 @@ def raw(rep):
 def main():
     OUT.mkdir(exist_ok=True)
     summary = {}
-    for name in ("attn_decode", "gemm", "attn_fa", "attn_decode_tc", "gemm_pair", "attn_fa_c4"):
+    for name in ("attn_decode", "gemm", "attn_fa", "attn_decode_tc", "gemm_pair", "attn_fa_c4", "attn_bwd_c4"):
         rep = SRC / f"{name}.ncu-rep"
         if rep.exists():
             summary[name] = raw(rep)
