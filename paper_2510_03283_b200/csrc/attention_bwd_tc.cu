@@ -30,7 +30,8 @@ struct BwdCfg {
   static constexpr int V_OFF = TILE;
   static constexpr int QD_OFF = 2 * TILE;           // buffer b: Q at QD_OFF + 2b*TILE, dO at +TILE
   static constexpr int DS_OFF = 6 * TILE;           // dS [128 keys][128 queries] bf16, 128B swizzle
-  static constexpr int BAR_OFF = DS_OFF + 128 * 128 * 2;
+  static constexpr int LD_OFF = DS_OFF + 128 * 128 * 2;  // lse * log2e [128], D [128] of the step's queries
+  static constexpr int BAR_OFF = LD_OFF + 2 * 128 * 4;
   static constexpr int SMEM = BAR_OFF + 128 + 1024;
   static constexpr uint32_t COL_S = 0, COL_P = 128, COL_DV = 256, COL_DK = 256 + HD;  // TMEM (dQ reuses COL_S)
 };
@@ -173,16 +174,25 @@ __global__ void __launch_bounds__(160, 1)
     const int r = threadIdx.x;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     const uint32_t ds_s = smem_u32(smem + C::DS_OFF);
+    float* l2_s = reinterpret_cast<float*>(smem + C::LD_OFF);
+    float* d_s = l2_s + 128;
     const int kg = j * 128 + r;  // this thread's key (S^T phase)
     for (int s = 0; s < steps; ++s) {
       int hq, qb;
       step_q(s, hq, qb);
+      // ---- the step's 128 query rows of lse (x log2e) and D -> smem (one load per thread instead of 128
+      // dependent broadcast loads per thread); every reader of the previous step passed mm_done already
+      const int q0 = qb * 128;
+      {
+        const int q = q0 + r;
+        const bool ok = q < n;
+        l2_s[r] = ok ? __ldg(lse + (size_t)(base + q) * Hq + hq) * 1.4426950408889634f : 0.f;
+        d_s[r] = ok ? __ldg(Dv + (size_t)(base + q) * Hq + hq) : 0.f;
+      }
+      named_bar_sync(1, 128);
       mbar_wait(sp_done, s & 1);
       tc_fence_after();
       // ---- P^T, dS^T (thread = key row); P^T -> TMEM bf16, dS -> smem
-      const int q0 = qb * 128;
-      const float* lse_col = lse + (size_t)(base + q0) * Hq + hq;
-      const float* d_col = Dv + (size_t)(base + q0) * Hq + hq;
 #pragma unroll 1
       for (int c0 = 0; c0 < 128; c0 += 32) {
         uint32_t sv[32], dv[32];
@@ -197,11 +207,9 @@ __global__ void __launch_bounds__(160, 1)
           for (int e = 0; e < 2; ++e) {
             const int q = q0 + c0 + c + e;
             const bool ok = q < n && kg < n && kg <= q;
-            const float l2 = ok ? __ldg(lse_col + (size_t)(c0 + c + e) * Hq) * 1.4426950408889634f : 0.f;
-            const float Dq = ok ? __ldg(d_col + (size_t)(c0 + c + e) * Hq) : 0.f;
-            const float p = ok ? exp2f(__uint_as_float(sv[c + e]) * sl2 - l2) : 0.f;
+            const float p = ok ? exp2f(__uint_as_float(sv[c + e]) * sl2 - l2_s[c0 + c + e]) : 0.f;
             p2[e] = p;
-            d2[e] = p * (__uint_as_float(dv[c + e]) - Dq);
+            d2[e] = p * (__uint_as_float(dv[c + e]) - d_s[c0 + c + e]);
           }
           pp[c / 2] = pack_bf16(p2[0], p2[1]);
           dd[c / 2] = pack_bf16(d2[0], d2[1]);

@@ -34,9 +34,9 @@ struct DecTc {
   static constexpr int ATOM_BYTES = 128 * SWZ;          // 128 token rows x one swizzle atom of head dims
   static constexpr int TILE = KATOMS * ATOM_BYTES;      // one K (or V) tile of 128 tokens
 #ifndef MACE_DTC_STAGES128
-#define MACE_DTC_STAGES128 2
+#define MACE_DTC_STAGES128 3
 #endif
-  static constexpr int STAGES = HD >= 128 ? MACE_DTC_STAGES128 : 3;  // hd 64: 2 CTAs per SM
+  static constexpr int STAGES = HD >= 128 ? MACE_DTC_STAGES128 : 3;  // hd 64: 2 CTAs per SM; hd 128: 1 (C4: 3 stages 0.49 of HBM, 2 stages 0.33)
   static constexpr int Q_OFF = STAGES * 2 * TILE;       // 2 x [16 rows][HD] K-major
   static constexpr int Q_BYTES = KATOMS * 16 * SWZ;
   static constexpr int P_OFF = Q_OFF + 2 * Q_BYTES;     // 2 x P^T [16 rows][128 tok] K-major SW128
