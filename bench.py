@@ -288,6 +288,19 @@ def run_ours(args, rank, world, lock):
     # C1-C3 ticks (the largest single kernel of the step; the GEMM line aggregates ~60 launches of several GEMM
     # shapes), the projection GEMMs for the prefill-heavy C4; the other one rides along
     dominant_gemm = wl.name == "c4"
+    # DRAM traffic per launch of the same kernel from the committed ncu --set full capture of this workload
+    # (tools/ncu_capture.sh -> profiles/r1final_ncu_full_summary.json; cold-cache, serialised)
+    cap = {"c2": "attn_decode", "c3": "attn_decode_tc", "c4": "gemm_pair"}.get(wl.name)
+    prof = ROOT / "profiles" / "r1final_ncu_full_summary.json"
+    if cap and prof.exists():
+        rows = [r for r in json.loads(prof.read_text()).get(cap, []) if "dram_read" in r]
+        if rows:
+            tr = float(np.mean([r["dram_read"] + r["dram_write"] for r in rows]))
+            target = roof_gemm if dominant_gemm else roof_attn
+            target["traffic"] = tr
+            target["traffic_source"] = f"profiles/r1final_ncu_full_summary.json[{cap}] ({rows[0]['kernel']})"
+            if rows[0].get("algorithmic_bytes"):
+                target["traffic_over_algorithmic_in_capture"] = tr / float(np.mean([r["algorithmic_bytes"] for r in rows]))
     out["roofline"] = roof_gemm if dominant_gemm else roof_attn
     out["roofline_other"] = roof_attn if dominant_gemm else roof_gemm
     n_ft_ticks = sum(1 for op in tape if op[0] == "step" and op[1].ft_pairs)
