@@ -12,9 +12,11 @@ from paper_2510_03283_b200.build import build  # noqa: E402
 
 build()
 ctx = Ctx(0)
+BWD = "--bwd" in sys.argv
+argv = [a for a in sys.argv[1:] if a != "--bwd"]
 cases = [(128, 32, 8, 16, 1280), (128, 32, 8, 4, 2048), (64, 12, 12, 16, 512), (64, 32, 8, 16, 1920)]
-if len(sys.argv) > 5:
-    cases = [tuple(int(x) for x in sys.argv[1:6])]
+if len(argv) >= 5:
+    cases = [tuple(int(x) for x in argv[:5])]
 for hd, Hq, Hkv, S, n in cases:
     W = (Hq + 2 * Hkv) * hd
     T = S * n
@@ -36,6 +38,20 @@ for hd, Hq, Hkv, S, n in cases:
     def run():
         ops.attn_fwd(ctx, qkv, Hq, Hkv, hd, seqs, items, None, lay, None, None, out, lse=lse)
 
+    if BWD:  # time the backward of the same sequences (forward once for o / lse)
+        run()
+        dout = torch.randn(T, Hq * hd, device="cuda").bfloat16()
+        kblk = 128 if hd >= 64 else 64
+        nkb = (n + kblk - 1) // kblk
+        bitems = sorted([[si, h, kb, nkb - kb] for si in range(S) for h in range(Hkv) for kb in range(nkb)],
+                        key=lambda x: -x[3])
+        bitems = torch.tensor(bitems, dtype=torch.int32, device="cuda")
+        dqkv = torch.zeros(T, W, device="cuda")
+
+        def run():  # noqa: F811
+            dqkv.zero_()
+            ops.attn_bwd(ctx, qkv, out, dout, lse, Hq, Hkv, hd, seqs, bitems, dqkv=dqkv)
+
     for _ in range(3):
         run()
     torch.cuda.synchronize()
@@ -47,5 +63,5 @@ for hd, Hq, Hkv, S, n in cases:
     e1.record()
     e1.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / reps
-    flops = S * 4 * Hq * hd * (n * (n + 1) / 2)
+    flops = S * (10 if BWD else 4) * Hq * hd * (n * (n + 1) / 2)
     print(f"hd={hd} Hq={Hq} Hkv={Hkv} seqs={S}x{n}: {us:9.1f} us  {flops / us / 1e6:7.1f} TF/s  (items {items.shape[0]})")
