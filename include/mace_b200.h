@@ -61,6 +61,8 @@ enum mace_epilogue {
   MACE_EPI_F32_ADD = 2,    /* out fp32 += result (residual stream, grad accumulate) */
   MACE_EPI_F32_ATOMIC = 3, /* out fp32 += result via atomics (shared destination)   */
   MACE_EPI_BF16_GELU = 4,  /* out bf16 = gelu_tanh(result) (fused GPT-2 MLP activation) */
+  MACE_EPI_BF16_SWIGLU = 5,/* out bf16 [M, N] = silu(A.Bg^T) * (A.Bu^T) with B = [gate rows 0..N-1; up rows
+                              N..2N-1] (K-major, no bias): the fused Llama MLP activation */
 };
 typedef struct MaceGemmArgs {
   const void* a; int lda; int a_mn_major;

@@ -44,8 +44,10 @@ struct GemmParams {
   int dbg;       // trace builds only (tools/gemm_trace.py probes); 0 otherwise
   int b_static;  // B not written by the preceding kernel: first ring of B tiles loads before the PDL wait
   int stages;    // smem ring depth of the single-CTA kernel
+  int swiglu;    // EPI_BF16_SWIGLU: a BN tile = BN/2 gate rows (row n) + BN/2 up rows (row N + n) of B
   GemmEpilogue ep;
 };
+
 
 // Epilogue chunk of one warp (32 rows) through smem and a TMA store: registers -> 128B-swizzled
 // [32 rows][128 B] staging (conflict-free: 16-byte chunk q of row r lives at q ^ (r & 7)) ->
@@ -53,6 +55,54 @@ struct GemmParams {
 // bounds-clipped by the tensor map, so the epilogue no longer issues 32 row-strided stores per warp.
 MACE_DEV void stage_row_chunk16(uint8_t* st, uint32_t lane, int q, uint4 w) {
   *reinterpret_cast<uint4*>(st + lane * 128 + ((q ^ (lane & 7)) << 4)) = w;
+}
+
+// silu(gate) * up for the fused Llama MLP epilogue (fp32 accumulators, one bf16 rounding of the product)
+MACE_DEV float swiglu_f(float g, float u) { return g * u / (1.f + __expf(-g)); }
+
+// fused SwiGLU epilogue of one tile (both GEMM kernels): this warp's 32 rows, TMEM columns [0, BN/2) hold
+// the gate projection and [BN/2, BN) the up projection of the same BN/2 outputs; two 64-column chunks are
+// staged in the warp's two 4 KB buffers and TMA-stored; the accumulator is released after the last loads
+template <int BN>
+MACE_DEV void swiglu_epilogue(const CUtensorMap* map_c, uint8_t* smem_c, uint32_t t_row, int quarter, int lane,
+                              int row0, int col_base, int N, uint64_t* tempty, bool remote, uint32_t tempty_cluster) {
+  constexpr int HALF = BN / 2;
+#pragma unroll 1
+  for (int oc = 0; oc < HALF; oc += 64) {
+    uint32_t r[128];
+    tmem_ld_32x32b_x32(t_row + oc, *reinterpret_cast<uint32_t(*)[32]>(r));
+    tmem_ld_32x32b_x32(t_row + oc + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+    tmem_ld_32x32b_x32(t_row + HALF + oc, *reinterpret_cast<uint32_t(*)[32]>(r + 64));
+    tmem_ld_32x32b_x32(t_row + HALF + oc + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 96));
+    tmem_ld_wait();
+    if (oc + 64 >= HALF) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (remote) mbar_arrive_cluster(tempty_cluster);
+        else mbar_arrive(tempty);
+      }
+    }
+    const int col0 = col_base + oc;
+    if (col0 >= N) continue;
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    uint8_t* st = smem_c + (quarter * 2 + ((oc / 64) & 1)) * 4096;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = swiglu_f(__uint_as_float(r[q * 8 + j]), __uint_as_float(r[64 + q * 8 + j]));
+      stage_row_chunk16(st, lane, q, make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                                                pack_bf16(v[6], v[7])));
+    }
+    fence_proxy_async_shared();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(map_c, st, col0, row0);
+      bulk_commit();
+    }
+  }
 }
 
 #ifdef MACE_GEMM_TRACE
@@ -120,7 +170,10 @@ __global__ void __launch_bounds__(256, 1)
     // every index is warp-uniform and lives in uniform registers; one elected lane issues)
     auto load_b = [&](int stage, int kb, int n_blk) {
       uint8_t* sb = smem_b + stage * Cfg::kBBytes;
-      if (!B_MN) {
+      if (!B_MN && p.swiglu) {  // gate rows n*BN/2.. and up rows N + n*BN/2.. of the stacked [2N, K] weight
+        tma_load_2d(sb, &map_b, &full_bar[stage], kb * kBK, n_blk * (BN / 2));
+        tma_load_2d(sb + (BN / 2) * kBK * 2, &map_b, &full_bar[stage], kb * kBK, p.N + n_blk * (BN / 2));
+      } else if (!B_MN) {
         tma_load_2d(sb, &map_b, &full_bar[stage], kb * kBK, n_blk * BN);
       } else {
 #pragma unroll
@@ -274,6 +327,15 @@ __global__ void __launch_bounds__(256, 1)
       if (warp == 4 && lane == 0 && ti_ < 5) TRACE(8 + ti_ * 4 + 1);
 #endif
       if constexpr (TMA_EPI) {
+        if (p.swiglu) {
+          swiglu_epilogue<BN>(&map_c, smem_c, tmem_base + ((quarter * 32u) << 16) + acc * BN, quarter, lane,
+                              m_blk * kBM + quarter * 32, n_blk * (BN / 2), p.N, &tempty_bar[acc], false, 0);
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+          continue;
+        }
         // per group of two staged chunks (bf16: 2 x 64 columns, fp32: 2 x 32): every TMEM load of the group is
         // issued before one wait, the accumulator is handed back to the MMA warp as soon as the tile's last
         // group is in registers, and one proxy fence + one commit cover both staging buffers
@@ -531,7 +593,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
     auto load_b = [&](int stage, int kb, int n_blk, uint32_t bar) {
-      tma_load_2d_pair(smem_b + stage * Cfg::kBBytes, &map_b, bar, kb * kBK, n_blk * BN + rank * (BN / 2));
+      // swiglu: the leader holds the gate rows, the peer the up rows of the same BN/2 outputs
+      const int row = p.swiglu ? (rank ? p.N : 0) + n_blk * (BN / 2) : n_blk * BN + rank * (BN / 2);
+      tma_load_2d_pair(smem_b + stage * Cfg::kBBytes, &map_b, bar, kb * kBK, row);
     };
     const uint32_t full0 = mapa_shared(smem_u32(&full_bar[0]), 0);  // leader's full barriers
     int pre = 0;
@@ -624,6 +688,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row0 = m_blk * 256 + rank * 128 + quarter * 32;
+      if (p.swiglu) {
+        swiglu_epilogue<BN>(&map_c, smem_c, tmem_base + ((quarter * 32u) << 16) + acc * BN, quarter, lane, row0,
+                            n_blk * (BN / 2), p.N, nullptr, true, tempty0 + acc * 8);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += cw) {
         const int col0 = n_blk * BN + c0;
@@ -744,7 +817,7 @@ static int make_map(MaceCtx* ctx, CUtensorMap* map, const void* ptr, uint64_t in
 // output map of the TMA-store epilogue: {cols, rows} (or {cols, rows, splits} for split-K slabs),
 // box = {128 bytes of columns, 32 rows}, 128B swizzle (matches stage_row_chunk16)
 static int make_map_c(MaceCtx* ctx, CUtensorMap* map, const GemmEpilogue& ep, int M, int N, int splits) {
-  const bool bf16 = ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU;
+  const bool bf16 = ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU || ep.mode == EPI_BF16_SWIGLU;
   const uint64_t es = bf16 ? 2 : 4;
   cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)splits};
   cuuint64_t strides[2] = {(cuuint64_t)ep.ldo * es, (cuuint64_t)ep.split_stride * es};
@@ -760,7 +833,7 @@ static int make_map_c(MaceCtx* ctx, CUtensorMap* map, const GemmEpilogue& ep, in
 
 // the TMA-store epilogue needs 16-byte aligned output rows (and slabs)
 static bool tma_epi_ok(const GemmEpilogue& ep) {
-  const size_t es = (ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU) ? 2 : 4;
+  const size_t es = (ep.mode == EPI_BF16 || ep.mode == EPI_BF16_GELU || ep.mode == EPI_BF16_SWIGLU) ? 2 : 4;
   return ((uintptr_t)ep.out & 15) == 0 && ((size_t)ep.ldo * es) % 16 == 0 && (ep.split_stride * es) % 16 == 0;
 }
 
@@ -771,14 +844,17 @@ static int launch_gemm(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStre
   // A logical [M,K]; K-major storage [M, lda>=K], MN-major storage [K, lda>=M]
   int rc = A_MN ? make_map(ctx, &ma, g->a, g->M, g->K, g->lda, 64, kBK) : make_map(ctx, &ma, g->a, g->K, g->M, g->lda, kBK, kBM);
   if (rc) return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm: tensor map A encode failed");
-  rc = B_MN ? make_map(ctx, &mb, g->b, g->N, g->K, g->ldb, 64, kBK) : make_map(ctx, &mb, g->b, g->K, g->N, g->ldb, kBK, BN);
+  const bool swiglu = ep.mode == EPI_BF16_SWIGLU;
+  rc = B_MN ? make_map(ctx, &mb, g->b, g->N, g->K, g->ldb, 64, kBK)
+            : make_map(ctx, &mb, g->b, g->K, swiglu ? 2 * g->N : g->N, g->ldb, kBK, swiglu ? BN / 2 : BN);
   if (rc) return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm: tensor map B encode failed");
   GemmParams p;
   p.M = g->M;
   p.N = g->N;
   p.K = g->K;
+  p.swiglu = swiglu ? 1 : 0;
   p.num_m = (g->M + kBM - 1) / kBM;
-  p.num_n = (g->N + BN - 1) / BN;
+  p.num_n = swiglu ? (g->N + BN / 2 - 1) / (BN / 2) : (g->N + BN - 1) / BN;
   p.kb_total = (g->K + kBK - 1) / kBK;
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
   p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
@@ -827,14 +903,16 @@ static int launch_gemm2(MaceCtx* ctx, const MaceGemmArgs* g, cudaStream_t stream
   CUtensorMap ma, mb, mc;
   if (make_map(ctx, &ma, g->a, g->K, g->M, g->lda, kBK, 128))
     return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm2: tensor map A encode failed");
-  if (make_map(ctx, &mb, g->b, g->K, g->N, g->ldb, kBK, BN / 2))
+  const bool swiglu = ep.mode == EPI_BF16_SWIGLU;
+  if (make_map(ctx, &mb, g->b, g->K, swiglu ? 2 * g->N : g->N, g->ldb, kBK, BN / 2))
     return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm2: tensor map B encode failed");
   GemmParams p{};
   p.M = g->M;
   p.N = g->N;
   p.K = g->K;
+  p.swiglu = swiglu ? 1 : 0;
   p.num_m = (g->M + 255) / 256;
-  p.num_n = (g->N + BN - 1) / BN;
+  p.num_n = swiglu ? (g->N + BN / 2 - 1) / (BN / 2) : (g->N + BN - 1) / BN;
   p.kb_total = (g->K + kBK - 1) / kBK;
   p.kb_per_split = p.kb_total;
   p.splits = 1;
@@ -891,7 +969,10 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 0;  // empty ragged batch: nothing to do
   if ((g->lda & 7) || (g->ldb & 7) || ((uintptr_t)g->a & 15) || ((uintptr_t)g->b & 15))
     return mace_fail(ctx, MACE_ERR_ARG, "gemm: operands need 16-byte aligned rows (ld % 8 == 0)");
-  if (g->mode < EPI_BF16 || g->mode > EPI_BF16_GELU) return mace_fail(ctx, MACE_ERR_ARG, "gemm: bad epilogue mode");
+  if (g->mode < EPI_BF16 || g->mode > EPI_BF16_SWIGLU) return mace_fail(ctx, MACE_ERR_ARG, "gemm: bad epilogue mode");
+  const bool swiglu = g->mode == EPI_BF16_SWIGLU;
+  if (swiglu && (g->a_mn_major || g->b_mn_major || g->bias || g->split_k > 1))
+    return mace_fail(ctx, MACE_ERR_UNSUPPORTED, "gemm: SwiGLU epilogue needs K-major operands, no bias, no split-K");
 
   // tile shape (tools/gemm_sweep.py on B200). Big GEMMs (>= one full wave of 256 x 256 pair tiles): the
   // CTA-pair kernel (MN-major operands: single-CTA BN 256). Otherwise a per-k-block cost model fitted on the
@@ -905,10 +986,14 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   const int kb_total = (g->K + kBK - 1) / kBK;
   const bool pair_ok = !g->a_mn_major && !g->b_mn_major && g->split_k <= 0 && g->mode != EPI_F32_ATOMIC &&
                        ((uintptr_t)g->out & 15) == 0 &&
-                       ((size_t)g->ldo * ((g->mode == EPI_BF16 || g->mode == EPI_BF16_GELU) ? 2 : 4)) % 16 == 0;
+                       ((size_t)g->ldo * ((g->mode == EPI_BF16 || g->mode == EPI_BF16_GELU || swiglu) ? 2 : 4)) % 16 == 0;
   const long sms = ctx->num_sms, pairs = ctx->num_sms / 2;
   int bn = 128, pair_bn = 0;
-  if (pair_ok && (long)num_m2 * ((g->N + 255) / 256) >= sms) {
+  if (swiglu) {  // 256-wide accumulator tiles = 128 gate + 128 up columns of the same 128 outputs
+    if (!pair_ok) return mace_fail(ctx, MACE_ERR_ARG, "gemm: SwiGLU output needs 16-byte aligned rows");
+    bn = 256;
+    if ((long)num_m2 * ((g->N + 127) / 128) >= sms) pair_bn = 256;
+  } else if (pair_ok && (long)num_m2 * ((g->N + 255) / 256) >= sms) {
     pair_bn = 256;
   } else if (!pair_ok && (long)num_m * ((g->N + 255) / 256) >= sms) {
     bn = 256;
@@ -930,7 +1015,7 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     }
   }
   int splits = g->split_k > 0 ? g->split_k : 1;
-  if (g->split_k <= 0 && kb_total >= 96 && (long)num_m * ((g->N + 127) / 128) < pairs) {
+  if (g->split_k <= 0 && !swiglu && kb_total >= 96 && (long)num_m * ((g->N + 127) / 128) < pairs) {
     // long K over few tiles (decode-sized down projections, FT dW): split K across the idle SMs (BN 128)
     bn = 128;
     pair_bn = 0;
@@ -941,7 +1026,7 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     if (splits < 1) splits = 1;
   }
   // tuning override (tools/gemm_sweep.py): MACE_GEMM_FORCE="<bn>,<splits>" | "pair,<bn>" | "single"
-  if (const char* f = getenv("MACE_GEMM_FORCE")) {
+  if (const char* f = getenv("MACE_GEMM_FORCE"); f && !swiglu) {
     int fb = 0, fs = 0;
     if (sscanf(f, "%d,%d", &fb, &fs) == 2) {
       if (fb == 64 || fb == 128 || fb == 192 || fb == 256) bn = fb;

@@ -95,7 +95,8 @@ static int gemm(ModelState& m, const MaceTickBuffers* b, cudaStream_t s, const v
   const int rc = mace_gemm_bf16(m.ctx, &g, s);
   if (ev) {
     cudaEventRecord((cudaEvent_t)t->gemm_events[2 * *t->gemm_count + 1], s);
-    t->gemm_flops[*t->gemm_count] = 2ll * M * N * K;
+    // the fused SwiGLU GEMM multiplies against both halves of the stacked [gate; up] weight
+    t->gemm_flops[*t->gemm_count] = 2ll * M * N * K * (mode == MACE_EPI_BF16_SWIGLU ? 2 : 1);
     ++*t->gemm_count;
   }
   return rc;
@@ -174,6 +175,8 @@ static int layer_fwd(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc
   MACE_TRY(mace_norm(m.ctx, io.x, D, nullptr, T, D, W.mlp_norm_w, W.mlp_norm_b, ln, d.norm_eps, io.h2, D, nullptr, s));
   if (ln && !io.keep_u) {  // GPT-2: GELU fused into the up-projection epilogue
     MACE_TRY(gemm(m, b, s, io.h2, D, false, W.up_w, D, false, T, d.ffn, D, io.a, d.ffn, MACE_EPI_BF16_GELU, W.up_b));
+  } else if (!ln && !io.keep_u) {  // Llama: SwiGLU fused (gate / up halves of one accumulator tile)
+    MACE_TRY(gemm(m, b, s, io.h2, D, false, W.up_w, D, false, T, d.ffn, D, io.a, d.ffn, MACE_EPI_BF16_SWIGLU, nullptr));
   } else {
     MACE_TRY(gemm(m, b, s, io.h2, D, false, W.up_w, D, false, T, d.up_dim, D, io.u, d.up_dim, MACE_EPI_BF16, W.up_b));
     MACE_TRY(mace_act(m.ctx, io.u, T, d.ffn, d.family == 0, io.a, s));

@@ -11,7 +11,7 @@ import torch
 
 from ._lib import Ctx, MaceGemmArgs
 
-EPI = {"bf16": 0, "f32": 1, "f32_add": 2, "f32_atomic": 3, "bf16_gelu": 4}
+EPI = {"bf16": 0, "f32": 1, "f32_add": 2, "f32_atomic": 3, "bf16_gelu": 4, "bf16_swiglu": 5}
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -55,11 +55,14 @@ def gemm(
     else:
         N, Kb = b.shape
     assert Kb == K, f"K mismatch {K} vs {Kb}"
+    if mode == "bf16_swiglu":  # b = [gate; up] stacked: 2N rows, N outputs
+        assert N % 2 == 0 and not b_mn
+        N //= 2
     if out is None:
-        assert mode in ("bf16", "f32", "bf16_gelu")
+        assert mode in ("bf16", "f32", "bf16_gelu", "bf16_swiglu")
         out = torch.empty(M, N, device=a.device, dtype=torch.float32 if mode == "f32" else torch.bfloat16)
     assert out.shape[0] >= M and out.shape[1] >= N and out.stride(1) == 1
-    assert out.dtype == (torch.bfloat16 if mode in ("bf16", "bf16_gelu") else torch.float32)
+    assert out.dtype == (torch.bfloat16 if mode in ("bf16", "bf16_gelu", "bf16_swiglu") else torch.float32)
     if bias is not None:
         assert bias.dtype == torch.bfloat16 and bias.numel() == N
     g = MaceGemmArgs(

@@ -108,3 +108,20 @@ def test_gemm_cta_pair(ctx, M, N, K, force, monkeypatch):
     monkeypatch.setenv("MACE_GEMM_FORCE", "single")
     out1 = ops.gemm(ctx, a, b, mode="f32")
     assert torch.equal(out, out1)
+
+
+@pytest.mark.parametrize("M,F,K", [(256, 8192, 2048), (300, 1024, 512), (4096, 14336, 512), (77, 2048, 256)])
+def test_gemm_swiglu(ctx, M, F, K):
+    """Fused SwiGLU epilogue (silu(x Wg^T) * (x Wu^T), W = [gate; up] stacked): single-CTA and CTA-pair tiles
+    against the fp32 reference."""
+    torch.manual_seed(M + F)
+    a = (torch.randn(M, K, device="cuda") * 0.5).bfloat16()
+    w = (torch.randn(2 * F, K, device="cuda") / K ** 0.5).bfloat16()
+    out = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(ctx, a, w, out, mode="bf16_swiglu")
+    torch.cuda.synchronize()
+    g = a.float() @ w[:F].float().t()
+    u = a.float() @ w[F:].float().t()
+    ref = torch.nn.functional.silu(g) * u
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item() + 1e-3, err
