@@ -18,6 +18,9 @@ namespace mace {
 
 // hd <= 64: 12 warps x 4-deep rings (C2 sweep on B200: 0.71 of HBM vs 0.68 for 16 x 3, 0.69 for 10 x 5,
 // 0.57 for 8 x 6); hd 128: 8 warps x 3 (the 4 KB pages fill the smem budget)
+#ifdef MACE_DEC_TRACE
+__device__ unsigned long long* g_dec_trace = nullptr;  // [item][4]: start ns, end ns, pages, smid
+#endif
 template <int HD, int G>
 struct Dec2 {
   static constexpr int WARPS = HD >= 128 ? 8 : 12;
@@ -68,6 +71,10 @@ __global__ void __launch_bounds__(Dec2<HD, G>::WARPS * 32) attn_decode2_kernel(
     const int4 it = items[item];
     const MaceSeq sq = seqs[it.x];
     const int h = it.y, chunk = it.z >> 16, nch = it.z & 0xffff;
+#ifdef MACE_DEC_TRACE
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     // ---- q of the G query heads of this kv group -> fp32 smem
     const __nv_bfloat16* qrow = qkv + (size_t)sq.q_start * W + (size_t)h * G * HD;
     for (int i = lane; i < G * HD; i += 32) qs[i] = __bfloat162float(qrow[i]);
@@ -233,6 +240,17 @@ __global__ void __launch_bounds__(Dec2<HD, G>::WARPS * 32) attn_decode2_kernel(
       }
     }
     ring_count = base_count + n_pg;
+#ifdef MACE_DEC_TRACE
+    if (g_dec_trace && lane == 0) {
+      unsigned long long t_end, smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      asm volatile("{ .reg .u32 s; mov.u32 s, %%smid; cvt.u64.u32 %0, s; }" : "=l"(smid));
+      g_dec_trace[item * 4 + 0] = t_start;
+      g_dec_trace[item * 4 + 1] = t_end;
+      g_dec_trace[item * 4 + 2] = n_pg;
+      g_dec_trace[item * 4 + 3] = smid * 64 + warp;
+    }
+#endif
 
     // ---- epilogue: direct write (one chunk) or chunk partial + deterministic merge by the last warp
     const int row = sq.q_start;
@@ -324,6 +342,10 @@ int launch_decode2(MaceCtx* ctx, const MaceAttnArgs* a, float scale_log2, cudaSt
   return 0;
 }
 
+#ifdef MACE_DEC_TRACE
+int dec_trace_set(void* buf) { return cudaMemcpyToSymbol(g_dec_trace, &buf, sizeof(buf)) == cudaSuccess ? 0 : -1; }
+#endif
+
 int dispatch_decode2(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStream_t s) {
   const int G = a->Hq / a->Hkv;
 #define MACE_D2(HD_)                                                  \
@@ -344,3 +366,7 @@ int dispatch_decode2(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStream_
 }
 
 }  // namespace mace
+
+#ifdef MACE_DEC_TRACE
+extern "C" int mace_debug_decode_trace(void* buf) { return mace::dec_trace_set(buf); }
+#endif
