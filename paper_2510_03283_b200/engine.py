@@ -39,7 +39,7 @@ ensure_macesim()
 import macesim.engine as _ref_engine  # noqa: E402
 from macesim.cache import dfs_order as _ref_dfs_order  # noqa: E402
 from macesim.scheduler import schedule_iteration as _ref_schedule_iteration  # noqa: E402
-from macesim.cost_model import CostProfile  # noqa: E402
+from macesim.cost_model import CostProfile, WorkloadEstimate  # noqa: E402
 from macesim.engine import Engine  # noqa: E402
 from macesim.workload import WorkloadType  # noqa: E402
 
@@ -501,16 +501,26 @@ class GpuEngine(Engine):
     def _synth_norms(self, req, rs):  # engine.py:433 — same draws, served from the per-request block stream
         return self.norm_stream.norms(req, rs).tolist()
 
-    def _estimate(self, req):  # engine.py:262 — decode estimates are constants (cost_model.py:101-102)
-        if req.workload is WorkloadType.DECODE:
+    def _estimate(self, req):  # engine.py:262 -> cost_model.get_workload (cost_model.py:92-106), same arithmetic
+        w = req.workload
+        if w is WorkloadType.DECODE:  # constants (cost_model.py:101-102)
             est = self._dec_est
             if est is None:
                 est = self._dec_est = super()._estimate(req)
             return est
+        if w is WorkloadType.PREFILL and self.fast_host and isinstance(self.trie, GpuPrefixTrie):
+            # cost_model.py:95-99 with the memoised cached-prefix walk of a queued prompt
+            shared = self.trie.cached_prefix_len_memo(req.id, req.prompt_tokens)
+            effective = max(0, len(req.prompt_tokens) - shared)
+            p = self.profile
+            return WorkloadEstimate(mem=(p.prefill_mem_per_token + p.decode_kv_mem_per_token) * effective,
+                                    lat=p.prefill_lat_per_token * effective)
         return super()._estimate(req)
 
     def _retire(self, req, t_end_ms, rejected=False):  # engine.py:538
         self.norm_stream.drop(req.id)
+        if isinstance(self.trie, GpuPrefixTrie):
+            self.trie.forget(req.id)
         super()._retire(req, t_end_ms, rejected)
         slot = self.slot_of.pop(req.id, None)
         table = self.table_of.pop(req.id, None)

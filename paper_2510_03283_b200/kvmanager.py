@@ -97,28 +97,61 @@ class GpuPrefixTrie(PrefixTrie):
         self.pool = pool
         self.node_pages: dict[int, dict[int, int]] = {}
         self.pending: dict[int, dict[int, int]] = {}   # pages a tick's prefill will hand to newly cached nodes
+        self._memo: dict[int, tuple] = {}  # request id -> (epoch, stop kind, a, b, cached prefix length)
+        self._epoch = 0                    # bumped by every split and every eviction
 
     def cached_prefix_len(self, prompt_tokens):  # cache.py:164-184, same walk; label matches compared by slices
+        return self._walk(prompt_tokens)[0]
+
+    def _walk(self, prompt_tokens):
+        """(shared, stop kind, a, b): how the walk ended -- 0 whole prompt cached, 1 no child for token b under
+        node a, 2 stopped at the uncached child a, 3 label mismatch inside a cached node."""
         node = self.root
         idx = 0
         shared = 0
         n = len(prompt_tokens)
         while idx < n:
-            child = node.children.get(prompt_tokens[idx])
-            if child is None or not child.cached:
-                break
+            tok = prompt_tokens[idx]
+            child = node.children.get(tok)
+            if child is None:
+                return shared, 1, node, tok
+            if not child.cached:
+                return shared, 2, child, None
             label = child.label
             limit = min(len(label), n - idx)
             match = _common_prefix(label, prompt_tokens, idx, limit)
             shared += match
             idx += match
             if match < len(label):
-                break
+                return shared, 3, None, None
             node = child
-        return shared
+        return shared, 0, None, None
+
+    def cached_prefix_len_memo(self, rid: int, prompt_tokens) -> int:
+        """cached_prefix_len of a queued request, re-walked only when its answer can have changed: a node became
+        cached where the last walk stopped (kind 1 / 2), or the trie was split or evicted since (any kind).
+        Inserts add uncached nodes and mark_executed only caches nodes, so nothing else moves the answer."""
+        m = self._memo.get(rid)
+        if m is not None and m[0] == self._epoch:
+            kind, a, b, val = m[1], m[2], m[3], m[4]
+            if kind == 0 or kind == 3:
+                return val
+            if kind == 1:
+                ch = a.children.get(b)
+                if ch is None or not ch.cached:
+                    return val
+            elif not a.cached:
+                return val
+        val, kind, a, b = self._walk(prompt_tokens)
+        self._memo[rid] = (self._epoch, kind, a, b, val)
+        return val
+
+    def forget(self, rid: int) -> None:
+        self._memo.pop(rid, None)
 
     # -- decisions stay the reference's; ownership follows
     def _split(self, node, at):
+        self._epoch += 1
         head = super()._split(node, at)
         pages = self.node_pages.get(node.node_id)
         if pages:
@@ -148,6 +181,8 @@ class GpuPrefixTrie(PrefixTrie):
 
     def lru_offload(self, bytes_needed, t):
         res = super().lru_offload(bytes_needed, t)
+        if res.evicted:
+            self._epoch += 1
         for n in res.evicted:
             for g in self.node_pages.pop(n.node_id, {}).values():
                 self.pool.decref(g)

@@ -301,3 +301,47 @@ def test_fast_schedule_iteration_matches_reference():
         assert (a.bin.used_memory, a.bin.max_latency, a.bin.n_inference, a.bin.n_ft) == \
             (b.bin.used_memory, b.bin.max_latency, b.bin.n_inference, b.bin.n_ft)
         assert len(queues[0]) == len(queues[1])
+
+
+def test_cached_prefix_memo_tracks_trie_changes():
+    """GpuPrefixTrie.cached_prefix_len_memo equals a fresh reference walk after every mix of inserts (with
+    splits), mark_executed and LRU evictions."""
+    import numpy as np
+
+    from paper_2510_03283_b200.kvmanager import GpuPrefixTrie, GroupPool
+
+    rng = np.random.default_rng(5)
+
+    class Tr(GpuPrefixTrie):  # page bookkeeping is not under test here
+        def mark_executed(self, leaf, t):
+            return super(GpuPrefixTrie, self).mark_executed(leaf, t)
+
+        def lru_offload(self, b, t):
+            res = super(GpuPrefixTrie, self).lru_offload(b, t)
+            if res.evicted:
+                self._epoch += 1
+            return res
+
+    tr = Tr(0.1, GroupPool(1))
+    prompts, leaves = {}, {}
+    base = [rng.integers(0, 4, 24).tolist() for _ in range(4)]
+    for step in range(1500):
+        op = rng.random()
+        if op < 0.35 or not prompts:
+            rid = len(prompts)
+            p = base[int(rng.integers(0, 4))][: int(rng.integers(1, 24))] + rng.integers(0, 4, int(rng.integers(1, 12))).tolist()
+            prompts[rid] = p
+            leaves[rid] = tr.insert(p, float(step)).leaf
+        elif op < 0.6:
+            rid = int(rng.integers(0, len(prompts)))
+            if leaves[rid] is not None:
+                tr.mark_executed(leaves[rid], float(step))
+        elif op < 0.7:
+            rid = int(rng.integers(0, len(prompts)))
+            if leaves[rid] is not None and all(n.ref_count > 0 for n in leaves[rid].path_nodes()):
+                tr.release(leaves[rid])
+                leaves[rid] = None
+        elif op < 0.75:
+            tr.lru_offload(float(rng.integers(1, 20)), float(step))
+        for rid in rng.integers(0, len(prompts), 4).tolist():
+            assert tr.cached_prefix_len_memo(rid, prompts[rid]) == tr._walk(prompts[rid])[0], (step, rid)
