@@ -103,8 +103,8 @@ class GpuEngine(Engine):
             raise ValueError("CacheConfig.num_heads must equal the model's KV heads (per-head KV windows)")
         if fast_host and self.queue is not None:  # vectorised re-keying, identical pop order (hostfast.py)
             self.queue = FastPriorityQueue(priority_params, loss_fn=self._loss_of)
-        self.norm_stream = NormStream(self)
         self.model = model
+        self.norm_stream = NormStream(self, model.max_slots)
         self.mcfg: ModelConfig = model.cfg
         self.mode = mode
         self.seed = engine_cfg.seed if seed is None else seed
@@ -480,7 +480,7 @@ class GpuEngine(Engine):
         if first.any():
             self.hstats.reset(slots[first])
         steps = np.fromiter((r.decode_pos + 1 for r in rows), np.int64, len(rows))
-        norms = np.stack([self.norm_stream.norms(r, self.state[r.id]) for r in rows])
+        norms = self.norm_stream.norms_many(rows, slots)
         kept, released = self.hstats.step(slots, steps, norms)
         kl = kept.tolist()
         rl = released.tolist()
@@ -492,7 +492,7 @@ class GpuEngine(Engine):
         if not (self.fast_host and _FAST_ALG1 and isinstance(self.queue, FastPriorityQueue)):
             return super()._plan()
         _ref_engine.schedule_iteration = lambda q, *a, _q=self.queue, **k: (
-            fast_schedule_iteration(q, *a, **k) if q is _q else _ref_schedule_iteration(q, *a, **k))
+            fast_schedule_iteration(q, *a, dec_est=self._dec_est, **k) if q is _q else _ref_schedule_iteration(q, *a, **k))
         try:
             return super()._plan()
         finally:

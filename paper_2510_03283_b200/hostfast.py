@@ -28,6 +28,7 @@ from macesim.scheduler import Bin, TickPlan  # noqa: E402
 from macesim.workload import WorkloadType  # noqa: E402
 
 _FT = WorkloadType.FINETUNE
+_DEC = WorkloadType.DECODE
 
 
 class FastPriorityQueue(PriorityQueue):
@@ -53,6 +54,8 @@ class FastPriorityQueue(PriorityQueue):
         # id -> (arrival, base, growth, is fine-tune, workload): a prefill turns into a decode in place
         # (workload.py:64-66), so an entry is only reused while the request's workload is unchanged
         self._meta: dict[int, tuple] = {}
+        self._pend: list[tuple] = []   # pushed keys not yet in the columns
+        self._pend_req: list = []
 
     def _meta_of(self, req) -> tuple:
         w = req.workload
@@ -108,31 +111,44 @@ class FastPriorityQueue(PriorityQueue):
             if loss < 0:
                 raise PriorityContractError("loss must be >= 0 under the positive-loss convention")
             p = p + self.params.gamma * loss
-        req.priority_state.value = p
-        req.priority_state.refreshed_at = t
-        key = (-p, arrival, req.id)
-        if self._n == self._neg.shape[0]:
-            if self._live < self._n // 2:
-                self._compact()
-            else:
-                self._grow()
-        k = self._n
-        self._n += 1
-        self._neg[k] = key[0]
-        self._arr[k] = arrival
-        self._bg[k, 0] = base
-        self._bg[k, 1] = growth
-        self._id[k] = req.id
-        self._ft[k] = is_ft
-        self._alive[k] = True
-        self._req[k] = req
+        ps = req.priority_state
+        ps.value = p
+        ps.refreshed_at = t
+        # keys land in the columns in bulk at the next refresh / pop / peek (_flush)
+        self._pend.append((-p, arrival, base, growth, req.id, is_ft))
+        self._pend_req.append(req)
         self._live += 1
         self._order = None
+
+    def _flush(self) -> None:
+        pend = self._pend
+        n_new = len(pend)
+        if not n_new:
+            return
+        while self._n + n_new > self._neg.shape[0]:
+            if self._live - n_new < self._n // 2:
+                self._compact()
+                if self._n + n_new <= self._neg.shape[0]:
+                    break
+            self._grow()
+        k0, k1 = self._n, self._n + n_new
+        cols = np.array(pend, np.float64)  # (-p, arrival, base, growth, id, is_ft): ids < 2^53 are exact
+        self._neg[k0:k1] = cols[:, 0]
+        self._arr[k0:k1] = cols[:, 1]
+        self._bg[k0:k1] = cols[:, 2:4]
+        self._id[k0:k1] = cols[:, 4].astype(np.int64)
+        self._ft[k0:k1] = cols[:, 5] != 0
+        self._alive[k0:k1] = True
+        self._req[k0:k1] = self._pend_req
+        self._n = k1
+        self._pend = []
+        self._pend_req = []
 
     def refresh(self, t: float) -> None:  # priority.py:121-127
         self._last_refresh = t
         if self._live == 0:
             return
+        self._flush()
         if self._live < self._n // 2:
             self._compact()
         n = self._n
@@ -164,6 +180,7 @@ class FastPriorityQueue(PriorityQueue):
         if self._live == 0:
             raise IndexError("pop from empty priority queue")
         if self._order is None:
+            self._flush()
             self._sort()
         while not self._alive[self._order[self._cur]]:
             self._cur += 1
@@ -181,42 +198,77 @@ class FastPriorityQueue(PriorityQueue):
         return req
 
     def peek(self):
-        return self._req[self._front()]
+        if self._order is not None or self._live == 0:
+            return self._req[self._front()]
+        # keys changed since the last sort (pushes): the smallest (-p, arrival, id) without sorting
+        self._flush()
+        idx = np.flatnonzero(self._alive[: self._n])
+        neg = self._neg[idx]
+        c = idx[neg == neg.min()]
+        if c.shape[0] > 1:
+            arr = self._arr[c]
+            c = c[arr == arr.min()]
+            if c.shape[0] > 1:
+                c = c[np.argmin(self._id[c]):][:1]
+        return self._req[int(c[0])]
 
 
 class NormStream:
-    """Per-request synthetic head-norm jitter in blocks (engine.py:433-442)."""
+    """Per-request synthetic head-norm jitter in blocks (engine.py:433-442), stored per KV slot so a tick's
+    decode rows are served by one gather; only rows whose block ran out draw from their Generator."""
 
     BLOCK = 64  # steps per draw
 
-    def __init__(self, engine):
+    def __init__(self, engine, n_slots: int):
         self.eng = engine
-        self.buf: dict[int, tuple[np.ndarray, int]] = {}
+        H = engine.cache_cfg.num_heads
+        self.blk = np.zeros((n_slots, self.BLOCK, H))
+        self.cur = np.zeros(n_slots, np.int64)
+        self.owner = np.full(n_slots, -1, np.int64)  # request id whose block the slot holds
 
-    def norms(self, req, rs) -> np.ndarray:
+    def _refill(self, req, rs, slot: int) -> None:
         eng = self.eng
         H = eng.cache_cfg.num_heads
         if rs.head_rng is None:
             rs.head_rng = np.random.default_rng([eng.ecfg.seed, 211, req.id])
             rs.head_scales = [eng.cache_cfg.weak_scale if h in eng.weak_heads else 1.0 for h in range(H)]
-        ent = self.buf.get(req.id)
-        if ent is None or ent[1] >= ent[0].shape[0]:
-            block = rs.head_rng.normal(1.0, 0.1, size=H * self.BLOCK).reshape(self.BLOCK, H)
-            ent = (np.maximum(0.0, np.asarray(rs.head_scales, np.float64) * block), 0)
-        row = ent[0][ent[1]]
-        self.buf[req.id] = (ent[0], ent[1] + 1)
-        return row
+        block = rs.head_rng.normal(1.0, 0.1, size=H * self.BLOCK).reshape(self.BLOCK, H)
+        self.blk[slot] = np.maximum(0.0, np.asarray(rs.head_scales, np.float64) * block)
+        self.cur[slot] = 0
+        self.owner[slot] = req.id
+
+    def norms(self, req, rs) -> np.ndarray:
+        slot = self.eng.slot_of[req.id]
+        if self.owner[slot] != req.id or self.cur[slot] >= self.BLOCK:
+            self._refill(req, rs, slot)
+        c = int(self.cur[slot])
+        self.cur[slot] = c + 1
+        return self.blk[slot, c].copy()
+
+    def norms_many(self, rows, slots: np.ndarray) -> np.ndarray:
+        """[n, H] norms of this step for decode rows ``rows`` in KV slots ``slots`` (distinct)."""
+        ids = np.fromiter((r.id for r in rows), np.int64, len(rows))
+        state = self.eng.state
+        for i in np.flatnonzero((self.owner[slots] != ids) | (self.cur[slots] >= self.BLOCK)).tolist():
+            r = rows[i]
+            self._refill(r, state[r.id], int(slots[i]))
+        c = self.cur[slots]
+        self.cur[slots] = c + 1
+        return self.blk[slots, c]
 
     def drop(self, rid: int) -> None:
-        self.buf.pop(rid, None)
+        slot = self.eng.slot_of.get(rid)
+        if slot is not None and self.owner[slot] == rid:
+            self.owner[slot] = -1
 
 
-def fast_schedule_iteration(queue, capacity_budget, cfg, estimator, t, hard_limit=None):
+def fast_schedule_iteration(queue, capacity_budget, cfg, estimator, t, hard_limit=None, dec_est=None):
     """Alg. 1 exactly as scheduler.py:133-188 (same dequeue stop rule, same best-fit score arithmetic
     lambda1*|free - mem| + lambda2*|maxlat - lat| with free = budget - used, same strict '<' tie rule,
     same requeue / defer / reject lists), with the Bin methods (scheduler.py:81-117) inlined into local
     arithmetic. Returns the reference TickPlan / Bin types; tests/test_host_cpu.py checks plan-for-plan
-    equality against the reference on randomized queues."""
+    equality against the reference on randomized queues. ``dec_est``: the estimator's (constant) decode
+    estimate (cost_model.py:100-102), used without the call when given."""
     if hard_limit is None:
         hard_limit = capacity_budget
     plan = TickPlan(bin=Bin(capacity_budget))
@@ -232,13 +284,15 @@ def fast_schedule_iteration(queue, capacity_budget, cfg, estimator, t, hard_limi
     rejected = plan.rejected
     examined = 0
     count = 0
+    pop = queue.pop
+    DEC = _DEC
     while queue:
         if bins and (bins[0][0] >= stop_mem or count >= tau_task):
             break
-        task = queue.pop()
+        task = pop()
         count += 1
         dequeued.append(task)
-        est = estimator(task)
+        est = dec_est if (dec_est is not None and task.workload is DEC) else estimator(task)
         mem, lat = est.mem, est.lat
         if mem > hard_limit:
             rejected.append(task)
