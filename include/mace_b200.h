@@ -51,6 +51,9 @@ int mace_ctx_destroy(mace_ctx* ctx);
 const char* mace_last_error(mace_ctx* ctx);
 /* number of kernels this ctx has launched (evidence for the bench's gpu_launches) */
 long long mace_launch_count(mace_ctx* ctx);
+/* host issue profile, process-wide, enabled by MACE_HOST_PROF=1 at load: out[4] = seconds in kernel launches,
+ * launches, seconds in tensor-map encodes, encodes, since the previous call (then reset); -1 when disabled */
+int mace_debug_host_prof(double* out4);
 
 /* ---------------------------------------------------------------- (2) bf16 tcgen05 GEMM
  * C[M,N] = alpha * A[M,K] . B[N,K]^T (+bias[N]).  A is stored K-major ([M, lda]) or, with

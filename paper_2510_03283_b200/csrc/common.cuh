@@ -1,6 +1,7 @@
 // Shared sm_100a device helpers: mbarrier, TMA (cp.async.bulk[.tensor]), tcgen05 / TMEM.
 // Everything here is raw PTX so the SASS is auditable (UTCHMMA / UTMALDG / LDTM / UBLKCP).
 #pragma once
+#include <chrono>
 #include <cstdlib>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -402,6 +403,17 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// host-side issue profile (MACE_HOST_PROF=1; tools/issue_profile.py): time spent in launches / map encodes
+struct HostProf {
+  double launch_s = 0, encode_s = 0;
+  long long n_launch = 0, n_encode = 0;
+};
+extern HostProf g_host_prof;
+inline bool host_prof_on() {
+  static const bool on = getenv("MACE_HOST_PROF") != nullptr;
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                             Args&&... args) {
@@ -415,7 +427,12 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (!host_prof_on()) return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  const auto t0 = std::chrono::steady_clock::now();
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  g_host_prof.launch_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  g_host_prof.n_launch++;
+  return e;
 }
 
 }  // namespace mace
