@@ -16,77 +16,111 @@ namespace mace {
 // rows i < n: x = xbuf[xrows ? xrows[i] : i], dy = dy[i]; dx written to dx[dxrows ? dxrows[i] : i] (+=).
 // Per-block partials of dw (and db) go to part[blockIdx.x][0..d) and part[blockIdx.x][d..2d).
 template <int kPerLane>
-__global__ void norm_bwd_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ xrows,
-                                const float* __restrict__ dy, int lddy, int n, int d, const __nv_bfloat16* __restrict__ w,
-                                int layernorm, float eps, float* __restrict__ dx, int lddx, const int* __restrict__ dxrows,
-                                float* __restrict__ part, int rows_per_block) {
+__global__ void __launch_bounds__(256, kPerLane <= 32 ? 2 : 1)
+    norm_bwd_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ xrows, const float* __restrict__ dy,
+                    int lddy, int n, int d, const __nv_bfloat16* __restrict__ w, int layernorm, float eps,
+                    float* __restrict__ dx, int lddx, const int* __restrict__ dxrows, float* __restrict__ part) {
+  // one row per warp, 8 rows per CTA, float4 columns (lane owns columns 4 * (32 k + lane) .. + 3); the CTA's
+  // dW / dB partials are merged in smem in warp order (deterministic) and reduced across CTAs by
+  // col_reduce_kernel. No per-warp accumulator arrays: <= 128 registers at d 768, two CTAs per SM.
+  constexpr int KV = kPerLane / 4;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
+  const int i = blockIdx.x * nw + warp;
+  const bool active = i < n;
+  // the norm weights do not depend on the previous kernel: fetched before the PDL wait (small d only;
+  // at d 4096 the row alone fills the register file)
+  constexpr bool kPre = KV <= 16;
+  uint2 wraw[kPre ? KV : 1];
+#pragma unroll
+  for (int k = 0; k < (kPre ? KV : 0); ++k) {
+    const int c = (k * 32 + lane) * 4;
+    wraw[k] = active && c < d ? *reinterpret_cast<const uint2*>(w + c) : make_uint2(0u, 0u);
+  }
   pdl_wait();
   pdl_trigger();
   extern __shared__ float sh[];  // [2][d] block partials
   for (int c = threadIdx.x; c < 2 * d; c += blockDim.x) sh[c] = 0.f;
-  __syncthreads();
-  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
-  const int r_begin = blockIdx.x * rows_per_block, r_end = min(n, r_begin + rows_per_block);
-  float dwa[kPerLane], dba[kPerLane];  // per-warp partials, merged in fixed warp order (deterministic)
-#pragma unroll
-  for (int k = 0; k < kPerLane; ++k) dwa[k] = dba[k] = 0.f;
-  for (int i = r_begin + warp; i < r_end; i += nw) {
+  float4 xv[KV], gv[KV];
+  float rstd = 0.f;
+  if (active) {
     const float* xr = x + (size_t)(xrows ? xrows[i] : i) * ldx;
     const float* gr = dy + (size_t)i * lddy;
-    float xv[kPerLane], gv[kPerLane];
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < kPerLane; ++k) {
-      const int c = k * 32 + lane;
-      xv[k] = c < d ? xr[c] : 0.f;
-      gv[k] = c < d ? gr[c] : 0.f;
-      s += xv[k];
+    for (int k = 0; k < KV; ++k) {
+      const int c = (k * 32 + lane) * 4;
+      xv[k] = c < d ? *reinterpret_cast<const float4*>(xr + c) : z;
+      gv[k] = c < d ? *reinterpret_cast<const float4*>(gr + c) : z;
+      s += (xv[k].x + xv[k].y) + (xv[k].z + xv[k].w);
     }
     const float mean = layernorm ? warp_sum(s) / d : 0.f;
     float ss = 0.f;
 #pragma unroll
-    for (int k = 0; k < kPerLane; ++k) {
-      const int c = k * 32 + lane;
+    for (int k = 0; k < KV; ++k) {
+      const int c = (k * 32 + lane) * 4;
       if (c < d) {
-        xv[k] -= mean;
-        ss += xv[k] * xv[k];
+        xv[k].x -= mean; xv[k].y -= mean; xv[k].z -= mean; xv[k].w -= mean;
+        ss += (xv[k].x * xv[k].x + xv[k].y * xv[k].y) + (xv[k].z * xv[k].z + xv[k].w * xv[k].w);
       }
     }
-    const float rstd = rsqrtf(warp_sum(ss) / d + eps);
+    rstd = rsqrtf(warp_sum(ss) / d + eps);
+    auto gw_of = [&](int k, int c) {  // g * w of the lane's 4 columns
+      const uint2 raw = kPre ? wraw[kPre ? k : 0] : *reinterpret_cast<const uint2*>(w + c);
+      const float2 w01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+      const float2 w23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+      return make_float4(gv[k].x * w01.x, gv[k].y * w01.y, gv[k].z * w23.x, gv[k].w * w23.y);
+    };
     float sum_g = 0.f, sum_gx = 0.f;
 #pragma unroll
-    for (int k = 0; k < kPerLane; ++k) {
-      const int c = k * 32 + lane;
+    for (int k = 0; k < KV; ++k) {
+      const int c = (k * 32 + lane) * 4;
       if (c < d) {
-        const float gw = gv[k] * __bfloat162float(w[c]);
-        sum_g += gw;
-        sum_gx += gw * xv[k] * rstd;
+        const float4 gw = gw_of(k, c);
+        sum_g += (gw.x + gw.y) + (gw.z + gw.w);
+        sum_gx += (gw.x * xv[k].x * rstd + gw.y * xv[k].y * rstd) + (gw.z * xv[k].z * rstd + gw.w * xv[k].w * rstd);
       }
     }
     sum_g = warp_sum(sum_g) / d;
     sum_gx = warp_sum(sum_gx) / d;
     float* dr = dx + (size_t)(dxrows ? dxrows[i] : i) * lddx;
 #pragma unroll
-    for (int k = 0; k < kPerLane; ++k) {
-      const int c = k * 32 + lane;
+    for (int k = 0; k < KV; ++k) {
+      const int c = (k * 32 + lane) * 4;
       if (c < d) {
-        const float xh = xv[k] * rstd;
-        const float gw = gv[k] * __bfloat162float(w[c]);
-        const float g = layernorm ? rstd * (gw - sum_g - xh * sum_gx) : rstd * (gw - xh * sum_gx);
-        dr[c] += g;
-        dwa[k] += gv[k] * xh;
-        dba[k] += gv[k];
+        const float4 gw = gw_of(k, c);
+        float4 o = *reinterpret_cast<float4*>(dr + c);
+        const float h0 = xv[k].x * rstd, h1 = xv[k].y * rstd, h2 = xv[k].z * rstd, h3 = xv[k].w * rstd;
+        if (layernorm) {
+          o.x += rstd * (gw.x - sum_g - h0 * sum_gx);
+          o.y += rstd * (gw.y - sum_g - h1 * sum_gx);
+          o.z += rstd * (gw.z - sum_g - h2 * sum_gx);
+          o.w += rstd * (gw.w - sum_g - h3 * sum_gx);
+        } else {
+          o.x += rstd * (gw.x - h0 * sum_gx);
+          o.y += rstd * (gw.y - h1 * sum_gx);
+          o.z += rstd * (gw.z - h2 * sum_gx);
+          o.w += rstd * (gw.w - h3 * sum_gx);
+        }
+        *reinterpret_cast<float4*>(dr + c) = o;
       }
     }
   }
-  for (int wv = 0; wv < nw; ++wv) {
-    if (warp == wv) {
+  __syncthreads();
+  for (int wq = 0; wq < nw; ++wq) {
+    if (warp == wq && active) {
 #pragma unroll
-      for (int k = 0; k < kPerLane; ++k) {
-        const int c = k * 32 + lane;
+      for (int k = 0; k < KV; ++k) {
+        const int c = (k * 32 + lane) * 4;
         if (c < d) {
-          sh[c] += dwa[k];
-          sh[d + c] += dba[k];
+          sh[c] += gv[k].x * (xv[k].x * rstd);
+          sh[c + 1] += gv[k].y * (xv[k].y * rstd);
+          sh[c + 2] += gv[k].z * (xv[k].z * rstd);
+          sh[c + 3] += gv[k].w * (xv[k].w * rstd);
+          sh[d + c] += gv[k].x;
+          sh[d + c + 1] += gv[k].y;
+          sh[d + c + 2] += gv[k].z;
+          sh[d + c + 3] += gv[k].w;
         }
       }
     }
@@ -378,10 +412,11 @@ extern "C" int mace_norm_bwd(mace_ctx* ctx, const float* x, int ldx, const int* 
   const int rows_per_block = 8;  // one row per warp: n/8 CTAs keep every SM busy
   const int nb = (n + rows_per_block - 1) / rows_per_block;
   if (workspace_bytes < (size_t)nb * 2 * d * 4) return mace_fail(ctx, MACE_ERR_ARG, "norm_bwd: workspace too small");
-  const int per_lane = (d + 31) / 32;
+  if ((d | ldx | lddy | lddx) & 3) return mace_fail(ctx, MACE_ERR_ARG, "norm_bwd: d and leading dims must be multiples of 4");
+  const int per_lane = (d + 127) / 128 * 4;  // float4 columns per lane, times 4
   const size_t sh = 2 * d * sizeof(float);
   auto* W = (const __nv_bfloat16*)w;
-#define MACE_NB(K) launch_k(norm_bwd_kernel<K>, nb, 256, sh, s, x, ldx, xrows, dy, lddy, n, d, W, layernorm, eps, dx, lddx, dxrows, workspace, rows_per_block)
+#define MACE_NB(K) launch_k(norm_bwd_kernel<K>, nb, 256, sh, s, x, ldx, xrows, dy, lddy, n, d, W, layernorm, eps, dx, lddx, dxrows, workspace)
   if (per_lane <= 8) MACE_NB(8);
   else if (per_lane <= 24) MACE_NB(24);
   else if (per_lane <= 64) MACE_NB(64);

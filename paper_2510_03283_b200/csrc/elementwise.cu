@@ -50,11 +50,25 @@ template <int kPerLane>
 __global__ void norm_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ rows, int n_rows, int d,
                             const __nv_bfloat16* __restrict__ w, const __nv_bfloat16* __restrict__ b, int layernorm,
                             float eps, __nv_bfloat16* __restrict__ out, int ldo, float* __restrict__ rstd_out) {
+  const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  // the weights do not depend on the previous kernel: fetched before the PDL wait, under its tail
+  // (up to d 2048; at d 4096 they are read after the statistics, keeping the row in registers)
+  constexpr int KV = kPerLane / 4;
+  constexpr bool kPre = KV <= 16;
+  uint2 wr[KV], br[KV];
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    wr[k] = br[k] = make_uint2(0u, 0u);
+    if (kPre && c < d && i < n_rows) {
+      wr[k] = *reinterpret_cast<const uint2*>(w + c);
+      if (layernorm) br[k] = *reinterpret_cast<const uint2*>(b + c);
+    }
+  }
   pdl_wait();
   pdl_trigger();
-  const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (i >= n_rows) return;
-  const int lane = threadIdx.x & 31;
   const int src = rows ? rows[i] : i;
   const float* xr = x + (size_t)src * ldx;
   float v[kPerLane];
@@ -89,11 +103,17 @@ __global__ void norm_kernel(const float* __restrict__ x, int ldx, const int* __r
   for (int k = 0; k < kPerLane / 4; ++k) {
     const int c = (k * 32 + lane) * 4;
     if (c < d) {
+      if (!kPre) {
+        wr[k] = *reinterpret_cast<const uint2*>(w + c);
+        if (layernorm) br[k] = *reinterpret_cast<const uint2*>(b + c);
+      }
+      const __nv_bfloat16* wk = reinterpret_cast<const __nv_bfloat16*>(&wr[k]);
+      const __nv_bfloat16* bk = reinterpret_cast<const __nv_bfloat16*>(&br[k]);
       float y[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        y[j] = (v[4 * k + j] - mean) * rstd * __bfloat162float(w[c + j]);
-        if (layernorm) y[j] += __bfloat162float(b[c + j]);
+        y[j] = (v[4 * k + j] - mean) * rstd * __bfloat162float(wk[j]);
+        if (layernorm) y[j] += __bfloat162float(bk[j]);
       }
       uint2 pk = make_uint2(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]));
       *reinterpret_cast<uint2*>(o + c) = pk;
