@@ -161,7 +161,9 @@ class GpuEngine(Engine):
         Hq, Hkv = c.n_heads, c.n_kv_heads
         i32 = np.int32
         tok_seg, pos_seg, seq_seg, kvi_seg = [], [], [], []
-        seqs: list[tuple] = []
+        seqs: list[tuple] = []  # sequence rows not yet in seq_blocks
+        seq_blocks: list[np.ndarray] = []
+        n_seq = 0  # sequences before `seqs`
         tc_seg = []
         ptab_slots, ptab_rows, copies = [], [], []
         n_rows = 0
@@ -200,7 +202,7 @@ class GpuEngine(Engine):
             q = P - start
             if q <= 0:
                 continue
-            si = len(seqs)
+            si = n_seq + len(seqs)
             seqs.append((KIND_PREFILL, n_rows, q, slot, P, P, -1, 0))
             tc_seg.append(tc_block(si, q, P))
             tok_seg.append(np.asarray(req.prompt_tokens[start:], i32))
@@ -217,11 +219,10 @@ class GpuEngine(Engine):
         dec_rows = np.zeros(0, i32)
         if n_dec:
             slot_of = self.slot_of
-            P = np.fromiter((len(r.prompt_tokens) for r in decodes), i32, n_dec)
-            k0 = np.fromiter((r.decode_pos for r in decodes), i32, n_dec)
-            dec_slots = np.fromiter((slot_of[r.id] for r in decodes), i32, n_dec)
-            last = np.fromiter((r.prompt_tokens[-1] for r in decodes), i32, n_dec)
-            si0 = len(seqs)
+            info = np.array([(len(pt), r.decode_pos, slot_of[r.id], pt[-1])
+                             for r in decodes for pt in (r.prompt_tokens,)], i32).reshape(n_dec, 4)
+            P, k0, dec_slots, last = info[:, 0], info[:, 1], info[:, 2], info[:, 3]
+            si0 = n_seq + len(seqs)
             dec_rows = np.arange(n_rows, n_rows + n_dec, dtype=i32)
             sarr = np.zeros((n_dec, 8), i32)
             sarr[:, 0] = KIND_DECODE
@@ -230,7 +231,10 @@ class GpuEngine(Engine):
             sarr[:, 3] = dec_slots
             sarr[:, 4] = P - 1
             sarr[:, 6] = np.arange(n_dec, dtype=i32)
-            seqs.extend(map(tuple, sarr.tolist()))
+            seq_blocks.append(np.asarray(seqs, i32).reshape(-1, 8))  # rows so far, then the decode block
+            seq_blocks.append(sarr)
+            seqs = []
+            n_seq = si0 + n_dec
             tok_seg.append(np.where(k0 == 0, last, -(dec_slots + 1)).astype(i32))
             pos_seg.append((P - 1 + k0).astype(i32))
             seq_seg.append(np.arange(si0, si0 + n_dec, dtype=i32))
@@ -242,7 +246,8 @@ class GpuEngine(Engine):
             per = -(-npp // nch)
             n_it = nch * Hkv
             seq_i = np.repeat(np.arange(si0, si0 + n_dec, dtype=i32), n_it)
-            within = np.concatenate([np.arange(k, dtype=i32) for k in n_it]) if n_dec else np.zeros(0, i32)
+            total_it = int(n_it.sum())
+            within = (np.arange(total_it, dtype=i32) - np.repeat(np.cumsum(n_it) - n_it, n_it)).astype(i32)
             nch_r = np.repeat(nch, n_it)
             per_r = np.repeat(per, n_it)
             npp_r = np.repeat(npp, n_it)
@@ -275,7 +280,7 @@ class GpuEngine(Engine):
             pr = []
             for side, resp in enumerate((chs, rjs)):
                 n = P + len(resp)
-                si = len(seqs)
+                si = n_seq + len(seqs)
                 q0 = n_rows
                 seqs.append((KIND_FT, q0, n, -1, 0, n, -1, 0))
                 tc_seg.append(tc_block(si, n, n))
@@ -328,7 +333,7 @@ class GpuEngine(Engine):
         tc_all = np.concatenate([lpt(tc_all[:n_tc_inference]), lpt(tc_all[n_tc_inference:])])
         return TickBatch(
             tokens=tokens, pos=cat(pos_seg), row_seq=cat(seq_seg), row_kvi=cat(kvi_seg),
-            seqs=arr(seqs, 8), tc_items=tc_all, dec_items=dec_items,
+            seqs=np.concatenate(seq_blocks + [arr(seqs, 8)]) if seq_blocks else arr(seqs, 8), tc_items=tc_all, dec_items=dec_items,
             dec_slots=dec_slots.astype(i32), dec_rows=dec_rows, ptab_slots=np.asarray(ptab_slots, i32), ptab_rows=pt,
             page_copies=arr(copies, 4), ft0=ft0, ft_pairs=pairs, ft_logit_rows=cat(lr_seg),
             ft_targets=cat(tg_seg), pair_rows=arr(pair_rows, 4), row_ps=cat(ps_seg),
