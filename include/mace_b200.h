@@ -269,6 +269,19 @@ int mace_model_create(mace_ctx* ctx, const MaceModelDesc* desc, mace_model** out
 int mace_model_destroy(mace_model* model);
 int mace_tick_run(mace_model* model, const MaceTickBuffers* bufs, const MaceTickDesc* tick, void* stream);
 
+/* ---------------------------------------------------------------- host bookkeeping (CPU, no GPU needed)
+ * One tick's per-decode-row head statistics, capacity allocation and prune trims
+ * (replaces the per-row Python of Engine._exec_decode, engine.py:496-529 -> HeadStats.update cache.py:291-309,
+ * allocate_capacity cache.py:318-352, prune_decision cache.py:355-362), over per-slot state arrays:
+ * ring [slots, H, W], count / pos [slots], sums / current / last_used / kept [slots, H], tau [slots] (NaN =
+ * unset). Rows: slots[n] (distinct), steps[n] (decode position + 1), norms [n, H]. Writes kept_out [n, H] and
+ * released_out [n]. Returns 0, or 1 without touching the state when a row hits allocate_capacity's rounding
+ * corner (leftover >= H) that the caller resolves with the reference function. */
+int mace_host_head_stats(int n, int H, int W, const int64_t* slots, const int64_t* steps, const double* norms,
+                         double* ring, int64_t* count, int64_t* pos, double* sums, double* current,
+                         double* last_used, double* tau, int64_t* kept, int c_total, double prune_window,
+                         int64_t* kept_out, int64_t* released_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,7 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "--expt-relaxed-constexpr",
-    "-Xcompiler", "-fPIC,-O3",
+    "-Xcompiler", "-fPIC,-O3,-ffp-contract=off",  # host bookkeeping (hoststats.cu) must not fuse mul+add
     "-Xptxas", "-warn-spills",
 ]
 

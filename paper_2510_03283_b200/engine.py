@@ -480,18 +480,16 @@ class GpuEngine(Engine):
         out: dict = {}
         if not rows:
             return out
-        slots = np.fromiter((self.slot_of[r.id] for r in rows), np.int64, len(rows))
-        first = np.fromiter((r.decode_pos == 0 for r in rows), bool, len(rows))
+        slot_of = self.slot_of
+        info = np.array([(slot_of[r.id], r.decode_pos) for r in rows], np.int64).reshape(len(rows), 2)
+        slots = np.ascontiguousarray(info[:, 0])
+        first = info[:, 1] == 0
         if first.any():
             self.hstats.reset(slots[first])
-        steps = np.fromiter((r.decode_pos + 1 for r in rows), np.int64, len(rows))
+        steps = info[:, 1] + 1
         norms = self.norm_stream.norms_many(rows, slots)
         kept, released = self.hstats.step(slots, steps, norms)
-        kl = kept.tolist()
-        rl = released.tolist()
-        for i, r in enumerate(rows):
-            out[r.id] = (kl[i], rl[i])
-        return out
+        return dict(zip([r.id for r in rows], zip(kept.tolist(), released.tolist())))
 
     def _plan(self):  # engine.py:393 — the reference _plan with Alg. 1's inlined restatement (hostfast.py)
         if not (self.fast_host and _FAST_ALG1 and isinstance(self.queue, FastPriorityQueue)):

@@ -22,6 +22,11 @@ ensure_macesim()
 from macesim.cache import allocate_capacity  # noqa: E402
 
 
+def _native():
+    from ._lib import lib
+    return lib()
+
+
 class BatchedHeadStats:
     def __init__(self, n_slots: int, n_heads: int, window: int, c_total: int, prune_window: float,
                  norm_tau: float | None):
@@ -50,7 +55,28 @@ class BatchedHeadStats:
 
     def step(self, slots: np.ndarray, steps: np.ndarray, norms: np.ndarray):
         """One decode step for rows ``slots`` (distinct) at decode positions ``steps`` with per-head
-        norms [n, H]. Returns (kept [n, H] after trims, released [n]) exactly as the reference."""
+        norms [n, H]. Returns (kept [n, H] after trims, released [n]) exactly as the reference. Runs the
+        native restatement (csrc/hoststats.cu, mace_host_head_stats); the numpy one below handles the
+        allocate_capacity rounding corner and is the test oracle for the native one."""
+        n = slots.shape[0]
+        slots = np.ascontiguousarray(slots, np.int64)
+        steps = np.ascontiguousarray(steps, np.int64)
+        norms = np.ascontiguousarray(norms, np.float64)
+        kept = np.empty((n, self.H), np.int64)
+        released = np.empty(n, np.int64)
+        p = lambda a: a.ctypes.data  # noqa: E731
+        rc = _native().mace_host_head_stats(
+            n, self.H, self.W, p(slots), p(steps), p(norms), p(self.ring), p(self.count), p(self.pos), p(self.sums),
+            p(self.current), p(self.last_used), p(self.tau), p(self.kept), self.c_total, float(self.prune_window),
+            p(kept), p(released))
+        if rc == 1:
+            return self.step_numpy(slots, steps, norms)
+        if rc != 0:
+            raise RuntimeError(f"mace_host_head_stats failed ({rc})")
+        return kept, released
+
+    def step_numpy(self, slots: np.ndarray, steps: np.ndarray, norms: np.ndarray):
+        """numpy restatement (same arithmetic as the native routine)."""
         H, W = self.H, self.W
         n = slots.shape[0]
         # ---- HeadStats.update (cache.py:291-309)

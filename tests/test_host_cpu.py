@@ -345,3 +345,36 @@ def test_cached_prefix_memo_tracks_trie_changes():
             tr.lru_offload(float(rng.integers(1, 20)), float(step))
         for rid in rng.integers(0, len(prompts), 4).tolist():
             assert tr.cached_prefix_len_memo(rid, prompts[rid]) == tr._walk(prompts[rid])[0], (step, rid)
+
+
+def test_native_head_stats_matches_numpy():
+    """csrc/hoststats.cu (the product path) equals the numpy restatement bit for bit over many steps:
+    first steps (tau unset), full windows, weak heads driving zero-cap repairs, resets, and the uniform split."""
+    import numpy as np
+
+    from paper_2510_03283_b200.hoststats import BatchedHeadStats
+
+    rng = np.random.default_rng(11)
+    H, W, S = 8, 64, 96
+    a = BatchedHeadStats(S, H, W, 160, 128.0, None)
+    b = BatchedHeadStats(S, H, W, 160, 128.0, None)
+    step_of = np.zeros(S, np.int64)
+    for it in range(400):
+        n = int(rng.integers(1, 60))
+        slots = rng.choice(S, n, replace=False).astype(np.int64)
+        reset = slots[rng.random(n) < 0.03]
+        if reset.size:
+            a.reset(reset)
+            b.reset(reset)
+            step_of[reset] = 0
+        step_of[slots] += 1
+        scale = np.where(rng.random((n, H)) < 0.25, 0.05, 1.0)
+        norms = np.maximum(0.0, scale * rng.normal(1.0, 0.1, (n, H)))
+        if it % 50 == 7:
+            norms[:3] = 0.0  # total <= 0: uniform split
+        ka, ra = a.step(slots, step_of[slots], norms)
+        kb, rb = b.step_numpy(slots, step_of[slots], norms)
+        assert np.array_equal(ka, kb) and np.array_equal(ra, rb)
+    for name in ("ring", "count", "pos", "sums", "current", "last_used", "kept"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name
+    assert np.array_equal(np.isnan(a.tau), np.isnan(b.tau)) and np.array_equal(np.nan_to_num(a.tau), np.nan_to_num(b.tau))
