@@ -29,7 +29,7 @@ import torch
 
 from .batch import KIND_DECODE, KIND_FT, KIND_PREFILL, PAGE, FtPair, TickBatch
 from .config import ModelConfig, TrainConfig
-from .hostfast import FastPriorityQueue, NormStream, fast_schedule_iteration
+from .hostfast import FastPriorityQueue, NormStream, fast_schedule_iteration, make_bulk_pair_losses
 from .hoststats import BatchedHeadStats
 from .kvmanager import GpuPrefixTrie, GroupPool, plan_prefill_pages
 from .model import HybridModel
@@ -103,6 +103,8 @@ class GpuEngine(Engine):
             raise ValueError("CacheConfig.num_heads must equal the model's KV heads (per-head KV windows)")
         if fast_host and self.queue is not None:  # vectorised re-keying, identical pop order (hostfast.py)
             self.queue = FastPriorityQueue(priority_params, loss_fn=self._loss_of)
+            if type(self)._loss_of is Engine._loss_of:  # the reference's loss chain, restated in bulk
+                self.queue.bulk_loss = make_bulk_pair_losses(self.env)
         self.model = model
         self.norm_stream = NormStream(self, model.max_slots)
         self.mcfg: ModelConfig = model.cfg

@@ -54,6 +54,7 @@ class FastPriorityQueue(PriorityQueue):
         # id -> (arrival, base, growth, is fine-tune, workload): a prefill turns into a decode in place
         # (workload.py:64-66), so an entry is only reused while the request's workload is unchanged
         self._meta: dict[int, tuple] = {}
+        self.bulk_loss = None          # optional many-request loss_fn (make_bulk_pair_losses)
         self._pend: list[tuple] = []   # pushed keys not yet in the columns
         self._pend_req: list = []
 
@@ -107,7 +108,7 @@ class FastPriorityQueue(PriorityQueue):
                 f"priority query at t={t} before arrival of request {req.id} at {arrival}")
         p = base + growth * (t - arrival)  # dynamic_priority (priority.py:73)
         if is_ft and self.loss_fn is not None:  # ft_total_priority (priority.py:76-81)
-            loss = self.loss_fn(req)
+            loss = self.loss_fn(req) if self.bulk_loss is None else self.bulk_loss((req,))[0]
             if loss < 0:
                 raise PriorityContractError("loss must be >= 0 under the positive-loss convention")
             p = p + self.params.gamma * loss
@@ -161,8 +162,11 @@ class FastPriorityQueue(PriorityQueue):
         p = self._bg[:n, 0] + self._bg[:n, 1] * (t - arr)  # dynamic_priority (priority.py:73), no FMA
         if self.loss_fn is not None:
             gamma = self.params.gamma
-            for k in np.flatnonzero(self._ft[:n] & alive).tolist():  # ft_total_priority (priority.py:76-81)
-                loss = self.loss_fn(self._req[k])
+            ks = np.flatnonzero(self._ft[:n] & alive).tolist()
+            reqs = self._req
+            losses = (self.bulk_loss([reqs[k] for k in ks]) if self.bulk_loss is not None
+                      else [self.loss_fn(reqs[k]) for k in ks])
+            for k, loss in zip(ks, losses):  # ft_total_priority (priority.py:76-81)
                 if loss < 0:
                     raise PriorityContractError("loss must be >= 0 under the positive-loss convention")
                 p[k] = p[k] + gamma * loss
@@ -211,6 +215,40 @@ class FastPriorityQueue(PriorityQueue):
             if c.shape[0] > 1:
                 c = c[np.argmin(self._id[c]):][:1]
         return self._req[int(c[0])]
+
+
+def make_bulk_pair_losses(env):
+    """pair_loss for many fine-tune requests at once, value-for-value equal to the reference chain
+    Engine._loss_of -> AlignmentEnv.pair_loss -> pair_margin -> dpo_loss (alignment.py:39-47, 151-166): the
+    per-request offset initial_margin - (mu0 - drift_rate * arrival) is computed once with the reference's
+    arithmetic, margin = mu + offset, MarginSample(margin, 0).margin = margin - 0.0, then the same math.exp /
+    math.log1p branch. None when env's methods are not the reference's (a subclass may override them)."""
+    import math
+
+    from macesim.alignment import AlignmentEnv
+
+    if type(env).pair_loss is not AlignmentEnv.pair_loss or type(env).pair_margin is not AlignmentEnv.pair_margin:
+        return None
+    offs: dict[int, float] = {}
+    exp, log1p = math.exp, math.log1p
+    tenants = env.tenants
+
+    def losses(reqs) -> list[float]:
+        beta = env.beta
+        if beta <= 0:  # dpo_loss raises AlignmentDomainError: let the reference say so
+            return [env.pair_loss(r) for r in reqs]
+        out = []
+        for r in reqs:
+            o = offs.get(r.id)
+            if o is None:
+                env.pair_margin(r)  # the reference's own argument checks (workload / pair / tenant)
+                prm = tenants[r.tenant].params
+                o = offs[r.id] = r.pair.initial_margin - (prm.mu0 - prm.drift_rate * r.arrival_time)
+            x = -beta * ((tenants[r.tenant].mu + o) - 0.0)
+            out.append(x + log1p(exp(-x)) if x > 0 else log1p(exp(x)))
+        return out
+
+    return losses
 
 
 class NormStream:

@@ -378,3 +378,27 @@ def test_native_head_stats_matches_numpy():
     for name in ("ring", "count", "pos", "sums", "current", "last_used", "kept"):
         assert np.array_equal(getattr(a, name), getattr(b, name)), name
     assert np.array_equal(np.isnan(a.tau), np.isnan(b.tau)) and np.array_equal(np.nan_to_num(a.tau), np.nan_to_num(b.tau))
+
+
+def test_bulk_pair_losses_equal_reference_chain():
+    """make_bulk_pair_losses returns exactly env.pair_loss (alignment.py:151-166) while the tenant's mu drifts
+    and fine-tune steps move it, for many requests at once."""
+    import numpy as np
+
+    from macesim.alignment import AlignmentEnv, TenantParams
+    from macesim.workload import PreferencePair, Request, WorkloadType
+    from paper_2510_03283_b200.hostfast import make_bulk_pair_losses
+
+    rng = np.random.default_rng(5)
+    env = AlignmentEnv.create({0: TenantParams(), 1: TenantParams(mu0=0.7)}, seed=3, beta=1.5)
+    reqs = [Request(id=i, tenant=int(rng.integers(0, 2)), workload=WorkloadType.FINETUNE,
+                    arrival_time=float(rng.random() * 20), prompt_tokens=[1, 2, 3], target_output_len=4,
+                    pair=PreferencePair(float(rng.normal(0.5, 2.0)), 4, 4)) for i in range(300)]
+    bulk = make_bulk_pair_losses(env)
+    assert bulk is not None
+    for it in range(50):
+        env.advance_all(float(rng.random() * 0.3))
+        if it % 7 == 3:
+            env.ft_step(reqs[int(rng.integers(0, len(reqs)))])
+        sub = [reqs[int(k)] for k in rng.choice(len(reqs), 40, replace=False)]
+        assert bulk(sub) == [env.pair_loss(r) for r in sub]
