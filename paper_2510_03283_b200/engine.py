@@ -139,6 +139,7 @@ class GpuEngine(Engine):
         self._dec_list: list = []
         self._dec_pending: dict | None = None
         self._dec_est = None
+        self._pre_est: dict[int, tuple] = {}  # request id -> (cached prefix length, its prefill estimate)
 
     # ------------------------------------------------------------------ helpers
     def _slot(self, rid: int) -> int:
@@ -516,14 +517,20 @@ class GpuEngine(Engine):
         if w is WorkloadType.PREFILL and self.fast_host and isinstance(self.trie, GpuPrefixTrie):
             # cost_model.py:95-99 with the memoised cached-prefix walk of a queued prompt
             shared = self.trie.cached_prefix_len_memo(req.id, req.prompt_tokens)
+            hit = self._pre_est.get(req.id)
+            if hit is not None and hit[0] == shared:
+                return hit[1]
             effective = max(0, len(req.prompt_tokens) - shared)
             p = self.profile
-            return WorkloadEstimate(mem=(p.prefill_mem_per_token + p.decode_kv_mem_per_token) * effective,
-                                    lat=p.prefill_lat_per_token * effective)
+            est = WorkloadEstimate(mem=(p.prefill_mem_per_token + p.decode_kv_mem_per_token) * effective,
+                                   lat=p.prefill_lat_per_token * effective)
+            self._pre_est[req.id] = (shared, est)
+            return est
         return super()._estimate(req)
 
     def _retire(self, req, t_end_ms, rejected=False):  # engine.py:538
         self.norm_stream.drop(req.id)
+        self._pre_est.pop(req.id, None)
         if isinstance(self.trie, GpuPrefixTrie):
             self.trie.forget(req.id)
         super()._retire(req, t_end_ms, rejected)

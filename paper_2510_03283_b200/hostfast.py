@@ -55,7 +55,8 @@ class FastPriorityQueue(PriorityQueue):
         # (workload.py:64-66), so an entry is only reused while the request's workload is unchanged
         self._meta: dict[int, tuple] = {}
         self.bulk_loss = None          # optional many-request loss_fn (make_bulk_pair_losses)
-        self._pend: list[tuple] = []   # pushed keys not yet in the columns
+        # pushed keys not yet in the columns: -p, arrival, base, growth, id, is fine-tune; the requests
+        self._pn, self._pa, self._pb, self._pg, self._pi, self._pf = [], [], [], [], [], []
         self._pend_req: list = []
 
     def _meta_of(self, req) -> tuple:
@@ -116,14 +117,18 @@ class FastPriorityQueue(PriorityQueue):
         ps.value = p
         ps.refreshed_at = t
         # keys land in the columns in bulk at the next refresh / pop / peek (_flush)
-        self._pend.append((-p, arrival, base, growth, req.id, is_ft))
+        self._pn.append(-p)
+        self._pa.append(arrival)
+        self._pb.append(base)
+        self._pg.append(growth)
+        self._pi.append(req.id)
+        self._pf.append(is_ft)
         self._pend_req.append(req)
         self._live += 1
         self._order = None
 
     def _flush(self) -> None:
-        pend = self._pend
-        n_new = len(pend)
+        n_new = len(self._pend_req)
         if not n_new:
             return
         while self._n + n_new > self._neg.shape[0]:
@@ -133,16 +138,16 @@ class FastPriorityQueue(PriorityQueue):
                     break
             self._grow()
         k0, k1 = self._n, self._n + n_new
-        cols = np.array(pend, np.float64)  # (-p, arrival, base, growth, id, is_ft): ids < 2^53 are exact
-        self._neg[k0:k1] = cols[:, 0]
-        self._arr[k0:k1] = cols[:, 1]
-        self._bg[k0:k1] = cols[:, 2:4]
-        self._id[k0:k1] = cols[:, 4].astype(np.int64)
-        self._ft[k0:k1] = cols[:, 5] != 0
+        self._neg[k0:k1] = self._pn
+        self._arr[k0:k1] = self._pa
+        self._bg[k0:k1, 0] = self._pb
+        self._bg[k0:k1, 1] = self._pg
+        self._id[k0:k1] = self._pi
+        self._ft[k0:k1] = self._pf
         self._alive[k0:k1] = True
         self._req[k0:k1] = self._pend_req
         self._n = k1
-        self._pend = []
+        self._pn, self._pa, self._pb, self._pg, self._pi, self._pf = [], [], [], [], [], []
         self._pend_req = []
 
     def refresh(self, t: float) -> None:  # priority.py:121-127
