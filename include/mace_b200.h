@@ -270,7 +270,17 @@ int mace_model_destroy(mace_model* model);
 int mace_tick_run(mace_model* model, const MaceTickBuffers* bufs, const MaceTickDesc* tick, void* stream);
 
 /* ---------------------------------------------------------------- host bookkeeping (CPU, no GPU needed)
- * One tick's per-decode-row head statistics, capacity allocation and prune trims
+ * Alg. 1's packing loop (replaces the loop of schedule_iteration, scheduler.py:133-188) over the queue's first
+ * n tasks in pop order with precomputed estimates mem[n] / lat[n] and is_ft[n]; more_queued: the queue holds
+ * more than n. assign[i] = bin index, -1 rejected, -2 deferred, for the first out_counts[0] tasks (the
+ * dequeued ones); out_counts = {dequeued, bins opened, bins examined, bin 0 n_inference, bin 0 n_ft};
+ * out_bin0 = {bin 0 used MB, bin 0 max latency}. Returns 0, or 2 when the loop would dequeue past the n
+ * candidates (the caller runs its own loop). */
+int mace_host_alg1(int n, const double* mem, const double* lat, const int8_t* is_ft, int more_queued,
+                   double budget, double hard_limit, double stop_mem, int tau_task, double lambda1, double lambda2,
+                   int max_ft, int max_inf, int* assign, int* out_counts, double* out_bin0);
+
+/* One tick's per-decode-row head statistics, capacity allocation and prune trims
  * (replaces the per-row Python of Engine._exec_decode, engine.py:496-529 -> HeadStats.update cache.py:291-309,
  * allocate_capacity cache.py:318-352, prune_decision cache.py:355-362), over per-slot state arrays:
  * ring [slots, H, W], count / pos [slots], sums / current / last_used / kept [slots, H], tau [slots] (NaN =

@@ -140,6 +140,9 @@ SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_last_error": (C.c_char_p, [C.c_void_p]),
     "mace_launch_count": (C.c_longlong, [C.c_void_p]),
     "mace_debug_host_prof": (C.c_int, [C.POINTER(C.c_double)]),
+    "mace_host_alg1": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double,
+                                 C.c_double, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_void_p,
+                                 C.c_void_p, C.c_void_p]),
     "mace_host_head_stats": (C.c_int, [C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 11 + [C.c_int, C.c_double,
                                                                                          C.c_void_p, C.c_void_p]),
     "mace_gemm_bf16": (C.c_int, [C.c_void_p, C.POINTER(MaceGemmArgs), C.c_void_p]),

@@ -55,9 +55,9 @@ class FastPriorityQueue(PriorityQueue):
         # (workload.py:64-66), so an entry is only reused while the request's workload is unchanged
         self._meta: dict[int, tuple] = {}
         self.bulk_loss = None          # optional many-request loss_fn (make_bulk_pair_losses)
-        # pushed keys not yet in the columns: -p, arrival, base, growth, id, is fine-tune; the requests
-        self._pn, self._pa, self._pb, self._pg, self._pi, self._pf = [], [], [], [], [], []
-        self._pend_req: list = []
+        # pushed keys not yet in the columns: (-p, arrival, base, growth, id, is fine-tune, request)
+        self._pend: list[tuple] = []
+        self._popped = False  # any pop since the last sort
 
     def _meta_of(self, req) -> tuple:
         w = req.workload
@@ -117,18 +117,12 @@ class FastPriorityQueue(PriorityQueue):
         ps.value = p
         ps.refreshed_at = t
         # keys land in the columns in bulk at the next refresh / pop / peek (_flush)
-        self._pn.append(-p)
-        self._pa.append(arrival)
-        self._pb.append(base)
-        self._pg.append(growth)
-        self._pi.append(req.id)
-        self._pf.append(is_ft)
-        self._pend_req.append(req)
+        self._pend.append((-p, arrival, base, growth, req.id, is_ft, req))
         self._live += 1
         self._order = None
 
     def _flush(self) -> None:
-        n_new = len(self._pend_req)
+        n_new = len(self._pend)
         if not n_new:
             return
         while self._n + n_new > self._neg.shape[0]:
@@ -138,17 +132,17 @@ class FastPriorityQueue(PriorityQueue):
                     break
             self._grow()
         k0, k1 = self._n, self._n + n_new
-        self._neg[k0:k1] = self._pn
-        self._arr[k0:k1] = self._pa
-        self._bg[k0:k1, 0] = self._pb
-        self._bg[k0:k1, 1] = self._pg
-        self._id[k0:k1] = self._pi
-        self._ft[k0:k1] = self._pf
+        pn, pa, pb, pg, pi, pf, preq = zip(*self._pend)
+        self._neg[k0:k1] = pn
+        self._arr[k0:k1] = pa
+        self._bg[k0:k1, 0] = pb
+        self._bg[k0:k1, 1] = pg
+        self._id[k0:k1] = pi
+        self._ft[k0:k1] = pf
         self._alive[k0:k1] = True
-        self._req[k0:k1] = self._pend_req
+        self._req[k0:k1] = preq
         self._n = k1
-        self._pn, self._pa, self._pb, self._pg, self._pi, self._pf = [], [], [], [], [], []
-        self._pend_req = []
+        self._pend = []
 
     def refresh(self, t: float) -> None:  # priority.py:121-127
         self._last_refresh = t
@@ -184,6 +178,7 @@ class FastPriorityQueue(PriorityQueue):
         o = np.lexsort((self._id[live], self._arr[live], self._neg[live]))  # heappop order of (-p, arrival, id)
         self._order = live[o].tolist()
         self._cur = 0
+        self._popped = False
 
     def _front(self) -> int:
         if self._live == 0:
@@ -197,6 +192,7 @@ class FastPriorityQueue(PriorityQueue):
 
     def pop(self):
         k = self._front()
+        self._popped = True
         self._alive[k] = False
         self._live -= 1
         self._cur += 1
@@ -205,6 +201,33 @@ class FastPriorityQueue(PriorityQueue):
         req.priority_state.value = -float(self._neg[k])
         req.priority_state.refreshed_at = self._last_refresh
         return req
+
+    def head(self, K: int) -> list[int] | None:
+        """Slots of the first K entries in pop order, when nothing was popped since the last sort (then
+        every entry of the order is live); None otherwise."""
+        if self._order is None:
+            self._flush()
+            self._sort()
+        if self._popped:
+            return None
+        return self._order[self._cur: self._cur + K]
+
+    def pop_head(self, ks: list[int]) -> None:
+        """Pop the entries ``head`` returned (a prefix of it), as that many pop() calls would."""
+        m = len(ks)
+        if not m:
+            return
+        self._alive[ks] = False
+        self._live -= m
+        self._cur += m
+        self._popped = True
+        t = self._last_refresh
+        reqs = self._req
+        for k, v in zip(ks, (-self._neg[ks]).tolist()):
+            ps = reqs[k].priority_state
+            ps.value = v
+            ps.refreshed_at = t
+            reqs[k] = None
 
     def peek(self):
         if self._order is not None or self._live == 0:
@@ -305,7 +328,60 @@ class NormStream:
             self.owner[slot] = -1
 
 
-def fast_schedule_iteration(queue, capacity_budget, cfg, estimator, t, hard_limit=None, dec_est=None):
+def _native_alg1(queue, capacity_budget, cfg, estimator, hard_limit, dec_est):
+    """Alg. 1 over the queue's head with csrc/hostsched.cu (mace_host_alg1); None hands the iteration to the
+    Python loop (something was popped since the sort, or the dequeue would run past tau_task candidates)."""
+    K = min(len(queue), cfg.tau_task)
+    ks = queue.head(K)
+    if ks is None or not ks:
+        return None
+    reqs = [queue._req[k] for k in ks]
+    DEC, FT = _DEC, _FT
+    ests = [dec_est if (dec_est is not None and r.workload is DEC) else estimator(r) for r in reqs]
+    n = len(reqs)
+    mem = np.array([e.mem for e in ests], np.float64)
+    lat = np.array([e.lat for e in ests], np.float64)
+    ft = np.array([r.workload is FT for r in reqs], np.int8)
+    assign = np.empty(n, np.int32)
+    counts = np.zeros(5, np.int32)
+    bin0 = np.zeros(2, np.float64)
+    from ._lib import lib
+    rc = lib().mace_host_alg1(n, mem.ctypes.data, lat.ctypes.data, ft.ctypes.data, int(len(queue) > n),
+                              float(capacity_budget), float(hard_limit), float(cfg.tau_mem * capacity_budget),
+                              int(cfg.tau_task), float(cfg.lambda1), float(cfg.lambda2), int(cfg.max_ft_batch),
+                              int(cfg.max_decode_batch), assign.ctypes.data, counts.ctypes.data, bin0.ctypes.data)
+    if rc == 2:
+        return None
+    if rc != 0:
+        raise RuntimeError(f"mace_host_alg1 failed ({rc})")
+    count, n_bins, examined = int(counts[0]), int(counts[1]), int(counts[2])
+    queue.pop_head(ks[:count])
+    plan = TickPlan(bin=Bin(capacity_budget))
+    plan.dequeued.extend(reqs[:count])
+    tasks = [[] for _ in range(n_bins)]
+    estl = [[] for _ in range(n_bins)]
+    deferred = []
+    for r, e, a in zip(reqs[:count], ests[:count], assign[:count].tolist()):
+        if a >= 0:
+            tasks[a].append(r)
+            estl[a].append(e)
+        elif a == -1:
+            plan.rejected.append(r)
+        else:
+            deferred.append(r)
+    plan.bins_opened += n_bins
+    plan.bins_examined = examined
+    if n_bins:
+        plan.bin = Bin(capacity_budget, tasks=tasks[0], estimates=estl[0], used_memory=float(bin0[0]),
+                       max_latency=float(bin0[1]), n_inference=int(counts[3]), n_ft=int(counts[4]))
+        for later in tasks[1:]:
+            plan.requeued.extend(later)
+    plan.requeued.extend(deferred)
+    return plan
+
+
+def fast_schedule_iteration(queue, capacity_budget, cfg, estimator, t, hard_limit=None, dec_est=None,
+                            native=True):
     """Alg. 1 exactly as scheduler.py:133-188 (same dequeue stop rule, same best-fit score arithmetic
     lambda1*|free - mem| + lambda2*|maxlat - lat| with free = budget - used, same strict '<' tie rule,
     same requeue / defer / reject lists), with the Bin methods (scheduler.py:81-117) inlined into local
@@ -314,6 +390,10 @@ def fast_schedule_iteration(queue, capacity_budget, cfg, estimator, t, hard_limi
     estimate (cost_model.py:100-102), used without the call when given."""
     if hard_limit is None:
         hard_limit = capacity_budget
+    if native and isinstance(queue, FastPriorityQueue) and len(queue):
+        plan = _native_alg1(queue, capacity_budget, cfg, estimator, hard_limit, dec_est)
+        if plan is not None:
+            return plan
     plan = TickPlan(bin=Bin(capacity_budget))
     FT = _FT
     max_ft, max_inf = cfg.max_ft_batch, cfg.max_decode_batch

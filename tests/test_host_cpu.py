@@ -278,7 +278,8 @@ def test_fast_schedule_iteration_matches_reference():
         budget = float(rng.choice([50.0, 200.0, 1000.0]))
         hard = budget * float(rng.choice([1.0, 1.5]))
         ests = {}
-        queues = (PriorityQueue(PriorityParams(), lambda r: 0.1), FastPriorityQueue(PriorityParams(), lambda r: 0.1))
+        queues = (PriorityQueue(PriorityParams(), lambda r: 0.1), FastPriorityQueue(PriorityParams(), lambda r: 0.1),
+                  FastPriorityQueue(PriorityParams(), lambda r: 0.1))
         for rid in range(int(rng.integers(0, 60))):
             w = kinds[int(rng.integers(0, 3))]
             pair = PreferencePair(0.5, 4, 4) if w is WorkloadType.FINETUNE else None
@@ -292,15 +293,19 @@ def test_fast_schedule_iteration_matches_reference():
             q.refresh(5.0)
         est = lambda r: ests[r.id]  # noqa: E731
         a = schedule_iteration(queues[0], budget, cfg, est, 5.0, hard_limit=hard)
-        b = fast_schedule_iteration(queues[1], budget, cfg, est, 5.0, hard_limit=hard)
         ids = lambda xs: [r.id for r in xs]  # noqa: E731
-        assert ids(a.bin.tasks) == ids(b.bin.tasks), trial
-        assert ids(a.requeued) == ids(b.requeued) and ids(a.rejected) == ids(b.rejected)
-        assert ids(a.dequeued) == ids(b.dequeued)
-        assert (a.bins_opened, a.bins_examined) == (b.bins_opened, b.bins_examined)
-        assert (a.bin.used_memory, a.bin.max_latency, a.bin.n_inference, a.bin.n_ft) == \
-            (b.bin.used_memory, b.bin.max_latency, b.bin.n_inference, b.bin.n_ft)
-        assert len(queues[0]) == len(queues[1])
+        for q, native in ((queues[1], True), (queues[2], False)):  # csrc/hostsched.cu and the Python loop
+            b = fast_schedule_iteration(q, budget, cfg, est, 5.0, hard_limit=hard, native=native)
+            assert ids(a.bin.tasks) == ids(b.bin.tasks), trial
+            assert ids(a.requeued) == ids(b.requeued) and ids(a.rejected) == ids(b.rejected)
+            assert ids(a.dequeued) == ids(b.dequeued)
+            assert (a.bins_opened, a.bins_examined) == (b.bins_opened, b.bins_examined)
+            assert (a.bin.used_memory, a.bin.max_latency, a.bin.n_inference, a.bin.n_ft) == \
+                (b.bin.used_memory, b.bin.max_latency, b.bin.n_inference, b.bin.n_ft)
+            assert [r.priority_state.value for r in a.dequeued] == [r.priority_state.value for r in b.dequeued]
+            assert len(queues[0]) == len(q)
+        rest = [[q.pop().id for _ in range(len(q))] for q in queues]  # the queues stay in step afterwards
+        assert rest[0] == rest[1] == rest[2]
 
 
 def test_cached_prefix_memo_tracks_trie_changes():
