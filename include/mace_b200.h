@@ -133,8 +133,8 @@ int mace_argmax(mace_ctx* ctx, const float* logits, int n, int V, int ld, int* o
  * Work lists are built per tick by the host:
  *   tc_items  int4 [n_tc]  = (seq, q_head, q_block, 0)
  *   dec_items int4 [n_dec] = (seq, kv_head, chunk << 16 | n_chunks, partial_base), ordered longest
- *             first; warps take items dynamically from the monotonic 64-bit ticket counter dec_work
- *             (never reset; the ctx remembers where each counter's next launch starts). Multi-chunk
+ *             first; warps take items dynamically from the ticket counter dec_work (zero between
+ *             launches: the warp drawing a launch's final ticket resets it). Multi-chunk
  *             partials go to
  *             dec_workspace[partial_base + chunk] ((2G + G*hd) fp32 each) and are merged in chunk
  *             order; dec_counters is a zero-initialised int [slots * Hkv] left zeroed.            */
@@ -151,7 +151,7 @@ typedef struct MaceAttnArgs {
   float scale;        /* softmax scale, 0 -> 1/sqrt(hd) */
   void* dec_workspace; size_t dec_workspace_bytes;
   int* dec_counters;
-  unsigned long long* dec_work;  /* zero-initialised ticket counter, owned by the caller, one per ctx */
+  unsigned long long* dec_work;  /* zero-initialised ticket counter, owned by the caller; each launch leaves it zero */
   int decode_impl;    /* 0 auto, 1 CUDA-core streaming kernel, 2 tcgen05 swap-AB kernel */
 } MaceAttnArgs;
 int mace_attn_fwd(mace_ctx* ctx, const MaceAttnArgs* args, void* stream);

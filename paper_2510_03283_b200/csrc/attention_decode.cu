@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(Dec2<HD, G>::WARPS * 32) attn_decode2_kernel(
     int n_items, const MaceKvLayout kv, const __nv_bfloat16* __restrict__ k_pool,
     const __nv_bfloat16* __restrict__ v_pool, int Hq, int Hkv, float scale_log2, __nv_bfloat16* __restrict__ out,
     float* __restrict__ head_norm, float* __restrict__ partials, int* __restrict__ counters,
-    unsigned long long* __restrict__ work, unsigned long long work_base) {
+    unsigned long long* __restrict__ work, unsigned long long n_warps_total) {
   using C = Dec2<HD, G>;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -61,12 +61,16 @@ __global__ void __launch_bounds__(Dec2<HD, G>::WARPS * 32) attn_decode2_kernel(
   uint32_t ring_count = 0;  // pages issued by this warp so far (mbarrier phase bookkeeping across items)
 
   while (true) {
-    // dynamic work distribution (items arrive longest-first): a monotonic 64-bit ticket counter, so no
-    // per-launch reset is needed (the host passes this launch's base)
+    // dynamic work distribution (items arrive longest-first) from a ticket counter that is zero between
+    // launches: every warp draws exactly one ticket past the last item and leaves, so the warp drawing the
+    // launch's final ticket (n_items + warps - 1) is the last to touch the counter and resets it
     unsigned long long ticket = 0;
-    if (lane == 0) ticket = atomicAdd(work, 1ull);
+    if (lane == 0) {
+      ticket = atomicAdd(work, 1ull);
+      if (ticket == (unsigned long long)n_items + n_warps_total - 1) atomicExch(work, 0ull);
+    }
     ticket = __shfl_sync(0xffffffffu, ticket, 0);
-    const long long item = (long long)(ticket - work_base);
+    const long long item = (long long)ticket;
     if (item >= n_items) break;
     const int4 it = items[item];
     const MaceSeq sq = seqs[it.x];
@@ -329,11 +333,8 @@ int launch_decode2(MaceCtx* ctx, const MaceAttnArgs* a, float scale_log2, cudaSt
   int grid = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
   const int need_ctas = (a->n_dec + C::WARPS - 1) / C::WARPS;
   if (grid > need_ctas) grid = need_ctas;
-  // tickets of this launch start where the previous launch on this counter stopped; every warp takes
-  // exactly one ticket past the end, so a launch consumes n_dec + grid * WARPS tickets
-  unsigned long long& next = ctx->work_next[a->dec_work];
-  const unsigned long long base = next;
-  next += (unsigned long long)a->n_dec + (unsigned long long)grid * C::WARPS;
+  // the kernel leaves the ticket counter at zero (its last ticket resets it): nothing to track here
+  const unsigned long long base = (unsigned long long)grid * C::WARPS;
   launch_k(attn_decode2_kernel<HD, G>, grid, C::WARPS * 32, C::SMEM, s, 
       (const __nv_bfloat16*)a->qkv, a->seqs, reinterpret_cast<const int4*>(a->dec_items), a->n_dec, a->kv,
       (const __nv_bfloat16*)a->k_pool, (const __nv_bfloat16*)a->v_pool, a->Hq, a->Hkv, scale_log2,

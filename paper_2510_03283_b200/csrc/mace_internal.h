@@ -31,7 +31,6 @@ struct MaceCtx {
   long long launches = 0;
   std::string last_error;
   PFN_cuTensorMapEncodeTiled_v12000 encode_tiled = nullptr;
-  std::unordered_map<const void*, unsigned long long> work_next;  // decode-attention ticket counters
 };
 
 int mace_fail(MaceCtx* ctx, int code, const std::string& msg);

@@ -140,6 +140,8 @@ class GpuEngine(Engine):
         self._dec_pending: dict | None = None
         self._dec_est = None
         self._pre_est: dict[int, tuple] = {}  # request id -> (cached prefix length, its prefill estimate)
+        self._pair_tokens: dict[int, tuple] = {}  # FT request id -> ((id, n_c, n_r), (chosen, rejected))
+        self._route_later: list | None = None     # route-backs of the executing bin (pushed after it)
 
     # ------------------------------------------------------------------ helpers
     def _slot(self, rid: int) -> int:
@@ -246,6 +248,16 @@ class GpuEngine(Engine):
             # decode attention work items: (seq, kv head, chunk << 16 | n_chunks, partial base), LPT order
             npp = (P - 1 + PAGE - 1) // PAGE
             nch = np.maximum(1, -(-npp // DECODE_CHUNK_PAGES))
+        if n_dec and int(nch.max()) == 1:
+            # every context fits one chunk: one item per (decode, kv head); a stable sort of the decodes by
+            # pages, heads ascending within each, is the stable sort of the expanded items
+            o = np.argsort(-(npp + k0 // PAGE + 1), kind="stable").astype(i32)
+            dec_items = np.empty((n_dec * Hkv, 4), i32)
+            dec_items[:, 0] = np.repeat(si0 + o, Hkv)
+            dec_items[:, 1] = np.tile(np.arange(Hkv, dtype=i32), n_dec)
+            dec_items[:, 2] = 1
+            dec_items[:, 3] = 0
+        elif n_dec:
             per = -(-npp // nch)
             n_it = nch * Hkv
             seq_i = np.repeat(np.arange(si0, si0 + n_dec, dtype=i32), n_it)
@@ -278,7 +290,11 @@ class GpuEngine(Engine):
             room = max(1, c.max_pos - P)
             n_c = min(req.pair.tokens_chosen, room)
             n_r = min(req.pair.tokens_rejected, room)
-            chs, rjs = synthetic_pair_tokens(self.seed, req.id, n_c, n_r, c.vocab)
+            key = (req.id, n_c, n_r)
+            hit = self._pair_tokens.get(req.id)
+            if hit is None or hit[0] != key:
+                hit = self._pair_tokens[req.id] = (key, synthetic_pair_tokens(self.seed, req.id, n_c, n_r, c.vocab))
+            chs, rjs = hit[1]
             pairs.append(FtPair(req.id, req.prompt_tokens, chs, rjs, self.ref_lp.get(req.id)))
             pr = []
             for side, resp in enumerate((chs, rjs)):
@@ -378,10 +394,15 @@ class GpuEngine(Engine):
         # (thread-safe: another engine's trie, e.g. a concurrent sweep thread, falls through to the reference)
         _ref_engine.dfs_order = lambda trie, pending, _o=prefills, _t=self.trie: (
             list(_o) if trie is _t else _ref_dfs_order(trie, pending))
+        defer = isinstance(self.queue, FastPriorityQueue)
+        self._route_later = [] if defer else None
         try:
             super()._execute(plan)
         finally:
             _ref_engine.dfs_order = _ref_dfs_order
+            later, self._route_later = self._route_later, None
+            if later:  # the bin's route-backs, pushed together at the clock they were issued at
+                self.queue.push_many(later, self.clock)
         # ---- mirror post-tick KV decisions onto the device (retired requests were released already)
         live_dec = [r for r in decodes if r.id in self.slot_of]
         if self.pruning and live_dec:
@@ -434,6 +455,12 @@ class GpuEngine(Engine):
         finally:
             self._budget_end = None
         return self.ticks_done - start
+
+    def _route_back(self, req, continued_ft):  # engine.py:561 — inside _execute: collected, pushed in bulk
+        later = self._route_later
+        if later is None:
+            return super()._route_back(req, continued_ft)
+        later.append(req)
 
     def _exec_prefill(self, req):  # engine.py:444 — check our plan against the reference's charge
         if self.trie is not None and self.state[req.id].leaf is not None:
@@ -531,6 +558,7 @@ class GpuEngine(Engine):
     def _retire(self, req, t_end_ms, rejected=False):  # engine.py:538
         self.norm_stream.drop(req.id)
         self._pre_est.pop(req.id, None)
+        self._pair_tokens.pop(req.id, None)
         if isinstance(self.trie, GpuPrefixTrie):
             self.trie.forget(req.id)
         super()._retire(req, t_end_ms, rejected)

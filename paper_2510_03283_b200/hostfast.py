@@ -121,6 +121,45 @@ class FastPriorityQueue(PriorityQueue):
         self._live += 1
         self._order = None
 
+    def push_many(self, reqs, t: float) -> None:
+        """push(req, t) for every request, keys computed together (same arithmetic, same contract checks)."""
+        n = len(reqs)
+        if not n:
+            return
+        meta = self._meta
+        ms = []
+        for r in reqs:
+            m = meta.get(r.id)
+            if m is None or m[4] is not r.workload:
+                m = self._meta_of(r)
+            ms.append(m)
+        arr = np.fromiter((m[0] for m in ms), np.float64, n)
+        if (t < arr).any():
+            bad = reqs[int(np.argmax(t < arr))]
+            raise PriorityContractError(
+                f"priority query at t={t} before arrival of request {bad.id} at {bad.arrival_time}")
+        base = np.fromiter((m[1] for m in ms), np.float64, n)
+        growth = np.fromiter((m[2] for m in ms), np.float64, n)
+        p = base + growth * (t - arr)  # dynamic_priority (priority.py:73), elementwise, no FMA
+        fts = [i for i, m in enumerate(ms) if m[3]]
+        if fts and self.loss_fn is not None:  # ft_total_priority (priority.py:76-81)
+            fr = [reqs[i] for i in fts]
+            losses = self.bulk_loss(fr) if self.bulk_loss is not None else [self.loss_fn(r) for r in fr]
+            gamma = self.params.gamma
+            for i, loss in zip(fts, losses):
+                if loss < 0:
+                    raise PriorityContractError("loss must be >= 0 under the positive-loss convention")
+                p[i] = p[i] + gamma * loss
+        pl = p.tolist()
+        for r, v in zip(reqs, pl):
+            ps = r.priority_state
+            ps.value = v
+            ps.refreshed_at = t
+        self._pend.extend(zip((-p).tolist(), arr.tolist(), base.tolist(), growth.tolist(), [r.id for r in reqs],
+                              [m[3] for m in ms], reqs))
+        self._live += n
+        self._order = None
+
     def _flush(self) -> None:
         n_new = len(self._pend)
         if not n_new:
