@@ -471,29 +471,29 @@ class GpuEngine(Engine):
         return super()._exec_prefill(req)
 
     def _exec_decode(self, req, t_end_ms):  # engine.py:482 — same effects, head stats batched per tick
-        if not (self.fast_host and self.pruning):
+        pend = self._dec_pending
+        if pend is None:
+            if not (self.fast_host and self.pruning) or self.state[req.id].head_stats is None:
+                return super()._exec_decode(req, t_end_ms)
+            pend = self._dec_pending = self._batch_head_stats()
+        hit = pend.get(req.id)
+        if hit is None:  # no head stats for this row: the reference path (engine.py:530-532)
             return super()._exec_decode(req, t_end_ms)
+        kept, released = hit
         rs = self.state[req.id]
-        if rs.head_stats is None:
-            return super()._exec_decode(req, t_end_ms)
-        if self._dec_pending is None:
-            self._dec_pending = self._batch_head_stats()
-        kept, released = self._dec_pending[req.id]
         req.decode_pos += 1
-        self.metrics.decoded_tokens += 1
+        metrics = self.metrics
+        metrics.decoded_tokens += 1
         if rs.first_token_ms is None:
             rs.first_token_ms = t_end_ms
-            self.metrics.ttft_ms[req.id] = t_end_ms - req.arrival_time * 1000.0
-            self.metrics.tbt_ms[req.id] = []
+            metrics.ttft_ms[req.id] = t_end_ms - req.arrival_time * 1000.0
+            metrics.tbt_ms[req.id] = []
         else:
-            self.metrics.tbt_ms[req.id].append(t_end_ms - rs.last_token_ms)
+            metrics.tbt_ms[req.id].append(t_end_ms - rs.last_token_ms)
         rs.last_token_ms = t_end_ms
-        kv = self.profile.decode_kv_mem_per_token
-        heads = self.cache_cfg.num_heads
-        per_head = kv / heads
+        heads, per_head, grown = self._dec_consts
         rs.kept = kept
         self.slots_created += heads
-        grown = per_head * heads
         rs.resident_kv_mb += grown
         self._resident_kv_total += grown
         if released:
@@ -506,6 +506,9 @@ class GpuEngine(Engine):
 
     def _batch_head_stats(self) -> dict:
         """Head-stats + allocation + prune for every decode row of this tick (id order)."""
+        heads = self.cache_cfg.num_heads
+        per_head = self.profile.decode_kv_mem_per_token / heads  # engine.py:494-497, same expressions
+        self._dec_consts = (heads, per_head, per_head * heads)
         rows = [r for r in self._dec_list if self.state[r.id].head_stats is not None]
         out: dict = {}
         if not rows:
