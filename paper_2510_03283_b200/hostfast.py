@@ -155,21 +155,35 @@ class FastPriorityQueue(PriorityQueue):
             ps = r.priority_state
             ps.value = v
             ps.refreshed_at = t
-        self._pend.extend(zip((-p).tolist(), arr.tolist(), base.tolist(), growth.tolist(), [r.id for r in reqs],
-                              [m[3] for m in ms], reqs))
+        # straight into the columns (no pending tuples)
+        self._reserve(n, len(self._pend))
+        k0, k1 = self._n, self._n + n
+        self._neg[k0:k1] = -p
+        self._arr[k0:k1] = arr
+        self._bg[k0:k1, 0] = base
+        self._bg[k0:k1, 1] = growth
+        self._id[k0:k1] = [r.id for r in reqs]
+        self._ft[k0:k1] = [m[3] for m in ms]
+        self._alive[k0:k1] = True
+        self._req[k0:k1] = reqs
+        self._n = k1
         self._live += n
         self._order = None
+
+    def _reserve(self, n_new: int, pending: int = 0) -> None:
+        """Room for n_new more column entries (``pending``: how many of the live count are not in the columns)."""
+        while self._n + n_new > self._neg.shape[0]:
+            if self._live - pending < self._n // 2:
+                self._compact()
+                if self._n + n_new <= self._neg.shape[0]:
+                    break
+            self._grow()
 
     def _flush(self) -> None:
         n_new = len(self._pend)
         if not n_new:
             return
-        while self._n + n_new > self._neg.shape[0]:
-            if self._live - n_new < self._n // 2:
-                self._compact()
-                if self._n + n_new <= self._neg.shape[0]:
-                    break
-            self._grow()
+        self._reserve(n_new, n_new)
         k0, k1 = self._n, self._n + n_new
         pn, pa, pb, pg, pi, pf, preq = zip(*self._pend)
         self._neg[k0:k1] = pn

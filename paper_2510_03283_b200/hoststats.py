@@ -42,6 +42,7 @@ class BatchedHeadStats:
         self.last_used = np.zeros((n_slots, n_heads))
         self.tau = np.full(n_slots, np.nan)
         self.kept = np.zeros((n_slots, n_heads), np.int64)
+        self._state_ptrs = None
 
     def reset(self, slots: np.ndarray) -> None:
         self.count[slots] = 0
@@ -64,11 +65,14 @@ class BatchedHeadStats:
         norms = np.ascontiguousarray(norms, np.float64)
         kept = np.empty((n, self.H), np.int64)
         released = np.empty(n, np.int64)
-        p = lambda a: a.ctypes.data  # noqa: E731
+        st = self._state_ptrs
+        if st is None:  # the state arrays never move: their addresses are taken once
+            st = self._state_ptrs = tuple(a.ctypes.data for a in (self.ring, self.count, self.pos, self.sums,
+                                                                   self.current, self.last_used, self.tau,
+                                                                   self.kept))
         rc = _native().mace_host_head_stats(
-            n, self.H, self.W, p(slots), p(steps), p(norms), p(self.ring), p(self.count), p(self.pos), p(self.sums),
-            p(self.current), p(self.last_used), p(self.tau), p(self.kept), self.c_total, float(self.prune_window),
-            p(kept), p(released))
+            n, self.H, self.W, slots.ctypes.data, steps.ctypes.data, norms.ctypes.data, *st, self.c_total,
+            float(self.prune_window), kept.ctypes.data, released.ctypes.data)
         if rc == 1:
             return self.step_numpy(slots, steps, norms)
         if rc != 0:

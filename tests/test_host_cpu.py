@@ -199,6 +199,7 @@ def test_fast_priority_queue_matches_reference_heap():
     ref, fast = PriorityQueue(PriorityParams(), loss_fn), FastPriorityQueue(PriorityParams(), loss_fn)
     t, rid = 0.0, 0
     for step in range(300):
+        batch = []
         for _ in range(int(rng.integers(0, 12))):
             w = kinds[int(rng.integers(0, 3))]
             arr = t if rng.random() < 0.3 else min(t, round(t - rng.random(), 1))  # ties on arrival time
@@ -207,8 +208,13 @@ def test_fast_priority_queue_matches_reference_heap():
                                  target_output_len=4, pair=pair)
             losses[rid] = float(rng.choice([0.0, 0.3, rng.random()]))
             ref.push(mk(), t)
-            fast.push(mk(), t)
+            batch.append(mk())
             rid += 1
+        if rng.random() < 0.5:
+            fast.push_many(batch, t)  # the bulk route-back path
+        else:
+            for r in batch:
+                fast.push(r, t)
         if rng.random() < 0.5:
             t += float(rng.choice([0.0, 0.05, rng.random()]))
             for k in list(losses):
