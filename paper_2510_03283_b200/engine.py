@@ -142,6 +142,7 @@ class GpuEngine(Engine):
         self._pre_est: dict[int, tuple] = {}  # request id -> (cached prefix length, its prefill estimate)
         self._pair_tokens: dict[int, tuple] = {}  # FT request id -> ((id, n_c, n_r), (chosen, rejected))
         self._route_later: list | None = None     # route-backs of the executing bin (pushed after it)
+        self._release_later: list | None = None   # KV slots retired by the executing bin (released after it)
 
     # ------------------------------------------------------------------ helpers
     def _slot(self, rid: int) -> int:
@@ -396,6 +397,7 @@ class GpuEngine(Engine):
             list(_o) if trie is _t else _ref_dfs_order(trie, pending))
         defer = isinstance(self.queue, FastPriorityQueue)
         self._route_later = [] if defer else None
+        self._release_later = []
         try:
             super()._execute(plan)
         finally:
@@ -403,6 +405,9 @@ class GpuEngine(Engine):
             later, self._route_later = self._route_later, None
             if later:  # the bin's route-backs, pushed together at the clock they were issued at
                 self.queue.push_many(later, self.clock)
+            rel, self._release_later = self._release_later, None
+            if rel:  # retired rows' KV slots (before any later tick can reuse them)
+                m.release_slots(rel)
         # ---- mirror post-tick KV decisions onto the device (retired requests were released already)
         live_dec = [r for r in decodes if r.id in self.slot_of]
         if self.pruning and live_dec:
@@ -571,7 +576,10 @@ class GpuEngine(Engine):
             for g in table:
                 self.pool.decref(g)
         if slot is not None:
-            self.model.release_slots([slot])
+            if self._release_later is not None:  # inside the bin's bookkeeping: one release call per tick
+                self._release_later.append(slot)
+            else:
+                self.model.release_slots([slot])
             self.free_slots.append(slot)
 
     # ------------------------------------------------------------------ results
