@@ -978,7 +978,8 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   // CTA-pair kernel (MN-major operands: single-CTA BN 256). Otherwise a per-k-block cost model fitted on the
   // tick's shapes picks among single-CTA BN 64 / 128 / 192 / 256 and pair BN 128:
   //   t ~ waves x k-blocks x c(BN),  c = 0.17 / 0.19 / 0.34 / 0.49 us (single), 0.155 us (pair 128)
-  // (a fixed ~4 us launch / fill / epilogue cost is common to all; pair only with >= 48 k-blocks). Split-K only
+  // (a fixed ~4 us launch / fill / epilogue cost is common to all, the pair kernel pays ~0.6 us more and is
+  // considered from 32 k-blocks). Split-K only
   // for < 37 tiles with >= 24
   // k-blocks per split: measured slower everywhere else (slab round trip + finalize launch).
   const int num_m = (g->M + kBM - 1) / kBM;
@@ -1009,9 +1010,9 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
         bn = kBn[c];
       }
     }
-    if (pair_ok && kb_total >= 48) {  // the pair kernel's fill only pays off over long K loops
+    if (pair_ok && kb_total >= 32) {  // the pair kernel's longer fill (~0.6 us) only pays off over long K loops
       const long t2 = (long)num_m2 * ((g->N + 127) / 128);
-      if ((double)((t2 + pairs - 1) / pairs) * kb_total * 0.155 < best) pair_bn = 128;
+      if ((double)((t2 + pairs - 1) / pairs) * kb_total * 0.155 + 0.6 < best) pair_bn = 128;
     }
   }
   int splits = g->split_k > 0 ? g->split_k : 1;

@@ -24,6 +24,13 @@ st = model.step
 def step(*a, **k):
     t = time.perf_counter(); r = st(*a, **k); acc["step"] += time.perf_counter() - t; return r
 model.step = step
+if os.environ.get("GC_MODE") == "freeze":
+    import gc
+    gc.collect()
+    gc.freeze()
+elif os.environ.get("GC_MODE") == "off":
+    import gc
+    gc.disable()
 hp = (ctypes.c_double * 4)()
 L.mace_debug_host_prof(hp)
 t0 = time.perf_counter()
