@@ -133,9 +133,42 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int T, int Hq, i
                                const float* __restrict__ cos_t, const float* __restrict__ sin_t, int apply_rope,
                                const MaceKvLayout kv, __nv_bfloat16* __restrict__ k_pool,
                                __nv_bfloat16* __restrict__ v_pool) {
+  const int row = blockIdx.x;
+  // the row tables and page tables were written before this tick's first kernel (H2D upload, page
+  // allocation): the destination of each thread's 16-byte chunk is resolved before the PDL wait
+  constexpr int kMaxChunks = 4;  // chunks per thread (Hkv * hd / 8 <= 4 * blockDim.x; checked at launch)
+  long long dst[kMaxChunks];
+  int src[kMaxChunks];
+  int n_chunks = 0;
+  bool paged = false;
+  if (row < T) {
+    const MaceSeq sq = seqs[row_seq[row]];
+    paged = sq.kind != 2 && k_pool != nullptr;
+    if (paged) {
+      const int t = row_kvi[row];
+#pragma unroll
+      for (int j = 0; j < kMaxChunks; ++j) {
+        const int idx = threadIdx.x + j * blockDim.x;
+        dst[j] = 0;
+        src[j] = 0;
+        if (idx < Hkv * (hd / 8)) {
+          const int h = idx / (hd / 8), c = (idx % (hd / 8)) * 8;
+          int page;
+          if (sq.kind == 0) {
+            page = kv.ptab[(size_t)sq.slot * kv.max_prompt_pages + t / kPageTokens] * Hkv + h;
+          } else {
+            const int base = kv.dec_base[sq.slot * Hkv + h];
+            page = kv.dtab[((size_t)sq.slot * Hkv + h) * kv.max_dec_pages + (t - base) / kPageTokens];
+          }
+          dst[j] = ((long long)page * kPageTokens + (t % kPageTokens)) * hd + c;
+          src[j] = h * hd + c;
+          n_chunks = j + 1;
+        }
+      }
+    }
+  }
   pdl_wait();
   pdl_trigger();
-  const int row = blockIdx.x;
   if (row >= T) return;
   const int W = (Hq + 2 * Hkv) * hd;
   __nv_bfloat16* r = qkv + (size_t)row * W;
@@ -154,21 +187,13 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int T, int Hq, i
     }
     __syncthreads();
   }
-  const MaceSeq sq = seqs[row_seq[row]];
-  if (sq.kind == 2 || k_pool == nullptr) return;
-  const int t = row_kvi[row];
-  for (int idx = threadIdx.x; idx < Hkv * (hd / 8); idx += blockDim.x) {
-    const int h = idx / (hd / 8), c = (idx % (hd / 8)) * 8;
-    int page;
-    if (sq.kind == 0) {
-      page = kv.ptab[(size_t)sq.slot * kv.max_prompt_pages + t / kPageTokens] * Hkv + h;
-    } else {
-      const int base = kv.dec_base[sq.slot * Hkv + h];
-      page = kv.dtab[((size_t)sq.slot * Hkv + h) * kv.max_dec_pages + (t - base) / kPageTokens];
+  if (!paged) return;
+#pragma unroll
+  for (int j = 0; j < kMaxChunks; ++j) {
+    if (j < n_chunks) {
+      *reinterpret_cast<uint4*>(k_pool + dst[j]) = *reinterpret_cast<const uint4*>(r + Hq * hd + src[j]);
+      *reinterpret_cast<uint4*>(v_pool + dst[j]) = *reinterpret_cast<const uint4*>(r + (Hq + Hkv) * hd + src[j]);
     }
-    const size_t off = ((size_t)page * kPageTokens + (t % kPageTokens)) * hd + c;
-    *reinterpret_cast<uint4*>(k_pool + off) = *reinterpret_cast<const uint4*>(r + (Hq + h) * hd + c);
-    *reinterpret_cast<uint4*>(v_pool + off) = *reinterpret_cast<const uint4*>(r + (Hq + Hkv + h) * hd + c);
   }
 }
 
@@ -297,6 +322,7 @@ extern "C" int mace_rope_kv(mace_ctx* ctx, void* qkv, int T, int Hq, int Hkv, in
                             void* stream) {
   if (T <= 0) return 0;
   if (hd % 8) return mace_fail(ctx, MACE_ERR_ARG, "rope_kv: hd % 8");
+  if (Hkv * (hd / 8) > 4 * 128) return mace_fail(ctx, MACE_ERR_ARG, "rope_kv: Hkv * hd / 8 > 512");
   launch_k(rope_kv_kernel, T, 128, 0, (cudaStream_t)stream, (__nv_bfloat16*)qkv, T, Hq, Hkv, hd, row_pos, row_seq, row_kvi,
                                                       seqs, cos_t, sin_t, apply_rope, *kv, (__nv_bfloat16*)k_pool,
                                                       (__nv_bfloat16*)v_pool);
