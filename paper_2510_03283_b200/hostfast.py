@@ -390,7 +390,10 @@ def _native_alg1(queue, capacity_budget, cfg, estimator, hard_limit, dec_est):
         return None
     reqs = [queue._req[k] for k in ks]
     DEC, FT = _DEC, _FT
-    ests = [dec_est if (dec_est is not None and r.workload is DEC) else estimator(r) for r in reqs]
+    try:
+        ests = [dec_est if (dec_est is not None and r.workload is DEC) else estimator(r) for r in reqs]
+    except Exception:  # e.g. a malformed request past the stop point: the Python loop raises where Alg. 1 would
+        return None
     n = len(reqs)
     mem = np.array([e.mem for e in ests], np.float64)
     lat = np.array([e.lat for e in ests], np.float64)
