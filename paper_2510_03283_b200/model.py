@@ -14,8 +14,8 @@ hand-written sm_100a kernel (see csrc/). Device state that persists across ticks
 from __future__ import annotations
 
 import ctypes as C
-import os
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -324,7 +324,7 @@ class HybridModel:
             else:
                 self.release_slots(op[1])
 
-    def _upload(self, batch: TickBatch) -> dict[str, torch.Tensor]:
+    def _upload(self, batch: TickBatch) -> dict[str, int | None]:
         if getattr(batch, "_packed", None) is None:
             batch._packed = batch.packed()
         buf, layout = batch._packed
@@ -336,11 +336,10 @@ class HybridModel:
         host = torch.from_numpy(buf).pin_memory()
         self.idx[:n].copy_(host, non_blocking=True)
         self.h2d_bytes = n * 4
-        views = {}
-        for name, (off, shape) in layout.items():
-            cnt = int(np.prod(shape)) if len(shape) else 0
-            views[name] = self.idx[off: off + cnt].view(*shape) if cnt else None
-        return views
+        # device addresses of the packed tables (int32 each; None for an empty table)
+        base = self.idx.data_ptr()
+        return {name: (base + 4 * off if (len(shape) and math.prod(shape)) else None)
+                for name, (off, shape) in layout.items()}
 
     # ------------------------------------------------------------------ tick
     @torch.no_grad()
@@ -369,14 +368,14 @@ class HybridModel:
         for name in ("tokens", "pos", "row_seq", "row_kvi", "seqs", "dec_slots", "dec_rows", "ptab_slots",
                      "ptab_rows", "page_copies", "ft_local_rows", "ft_targets", "pair_rows", "row_ps", "ref_cached",
                      "ft_seqs", "ft_row_seq"):
-            setattr(d, name, _p(v[name]))
-        d.tc_items, d.n_tc = _p(v["tc_items"]), batch.tc_items.shape[0]
+            setattr(d, name, v[name])
+        d.tc_items, d.n_tc = v["tc_items"], batch.tc_items.shape[0]
         d.n_tc_inference = int(batch.meta.get("n_tc_inference", d.n_tc))
-        d.dec_items, d.n_dec_items = _p(v["dec_items"]), batch.dec_items.shape[0]
+        d.dec_items, d.n_dec_items = v["dec_items"], batch.dec_items.shape[0]
         d.n_ptab, d.ptab_cols = batch.ptab_slots.shape[0], batch.ptab_rows.shape[1] if batch.ptab_rows.ndim == 2 else 0
         d.n_copies = batch.page_copies.shape[0]
-        d.ft_tc_items, d.n_ft_tc = _p(v["ft_tc_items"]), batch.ft_tc_items.shape[0]
-        d.bwd_items, d.n_bwd = _p(v["bwd_items"]), batch.bwd_items.shape[0]
+        d.ft_tc_items, d.n_ft_tc = v["ft_tc_items"], batch.ft_tc_items.shape[0]
+        d.bwd_items, d.n_bwd = v["bwd_items"], batch.bwd_items.shape[0]
         events = None
         if self.instrument is not None and n_dec and T:
             events = [torch.cuda.Event(enable_timing=True) for _ in range(2 * self.cfg.n_layers)]
