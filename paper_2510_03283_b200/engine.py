@@ -143,6 +143,8 @@ class GpuEngine(Engine):
         self._pair_tokens: dict[int, tuple] = {}  # FT request id -> ((id, n_c, n_r), (chosen, rejected))
         self._route_later: list | None = None     # route-backs of the executing bin (pushed after it)
         self._release_later: list | None = None   # KV slots retired by the executing bin (released after it)
+        self._tok_arena: torch.Tensor | None = None  # pinned arena for the per-tick greedy-token copies
+        self._tok_off = 0
 
     # ------------------------------------------------------------------ helpers
     def _slot(self, rid: int) -> int:
@@ -151,6 +153,17 @@ class GpuEngine(Engine):
                 raise RuntimeError("out of KV slots (raise HybridModel max_slots)")
             self.slot_of[rid] = self.free_slots.pop()
         return self.slot_of[rid]
+
+    def _token_slots(self, n: int) -> torch.Tensor:
+        """n int32 slots of pinned host memory for this tick's greedy tokens: carved from a pinned arena (the
+        tokens are kept for decoded_tokens() anyway), a new arena when the current one is full."""
+        a = self._tok_arena
+        if a is None or self._tok_off + n > a.numel():
+            a = self._tok_arena = torch.empty(max(1 << 16, n), dtype=torch.int32, pin_memory=True)
+            self._tok_off = 0
+        t = a[self._tok_off: self._tok_off + n]
+        self._tok_off += n
+        return t
 
     def _resolve_ref(self) -> None:
         for host, ev, rids in self._pending_ref:
@@ -415,7 +428,7 @@ class GpuEngine(Engine):
             kept = np.array([self.state[r.id].kept for r in live_dec], np.int32)
             m.apply_trim(slots, kept)
         if out.dec_tokens is not None and self.keep_outputs:
-            host = torch.empty(batch.n_dec, dtype=torch.int32, pin_memory=True)
+            host = self._token_slots(batch.n_dec)
             host.copy_(out.dec_tokens, non_blocking=True)
             self.d2h_bytes += batch.n_dec * 4
             self._dec_out.append(([r.id for r in decodes], host))
