@@ -128,6 +128,9 @@ class HybridModel:
         self.vpad = (cfg.vocab + 7) // 8 * 8
         self.ws = torch.empty(16 << 20, dtype=torch.float32, device=self.dev)  # 64 MB split-K / reduction scratch
         self.tape: list | None = None   # when a list: every device-side call is appended (bench replay)
+        self._stage_ring: list = [(None, None)] * 8   # pinned staging buffers (+ the event of their last copy)
+        self._stage_dev: list = [None] * 8             # device scratch per staging slot
+        self._stage_i = 0
         self.instrument: list | None = None  # when a list: (ev0, ev1, bytes) per decode-attention launch
         self.gemm_instrument: list | None = None  # when a list: (ms, flops, launches) of the GEMMs of each tick
         self._attn_bytes = 0
@@ -442,21 +445,43 @@ class HybridModel:
             return
         if self.tape is not None:
             self.tape.append(("trim", slots.copy(), kept.copy()))
-        t_s = torch.from_numpy(np.ascontiguousarray(slots, np.int32)).pin_memory().to(self.dev, non_blocking=True)
-        t_k = torch.from_numpy(np.ascontiguousarray(kept, np.int32).reshape(-1)).pin_memory().to(self.dev, non_blocking=True)
-        self._keep = (t_s, t_k)  # keep alive until the stream consumes them
-        self._chk(self.ctx.L.mace_kv_trim(self.ctx.h, C.byref(self.kv), t_s.data_ptr(), t_k.data_ptr(), n, self._s),
-                  "kv_trim")
+        dev = self._stage((np.ascontiguousarray(slots, np.int32).reshape(-1),
+                           np.ascontiguousarray(kept, np.int32).reshape(-1)))
+        self._chk(self.ctx.L.mace_kv_trim(self.ctx.h, C.byref(self.kv), dev, dev + 4 * n, n, self._s), "kv_trim")
 
     def release_slots(self, slots: list[int]) -> None:
         if not slots:
             return
         if self.tape is not None:
             self.tape.append(("release", list(slots)))
-        t_s = torch.tensor(slots, dtype=torch.int32).pin_memory().to(self.dev, non_blocking=True)
-        self._keep_rel = t_s
-        self._chk(self.ctx.L.mace_kv_release(self.ctx.h, C.byref(self.kv), t_s.data_ptr(), len(slots), self._s),
-                  "kv_release")
+        dev = self._stage((np.asarray(slots, np.int32),))
+        self._chk(self.ctx.L.mace_kv_release(self.ctx.h, C.byref(self.kv), dev, len(slots), self._s), "kv_release")
+
+    def _stage(self, parts) -> int:
+        """Copy small int32 host arrays (concatenated) to a device scratch buffer, stream-ordered, through a
+        ring of pinned staging buffers; returns the device address. A staging buffer is reused only after
+        the copy that last read it has completed (its event)."""
+        n = sum(a.size for a in parts)
+        ring = self._stage_ring
+        i = self._stage_i = (self._stage_i + 1) % len(ring)
+        host, ev = ring[i]
+        if ev is not None:
+            ev.synchronize()  # recorded many calls ago: normally already complete
+        if host is None or host.numel() < n:
+            host = torch.empty(max(n, 1 << 14), dtype=torch.int32, pin_memory=True)
+        hv = host.numpy()
+        o = 0
+        for a in parts:
+            hv[o: o + a.size] = a
+            o += a.size
+        if self._stage_dev[i] is None or self._stage_dev[i].numel() < n:
+            self._stage_dev[i] = torch.empty(max(n, 1 << 14), dtype=torch.int32, device=self.dev)
+        d = self._stage_dev[i]
+        d[:n].copy_(host[:n], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        ring[i] = (host, ev)
+        return d.data_ptr()
 
     # ------------------------------------------------------------------ fine-tune update
     def apply_update(self, local_ft: bool) -> None:
