@@ -15,6 +15,10 @@ here without changing a single decision:
 * ``NormStream`` draws a request's head-norm jitter ``normal(1, 0.1)`` in blocks from the same Generator
   (seed ``[seed, 211, id]``); numpy's Generator fills an array with the same sequence as repeated
   ``size=num_heads`` calls, so the per-step values equal the reference's (checked in tests/test_host_cpu.py).
+* ``fast_schedule_iteration`` runs Alg. 1 (scheduler.py:133-188) natively (csrc/hostsched.cu) over the queue
+  head with precomputed estimates, with an inlined Python restatement for the iterations it hands back.
+* ``make_bulk_pair_losses`` restates the fine-tune loss chain (alignment.py:39-47, 151-166) for many requests
+  per refresh / push_many, value for value.
 """
 from __future__ import annotations
 

@@ -1,3 +1,5 @@
+"""e2e host time of C2 ticks on the GPU box, split into model.step, the native tick call and its kernel
+launches (MACE_HOST_PROF). Usage: python tools/e2e_native_split.py"""
 import os, sys, time, ctypes
 os.environ["MACE_HOST_PROF"] = "1"
 sys.path.insert(0, "/root/repo")
@@ -24,13 +26,6 @@ st = model.step
 def step(*a, **k):
     t = time.perf_counter(); r = st(*a, **k); acc["step"] += time.perf_counter() - t; return r
 model.step = step
-if os.environ.get("GC_MODE") == "freeze":
-    import gc
-    gc.collect()
-    gc.freeze()
-elif os.environ.get("GC_MODE") == "off":
-    import gc
-    gc.disable()
 hp = (ctypes.c_double * 4)()
 L.mace_debug_host_prof(hp)
 t0 = time.perf_counter()
