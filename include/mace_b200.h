@@ -120,6 +120,9 @@ int mace_embed(mace_ctx* ctx, const int* tokens, const int* pos, const int* last
                const void* pos_emb, int T, int d, float* x, void* stream);
 int mace_norm(mace_ctx* ctx, const float* x, int ldx, const int* rows, int n_rows, int d, const void* w,
               const void* b, int layernorm, float eps, void* out, int ldo, float* rstd_out, void* stream);
+/* mace_rope_kv resolves each row's KV page from the row / sequence / page tables before its PDL wait: those
+ * tables must not be written by either of the two kernels launched just before it on the stream (the tick
+ * writes them before its first layer). */
 int mace_rope_kv(mace_ctx* ctx, void* qkv, int T, int Hq, int Hkv, int hd, const int* row_pos, const int* row_seq,
                  const int* row_kvi, const MaceSeq* seqs, const float* cos_t, const float* sin_t, int apply_rope,
                  const MaceKvLayout* kv, void* k_pool, void* v_pool, void* stream);
