@@ -478,8 +478,9 @@ class HybridModel:
             self._stage_dev[i] = torch.empty(max(n, 1 << 14), dtype=torch.int32, device=self.dev)
         d = self._stage_dev[i]
         d[:n].copy_(host[:n], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
+        if ev is None:
+            ev = torch.cuda.Event()
+        ev.record()  # re-recorded only after its previous copy completed (synchronize above)
         ring[i] = (host, ev)
         return d.data_ptr()
 
