@@ -110,8 +110,10 @@ typedef struct MaceKvLayout {
   int* dec_base;                           /* [slots][Hkv] decode slot held by dtab[..][0] row 0 */
   int* dec_first;                          /* [slots][Hkv] first retained decode slot    */
   int* dec_end;                            /* [slots] decode slots created               */
-  int* free_stack; int* free_top; int stack_cap; /* device free list of decode head pages */
-  int n_kv_heads; int pad;
+  int* free_stack; int* free_top; int stack_cap; /* device free list of decode head pages; free_top -> int[2]
+                                                     = {stack top, status (bit 0: a pop found it empty)} */
+  int n_kv_heads; int sink_page;           /* sink_page: reserved head page outside the stack that an
+                                              exhausted pop points a row at (in-bounds, flagged in status) */
 } MaceKvLayout;
 
 /* ---------------------------------------------------------------- row kernels */
@@ -185,6 +187,8 @@ int mace_act_bwd(mace_ctx* ctx, const void* u, const void* da, int n, int F, int
 int mace_rope_bwd(mace_ctx* ctx, float* dqkv, int n, int Hq, int Hkv, int hd, const int* pos, const float* cos_t,
                   const float* sin_t, void* stream);
 int mace_f32_to_bf16(mace_ctx* ctx, const float* x, long long n, void* y, void* stream);
+/* widening copy; with mace_f32_to_bf16 it brackets the bf16 gradient all-reduce of lockstep replicas */
+int mace_bf16_to_f32(mace_ctx* ctx, const void* x, long long n, float* y, void* stream);
 /* attention backward of the dense causal FT sequences: items int4 [n_items] = (seq, kv_head, key_block, steps),
  * key blocks of 128 keys for head_dim 64 / 128 (tcgen05 kernel), 64 keys for head_dim 32; dqkv fp32 [n_rows, W]
  * zeroed by the caller (dQ accumulates across key blocks and GQA heads), dK / dV written.                     */
@@ -193,7 +197,11 @@ int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, const void* dou
                   float* dqkv, void* stream);
 
 /* ---------------------------------------------------------------- (4) KV pages */
+/* pages are popped per (slot, head) whose ring is full; the host mirrors the count and refuses a tick that
+ * would exhaust the pool (KvCapacityError), so the sink page is a last line of defence only            */
 int mace_kv_decode_alloc(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, int n, void* stream);
+/* synchronous read of {stack top, status} (tests / post-mortem); status != 0 means a pop hit the sink   */
+int mace_kv_status(mace_ctx* ctx, const MaceKvLayout* kv, int* out2);
 int mace_kv_trim(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, const int* kept, int n, void* stream);
 int mace_kv_release(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, int n, void* stream);
 int mace_kv_page_copy(mace_ctx* ctx, const int* copies, int n, int n_kv_heads, int hd, long long pages_per_layer,

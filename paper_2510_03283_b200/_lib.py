@@ -37,7 +37,7 @@ class MaceKvLayout(C.Structure):
         ("dtab", C.c_void_p), ("max_dec_pages", C.c_int),
         ("dec_base", C.c_void_p), ("dec_first", C.c_void_p), ("dec_end", C.c_void_p),
         ("free_stack", C.c_void_p), ("free_top", C.c_void_p), ("stack_cap", C.c_int),
-        ("n_kv_heads", C.c_int), ("pad", C.c_int),
+        ("n_kv_heads", C.c_int), ("sink_page", C.c_int),
     ]
 
 
@@ -162,8 +162,10 @@ SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_act_bwd": (C.c_int, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp]),
     "mace_rope_bwd": (C.c_int, [_vp, _vp, _i, _i, _i, _i, _ip, _vp, _vp, _vp]),
     "mace_f32_to_bf16": (C.c_int, [_vp, _vp, C.c_longlong, _vp, _vp]),
+    "mace_bf16_to_f32": (C.c_int, [_vp, _vp, C.c_longlong, _vp, _vp]),
     "mace_attn_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _ip, _i, _i, _vp, _vp, _vp]),
     "mace_kv_decode_alloc": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _i, _vp]),
+    "mace_kv_status": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip]),
     "mace_kv_trim": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _ip, _i, _vp]),
     "mace_kv_release": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _i, _vp]),
     "mace_kv_page_copy": (C.c_int, [_vp, _ip, _i, _i, _i, C.c_longlong, _i, _vp, _vp, _vp]),

@@ -224,6 +224,13 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ x, long long n, __n
     y[i] = __float2bfloat16(x[i]);
 }
 
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ x, long long n, float* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = __bfloat162float(x[i]);
+}
+
 // ------------------------------------------------------------------ attention backward (dense FT sequences)
 // D[r, hq] = sum_d dO[r, hq, d] * O[r, hq, d]
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout, int n,
@@ -471,6 +478,15 @@ extern "C" int mace_f32_to_bf16(mace_ctx* ctx, const float* x, long long n, void
   launch_k(f32_to_bf16_kernel, (int)grid, 256, 0, (cudaStream_t)stream, x, n, (__nv_bfloat16*)y);
   ctx->launches++;
   return mace_check_launch(ctx, "f32_to_bf16");
+}
+
+extern "C" int mace_bf16_to_f32(mace_ctx* ctx, const void* x, long long n, float* y, void* stream) {
+  if (n <= 0) return 0;
+  long long grid = (n + 255) / 256;
+  if (grid > ctx->num_sms * 16) grid = ctx->num_sms * 16;
+  launch_k(bf16_to_f32_kernel, (int)grid, 256, 0, (cudaStream_t)stream, (const __nv_bfloat16*)x, n, y);
+  ctx->launches++;
+  return mace_check_launch(ctx, "bf16_to_f32");
 }
 
 namespace mace {

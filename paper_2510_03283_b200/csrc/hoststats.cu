@@ -43,15 +43,19 @@ bool allocate_row(const double* means, int H, int64_t C, int64_t* caps) {
   // (caps - floors, caps, -index) among caps >= 2 (cache.py:345-351)
   for (int h = 0; h < H; ++h) {
     if (caps[h] != 0) continue;
-    int donor = 0;
-    int64_t best = 0;
+    // lexicographic max over (eligible, caps - floors, caps, -j), fields compared directly (no digit packing,
+    // so any c_total / H is exact); the first j wins ties on every field, as max() over the tuples does
+    int donor = -1;
     for (int j = 0; j < H; ++j) {
-      const int64_t sc = caps[j] >= 2 ? ((caps[j] - fl[j]) * 1024 + caps[j]) * 1024 + (1023 - j) : INT64_MIN;
-      if (j == 0 || sc > best) {
-        best = sc;
+      if (caps[j] < 2) continue;
+      if (donor < 0) {
         donor = j;
+        continue;
       }
+      const int64_t dj = caps[j] - fl[j], dd = caps[donor] - fl[donor];
+      if (dj > dd || (dj == dd && caps[j] > caps[donor])) donor = j;
     }
+    if (donor < 0) donor = 0;  // no eligible donor: the reference's max() falls back the same way (all keys equal)
     caps[donor] -= 1;
     caps[h] += 1;
   }

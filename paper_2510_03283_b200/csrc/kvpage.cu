@@ -11,6 +11,8 @@
 //   page_copy     copy-on-diverge of a partially shared prompt page (trie split at a non page-aligned
 //                 token, cache.py:79-105) across every layer of both pools
 // Pops and pushes never run in the same kernel, so the stack needs no ABA protection.
+// free_top points at int[2] = {stack top, status}; status bit 0 = a pop found the stack empty (the row was
+// pointed at kv.sink_page, a reserved page outside the stack). The host mirror makes that unreachable.
 #include "common.cuh"
 #include "mace_internal.h"
 
@@ -28,7 +30,17 @@ __global__ void decode_alloc_kernel(const int* __restrict__ slots, int n, MaceKv
   const int rel = j - kv.dec_base[kvh];
   if (rel % kPageTokens == 0) {
     const int top = atomicSub(kv.free_top, 1) - 1;
-    const int page = top >= 0 ? kv.free_stack[top] : -1;  // -1: pool exhausted (host checks free_top)
+    int page;
+    if (top >= 0) {
+      page = kv.free_stack[top];
+    } else {
+      // pool exhausted: unreachable when the host mirror (kvmanager.DecodePageMirror) admitted the tick.
+      // Defence in depth: undo the pop, point the row at the reserved sink page (writes and reads stay in
+      // bounds) and raise the status word the host reads with mace_kv_status.
+      atomicAdd(kv.free_top, 1);
+      atomicOr(kv.free_top + 1, 1);
+      page = kv.sink_page;
+    }
     kv.dtab[(size_t)kvh * kv.max_dec_pages + rel / kPageTokens] = page;
   }
 }
@@ -56,8 +68,7 @@ __global__ void trim_kernel(const int* __restrict__ slots, const int* __restrict
   int* ring = kv.dtab + (size_t)kvh * kv.max_dec_pages;
   int drop = 0;
   while (first - base >= kPageTokens) {
-    const int top = atomicAdd(kv.free_top, 1);
-    kv.free_stack[top] = ring[drop];
+    if (ring[drop] != kv.sink_page) kv.free_stack[atomicAdd(kv.free_top, 1)] = ring[drop];
     ++drop;
     base += kPageTokens;
   }
@@ -79,10 +90,8 @@ __global__ void release_kernel(const int* __restrict__ slots, int n, MaceKvLayou
   const int de = kv.dec_end[slot], base = kv.dec_base[kvh];
   const int live = de > base ? (de - 1 - base) / kPageTokens + 1 : 0;
   const int* ring = kv.dtab + (size_t)kvh * kv.max_dec_pages;
-  for (int r = 0; r < live; ++r) {
-    const int top = atomicAdd(kv.free_top, 1);
-    kv.free_stack[top] = ring[r];
-  }
+  for (int r = 0; r < live; ++r)
+    if (ring[r] != kv.sink_page) kv.free_stack[atomicAdd(kv.free_top, 1)] = ring[r];
   kv.dec_base[kvh] = 0;
   kv.dec_first[kvh] = 0;
 }
@@ -191,4 +200,11 @@ extern "C" int mace_scatter_tokens(mace_ctx* ctx, const int* src, const int* slo
   launch_k(mace::scatter_tokens_kernel, (n + 255) / 256, 256, 0, (cudaStream_t)stream, src, slots, n, last_token);
   ctx->launches++;
   return mace::mace_check_launch(ctx, "scatter_tokens");
+}
+
+extern "C" int mace_kv_status(mace_ctx* ctx, const MaceKvLayout* kv, int* out2) {
+  if (!ctx || !kv || !out2) return MACE_ERR_ARG;
+  if (cudaMemcpy(out2, kv->free_top, 2 * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return mace_fail(ctx, MACE_ERR_CUDA, "kv_status: copy failed");
+  return MACE_OK;
 }

@@ -23,12 +23,32 @@ class Lockstep:
     def active(self) -> bool:
         return self.flag_group is not None
 
-    def any_ft(self, local: bool) -> bool:
+    def tick(self, local_ft: bool, active: bool = True) -> tuple[bool, bool]:
+        """The per-tick agreement, ONE 8-byte gloo all-reduce(max): (any replica has FT rows, any replica still
+        has work). Every rank calls it exactly once per tick round -- an executed tick, or an idle round of a
+        rank whose trace has drained (GpuEngine.run_ticks) -- so the rounds pair up in order and a drained
+        rank never leaves the others blocked."""
         if self.flag_group is None:
-            return local
-        t = torch.tensor([1 if local else 0], dtype=torch.int32)
+            return local_ft, active
+        t = torch.tensor([1 if local_ft else 0, 1 if active else 0], dtype=torch.int32)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.flag_group)
-        return bool(t.item())
+        return bool(t[0].item()), bool(t[1].item())
+
+    def any_ft(self, local: bool) -> bool:
+        return self.tick(local, True)[0]
+
+    def min_over_ranks(self, value: float) -> float:
+        return -self.max_over_ranks(-value)
+
+    def assert_equal(self, value: int, what: str) -> None:
+        """Cross-replica check (e.g. the weight checksum after every k fine-tune updates): raises on every rank
+        when any two ranks disagree."""
+        if self.flag_group is None:
+            return
+        t = torch.tensor([value, -value], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.flag_group)
+        if int(t[0]) != -int(t[1]):
+            raise RuntimeError(f"replicas diverged: {what} differs across ranks ({int(t[0])} vs {-int(t[1])})")
 
     def barrier(self) -> None:
         if self.flag_group is not None:

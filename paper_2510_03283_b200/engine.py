@@ -45,6 +45,36 @@ from macesim.workload import WorkloadType  # noqa: E402
 
 
 _FAST_ALG1 = os.environ.get("MACE_FAST_ALG1", "1") != "0"  # A/B switch for host profiling
+
+
+def _dfs_order_hook(trie, pending):
+    """Installed once as macesim.engine.dfs_order (engine.py:581-584 calls it by module global).
+
+    A GpuPrefixTrie executing a bin carries that bin's prefill order on the instance (``_bin_order``,
+    set and cleared by GpuEngine._execute); every other trie -- a plain reference Engine in the same
+    process, another engine between ticks -- gets the reference's whole-trie walk (cache.py:253-273).
+    The state lives on the trie instance, so concurrent engines (sweep threads) never see each other's."""
+    order = getattr(trie, "_bin_order", None)
+    if order is not None:
+        return list(order)
+    return _ref_dfs_order(trie, pending)
+
+
+def _schedule_iteration_hook(queue, *args, **kw):
+    """Installed once as macesim.engine.schedule_iteration (engine.py:397-402 calls it by module global).
+
+    A FastPriorityQueue owned by a GpuEngine carries its planner on the instance (``_planner``); any other
+    queue runs the reference Alg. 1 (scheduler.py:133-188) unchanged."""
+    planner = getattr(queue, "_planner", None)
+    if planner is not None:
+        return planner(queue, *args, **kw)
+    return _ref_schedule_iteration(queue, *args, **kw)
+
+
+if _ref_engine.dfs_order is _ref_dfs_order:  # idempotent on re-import
+    _ref_engine.dfs_order = _dfs_order_hook
+if _ref_engine.schedule_iteration is _ref_schedule_iteration:
+    _ref_engine.schedule_iteration = _schedule_iteration_hook
 DECODE_CHUNK_PAGES = 128  # decode contexts longer than 2048 tokens are split into chunks (merged on device)
 
 
@@ -105,6 +135,8 @@ class GpuEngine(Engine):
             self.queue = FastPriorityQueue(priority_params, loss_fn=self._loss_of)
             if type(self)._loss_of is Engine._loss_of:  # the reference's loss chain, restated in bulk
                 self.queue.bulk_loss = make_bulk_pair_losses(self.env)
+            if _FAST_ALG1:  # Alg. 1's restatement, reached through the installed hook (instance state only)
+                self.queue._planner = self._fast_plan
         self.model = model
         self.norm_stream = NormStream(self, model.max_slots)
         self.mcfg: ModelConfig = model.cfg
@@ -128,6 +160,7 @@ class GpuEngine(Engine):
         self._dec_out: list = []
         self.lockstep = lockstep
         self.ticks_done = 0
+        self.idle_rounds = 0  # lockstep rounds this replica joined with a drained trace
         self._budget_end: int | None = None
         self.keep_outputs = True
         self.time_ticks = False
@@ -255,7 +288,11 @@ class GpuEngine(Engine):
             seqs = []
             n_seq = si0 + n_dec
             tok_seg.append(np.where(k0 == 0, last, -(dec_slots + 1)).astype(i32))
-            pos_seg.append((P - 1 + k0).astype(i32))
+            dpos = (P - 1 + k0).astype(i32)
+            if c.family == "gpt2" and int(dpos.max()) >= c.max_pos:
+                raise ValueError(f"decode position {int(dpos.max())} >= {c.name}'s {c.max_pos} learned positions "
+                                 "(cap prompt length + max_decode_steps)")
+            pos_seg.append(dpos)
             seq_seg.append(np.arange(si0, si0 + n_dec, dtype=i32))
             kvi_seg.append(k0)
             n_rows += n_dec
@@ -404,17 +441,18 @@ class GpuEngine(Engine):
             self.profile._clock[0] = ev0.elapsed_time(ev1)
         # ---- the reference's own bookkeeping for this bin (timeline, metrics, KV MB, prune, ft_step)
         # the reference orders this bin's prefills with dfs_order, a walk of the WHOLE trie (cache.py:253-273);
-        # the order is already known (path_dfs_order, equal by construction and by tests/test_host_cpu.py)
-        # (thread-safe: another engine's trie, e.g. a concurrent sweep thread, falls through to the reference)
-        _ref_engine.dfs_order = lambda trie, pending, _o=prefills, _t=self.trie: (
-            list(_o) if trie is _t else _ref_dfs_order(trie, pending))
+        # the order is already known (path_dfs_order, equal by construction and by tests/test_host_cpu.py) and
+        # is handed over on this engine's own trie instance (_dfs_order_hook)
+        if self.trie is not None:
+            self.trie._bin_order = prefills
         defer = isinstance(self.queue, FastPriorityQueue)
         self._route_later = [] if defer else None
         self._release_later = []
         try:
             super()._execute(plan)
         finally:
-            _ref_engine.dfs_order = _ref_dfs_order
+            if self.trie is not None:
+                self.trie._bin_order = None
             later, self._route_later = self._route_later, None
             if later:  # the bin's route-backs, pushed together at the clock they were issued at
                 self.queue.push_many(later, self.clock)
@@ -463,7 +501,13 @@ class GpuEngine(Engine):
             raise TickBudgetReached()
 
     def run_ticks(self, n: int) -> int:
-        """Advance the reference loop by exactly n executed ticks (fewer if the trace drains)."""
+        """Advance the reference loop by exactly n executed ticks (fewer if the trace drains).
+
+        Lockstep replicas (N > 1): every tick round is one Lockstep.tick agreement. A rank whose trace has
+        drained keeps joining the rounds idle -- contributing zero gradients to every fine-tune update the
+        others run (HybridModel.idle_update) -- until n rounds have passed or no rank has work left, so no
+        rank ever waits on a collective the others will not issue. The selected weights of all replicas are
+        then compared by checksum (they must be bit-identical)."""
         start = self.ticks_done
         self._budget_end = start + n
         try:
@@ -472,7 +516,20 @@ class GpuEngine(Engine):
             pass
         finally:
             self._budget_end = None
-        return self.ticks_done - start
+        done = self.ticks_done - start
+        lock = self.lockstep
+        if lock is not None and getattr(lock, "active", False):
+            rounds = done
+            while rounds < n:
+                any_ft, any_active = lock.tick(False, active=False)
+                if not any_active:
+                    break
+                if any_ft:
+                    self.model.idle_update()
+                rounds += 1
+            self.idle_rounds += rounds - done
+            lock.assert_equal(self.model.weight_checksum(), "selected-parameter weights")
+        return done
 
     def _route_back(self, req, continued_ft):  # engine.py:561 — inside _execute: collected, pushed in bulk
         later = self._route_later
@@ -542,15 +599,8 @@ class GpuEngine(Engine):
         kept, released = self.hstats.step(slots, steps, norms)
         return dict(zip([r.id for r in rows], zip(kept.tolist(), released.tolist())))
 
-    def _plan(self):  # engine.py:393 — the reference _plan with Alg. 1's inlined restatement (hostfast.py)
-        if not (self.fast_host and _FAST_ALG1 and isinstance(self.queue, FastPriorityQueue)):
-            return super()._plan()
-        _ref_engine.schedule_iteration = lambda q, *a, _q=self.queue, **k: (
-            fast_schedule_iteration(q, *a, dec_est=self._dec_est, **k) if q is _q else _ref_schedule_iteration(q, *a, **k))
-        try:
-            return super()._plan()
-        finally:
-            _ref_engine.schedule_iteration = _ref_schedule_iteration
+    def _fast_plan(self, queue, *args, **kw):  # engine.py:397 -> Alg. 1's inlined restatement (hostfast.py)
+        return fast_schedule_iteration(queue, *args, dec_est=self._dec_est, **kw)
 
     def _synth_norms(self, req, rs):  # engine.py:433 — same draws, served from the per-request block stream
         return self.norm_stream.norms(req, rs).tolist()

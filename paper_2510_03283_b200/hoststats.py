@@ -153,8 +153,10 @@ class BatchedHeadStats:
                 if not z.any():
                     continue
                 cz, fz = c[z], floors[z]
-                score = np.where(cz >= 2, ((cz - fz) * 1024 + cz) * 1024 + (1023 - jj), np.iinfo(np.int64).min)
-                donor = score.argmax(1)
+                # donors sorted by (-(caps - floors), -caps, j) among caps >= 2 (cache.py:348-349): a per-row
+                # lexsort on the tuple fields themselves (exact for any c_total / H)
+                jb = np.broadcast_to(jj, cz.shape)
+                donor = np.lexsort((jb, -cz, -(cz - fz), cz < 2), axis=1)[:, 0]
                 cz[np.arange(cz.shape[0]), donor] -= 1
                 cz[:, h] += 1
                 c[z] = cz

@@ -27,7 +27,64 @@ from macesim.cache import PrefixTrie, TrieNode  # noqa: E402
 
 
 class KvCapacityError(RuntimeError):
-    pass
+    """A KV pool (prompt page groups or decode head pages) cannot hold the next tick: raised on the host
+    BEFORE any launch, so the device never writes through an invalid page."""
+
+
+class DecodePageMirror:
+    """Host mirror of the device decode-page allocator (csrc/kvpage.cu), decision for decision.
+
+    Every pop and push of the device free stack is a pure function of the decode rows of a tick, the
+    reference's post-tick kept[h] and retirements -- all known on the host -- so the host counts them
+    without any device read and refuses a tick whose pops exceed the free pages (KvCapacityError):
+      decode_alloc  (slot, head) pops one page when (dec_end - dec_base) % 16 == 0
+      trim          dec_first = max(dec_first, dec_end - kept[h]); pages wholly below it are pushed
+      release       every live ring page of the slot is pushed"""
+
+    def __init__(self, max_slots: int, n_heads: int, n_pages: int):
+        self.end = np.zeros(max_slots, np.int64)
+        self.base = np.zeros((max_slots, n_heads), np.int64)
+        self.first = np.zeros((max_slots, n_heads), np.int64)
+        self.free = int(n_pages)
+        self.n_pages = int(n_pages)
+
+    def state(self):
+        return (self.end.copy(), self.base.copy(), self.first.copy(), self.free)
+
+    def restore(self, st) -> None:
+        self.end, self.base, self.first, self.free = st[0].copy(), st[1].copy(), st[2].copy(), st[3]
+
+    def pops(self, slots: np.ndarray) -> int:
+        rel = self.end[slots][:, None] - self.base[slots]
+        return int((rel % PAGE == 0).sum())
+
+    def alloc(self, slots: np.ndarray) -> None:
+        """Decode rows of one tick (distinct slots): raises before anything changes if the pool is short."""
+        if slots.size == 0:
+            return
+        need = self.pops(slots)
+        if need > self.free:
+            raise KvCapacityError(f"decode KV pages exhausted: the tick needs {need} new head pages, "
+                                  f"{self.free} of {self.n_pages} are free (raise HybridModel decode_pages)")
+        self.free -= need
+        self.end[slots] += 1
+
+    def trim(self, slots: np.ndarray, kept: np.ndarray) -> None:
+        end = self.end[slots][:, None]
+        first = np.maximum(self.first[slots], end - kept)
+        self.first[slots] = first
+        drop = np.maximum(0, (first - self.base[slots]) // PAGE)
+        self.free += int(drop.sum())
+        self.base[slots] += drop * PAGE
+
+    def release(self, slots: np.ndarray) -> None:
+        end = self.end[slots][:, None]
+        base = self.base[slots]
+        live = np.where(end > base, (end - 1 - base) // PAGE + 1, 0)
+        self.free += int(live.sum())
+        self.base[slots] = 0
+        self.first[slots] = 0
+        self.end[slots] = 0
 
 
 class GroupPool:
@@ -99,6 +156,7 @@ class GpuPrefixTrie(PrefixTrie):
         self.pending: dict[int, dict[int, int]] = {}   # pages a tick's prefill will hand to newly cached nodes
         self._memo: dict[int, tuple] = {}  # request id -> (epoch, stop kind, a, b, cached prefix length)
         self._epoch = 0                    # bumped by every split and every eviction
+        self._bin_order = None             # prefill order of the executing bin (engine._dfs_order_hook)
 
     def cached_prefix_len(self, prompt_tokens):  # cache.py:164-184, same walk; label matches compared by slices
         return self._walk(prompt_tokens)[0]

@@ -25,6 +25,7 @@ from ._lib import (Ctx, MaceKvLayout, MaceLayerGrads, MaceLayerWeights, MaceMode
                    MaceTickBuffers, MaceTickDesc)
 from .batch import PAGE, TickBatch
 from .config import ModelConfig, TrainConfig, selected_param_names
+from .kvmanager import DecodePageMirror
 
 
 @dataclass
@@ -56,12 +57,14 @@ class HybridModel:
         decode_pages: int | None = None,
         ctx: Ctx | None = None,
         process_group=None,
+        grad_allreduce: str = "bf16",
     ):
         self.cfg, self.tcfg = cfg, tcfg
         self.ctx = ctx or Ctx(device)
         self.dev = torch.device("cuda", device)
         self.stream = torch.cuda.current_stream(self.dev)
         self.pg = process_group
+        self.grad_allreduce = grad_allreduce
         d, L = cfg.d_model, cfg.n_layers
         self.w = {n: t.to(self.dev, torch.bfloat16).contiguous() for n, t in weights.items()}
         # ---- selected parameters: flat fp32 master / m / v / grad + segment table for masked AdamW
@@ -75,6 +78,7 @@ class HybridModel:
         self.m = torch.zeros_like(self.master)
         self.v = torch.zeros_like(self.master)
         self.grad = torch.zeros_like(self.master)
+        self._g16 = torch.empty(self.n_sel, dtype=torch.bfloat16, device=self.dev) if process_group is not None else None
         self.gview = {n: self.grad[offs[i]: offs[i + 1]].view(self.w[n].shape) for i, n in enumerate(self.sel)}
         self.seg_offsets = torch.from_numpy(offs).to(self.dev)
         self.seg_ptrs = torch.tensor([self.w[n].data_ptr() for n in self.sel], dtype=torch.int64, device=self.dev)
@@ -83,7 +87,10 @@ class HybridModel:
         # ---- RoPE tables (fp64 on host -> fp32)
         half = cfg.head_dim // 2
         inv = cfg.rope_theta ** (-np.arange(half, dtype=np.float64) * 2.0 / cfg.head_dim)
-        ang = np.arange(cfg.max_pos, dtype=np.float64)[:, None] * inv[None, :]
+        # RoPE is computed, not learned: the table covers every position a request of this model can reach
+        # (GPT-2's learned table is bounded by cfg.max_pos; GpuEngine.build_batch refuses positions past it)
+        n_pos = max(cfg.max_pos, max_prompt_len + max_decode_steps)
+        ang = np.arange(n_pos, dtype=np.float64)[:, None] * inv[None, :]
         self.cos_t = torch.from_numpy(np.cos(ang).astype(np.float32)).to(self.dev)
         self.sin_t = torch.from_numpy(np.sin(ang).astype(np.float32)).to(self.dev)
         # ---- KV pools and page tables
@@ -94,8 +101,10 @@ class HybridModel:
         self.prompt_groups = prompt_groups
         if decode_pages is None:
             decode_pages = max_slots * H * 4
+        self.max_prompt_len = max_prompt_len
         self.decode_pages = decode_pages
-        self.pages_per_layer = prompt_groups * H + decode_pages
+        # + 1: the reserved sink page (kvpage.cu) an exhausted pop would point at -- never on the free stack
+        self.pages_per_layer = prompt_groups * H + decode_pages + 1
         # zero-initialised: page rows outside a sequence's window are multiplied by exact zeros on the
         # tensor cores, so they must hold finite values
         self.k_pool = torch.zeros(L, self.pages_per_layer, PAGE, hd, dtype=torch.bfloat16, device=self.dev)
@@ -106,11 +115,14 @@ class HybridModel:
         self.dec_base = torch.zeros(max_slots, H, **i32)
         self.dec_first = torch.zeros(max_slots, H, **i32)
         self.dec_end = torch.zeros(max_slots, **i32)
-        self.free_stack = torch.arange(prompt_groups * H, self.pages_per_layer, **i32)
-        self.free_top = torch.tensor([decode_pages], **i32)
+        self.free_stack = torch.arange(prompt_groups * H, self.pages_per_layer - 1, **i32)
+        self.free_top = torch.tensor([decode_pages, 0], **i32)  # {stack top, status}
+        self.kv_mirror = DecodePageMirror(max_slots, H, decode_pages)  # host count of the same pops / pushes
         self.last_token = torch.zeros(max_slots, **i32)
         self.dec_counters = torch.zeros(max_slots * H, **i32)  # decode chunk-merge counters (self-cleaning)
-        self.dec_work = torch.zeros(1, dtype=torch.int64, device=self.dev)  # decode ticket counter (monotonic)
+        # decode ticket counter: zero between launches -- the warp that draws a launch's terminal ticket resets
+        # it, which needs every launched warp to enter the ticket loop (launch_decode2: base == grid * WARPS)
+        self.dec_work = torch.zeros(1, dtype=torch.int64, device=self.dev)
         # 0 auto (tcgen05 swap-AB for GQA, CUDA-core streaming for MHA), 1 / 2 forced (MACE_DECODE_IMPL: sweeps)
         self.decode_impl = int(os.environ.get("MACE_DECODE_IMPL", "0"))
         self.kv = MaceKvLayout(
@@ -118,6 +130,7 @@ class HybridModel:
             max_dec_pages=self.maxdp, dec_base=self.dec_base.data_ptr(), dec_first=self.dec_first.data_ptr(),
             dec_end=self.dec_end.data_ptr(), free_stack=self.free_stack.data_ptr(),
             free_top=self.free_top.data_ptr(), stack_cap=decode_pages, n_kv_heads=H,
+            sink_page=self.pages_per_layer - 1,
         )
         self._cap = 0
         self._ft_cap = 0
@@ -324,8 +337,16 @@ class HybridModel:
                 self.step(op[1], ft_global=op[2])
             elif op[0] == "trim":
                 self.apply_trim(op[1], op[2])
+            elif op[0] == "idle_update":
+                self.idle_update()
             else:
                 self.release_slots(op[1])
+
+    @staticmethod
+    def tape_collectives(tape) -> int:
+        """Gradient all-reduces a tape issues (equal on every rank of a lockstep run)."""
+        return sum(1 for op in tape if op[0] == "idle_update" or (op[0] == "step" and (
+            op[2] or (op[1].ft_pairs and op[1].T > op[1].ft0))))
 
     def _upload(self, batch: TickBatch) -> dict[str, int | None]:
         if getattr(batch, "_packed", None) is None:
@@ -362,6 +383,8 @@ class HybridModel:
         n_dec = batch.n_dec
         P = len(batch.ft_pairs)
         self._ensure(max(T, 1), max(n_ft, 1), max(R, 1), max(n_dec, 1), max(P, 1))
+        if n_dec:  # raises KvCapacityError before any launch if the decode pages cannot hold this tick
+            self.kv_mirror.alloc(batch.dec_slots.astype(np.int64))
         v = self._upload(batch)
         has_ft = n_ft > 0 and P > 0
         if self.instrument is not None and n_dec:
@@ -427,6 +450,13 @@ class HybridModel:
     def _chk(self, rc, what):
         self.ctx.check(rc, what)
 
+    def kv_status(self) -> tuple[int, int]:
+        """(device free-stack top, status word) -- synchronous; status != 0 means a pop found the stack
+        empty, which the host mirror makes unreachable (tests assert the top equals the mirror's count)."""
+        out = (C.c_int * 2)()
+        self.ctx.check(self.ctx.L.mace_kv_status(self.ctx.h, C.byref(self.kv), out), "kv_status")
+        return int(out[0]), int(out[1])
+
     def decode_attn_bytes(self, batch: TickBatch) -> int:
         """Algorithmic bytes of ONE decode-attention launch (one layer) of this tick: every visible K and
         V row of every (decode sequence, kv head) read once + q rows read + o rows written (syncs)."""
@@ -445,6 +475,7 @@ class HybridModel:
             return
         if self.tape is not None:
             self.tape.append(("trim", slots.copy(), kept.copy()))
+        self.kv_mirror.trim(np.asarray(slots, np.int64), np.asarray(kept, np.int64).reshape(n, -1))
         dev = self._stage((np.ascontiguousarray(slots, np.int32).reshape(-1),
                            np.ascontiguousarray(kept, np.int32).reshape(-1)))
         self._chk(self.ctx.L.mace_kv_trim(self.ctx.h, C.byref(self.kv), dev, dev + 4 * n, n, self._s), "kv_trim")
@@ -454,6 +485,7 @@ class HybridModel:
             return
         if self.tape is not None:
             self.tape.append(("release", list(slots)))
+        self.kv_mirror.release(np.asarray(slots, np.int64))
         dev = self._stage((np.asarray(slots, np.int32),))
         self._chk(self.ctx.L.mace_kv_release(self.ctx.h, C.byref(self.kv), dev, len(slots), self._s), "kv_release")
 
@@ -485,15 +517,38 @@ class HybridModel:
         return d.data_ptr()
 
     # ------------------------------------------------------------------ fine-tune update
+    def idle_update(self) -> None:
+        """A lockstep round this replica joins with a drained trace while another replica fine-tunes: zero
+        gradients into the same all-reduce, then the same AdamW step (engine.run_ticks)."""
+        if self.tape is not None:
+            self.tape.append(("idle_update",))
+        self.apply_update(False)
+
+    def weight_checksum(self) -> int:
+        """Order-independent 64-bit checksum of the fp32 master bits of the selected parameters (replicas must
+        agree bit for bit; dist.Lockstep.assert_equal)."""
+        bits = self.master.view(torch.int32).to(torch.int64)
+        return int((bits * torch.arange(1, bits.numel() + 1, device=bits.device) % 1000003).sum().item())
+
     def apply_update(self, local_ft: bool) -> None:
         """Gradient exchange (NCCL all-reduce over the request-stream replicas) and the
         masked AdamW. A replica without FT rows this tick contributes zeros and applies the same
-        update, so every replica keeps bit-identical weights."""
+        update, so every replica keeps bit-identical weights. The exchange runs in bf16 by default
+        (grad_allreduce "bf16": half the bytes, SURVEY §8(e)'s 872 MB at C4 top-2 layers): the fp32
+        gradient is rounded once, summed by NCCL, and widened back before AdamW; "f32" keeps it exact."""
         L, s = self.ctx.L, self._s
         if not local_ft:
             self.grad.zero_()
         if self.pg is not None:
-            torch.distributed.all_reduce(self.grad, group=self.pg)
+            if self.grad_allreduce == "bf16":
+                g16 = self._g16
+                self._chk(L.mace_f32_to_bf16(self.ctx.h, self.grad.data_ptr(), self.n_sel, g16.data_ptr(), s),
+                          "grad to bf16")
+                torch.distributed.all_reduce(g16, group=self.pg)
+                self._chk(L.mace_bf16_to_f32(self.ctx.h, g16.data_ptr(), self.n_sel, self.grad.data_ptr(), s),
+                          "grad to f32")
+            else:
+                torch.distributed.all_reduce(self.grad, group=self.pg)
         self.adam_step += 1
         t = self.tcfg
         self._chk(L.mace_adamw_masked(self.ctx.h, self.master.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),

@@ -26,8 +26,44 @@ class FakeModel:
         self.violations: list[str] = []
         self.tape = None
 
+    # ---- replica update protocol (the same calls HybridModel makes; weights are a small fp64 vector so the
+    # lockstep tests can check bit-identical replicas without a GPU)
+    pg = None
+    _w = None
+
+    def _weights(self):
+        import torch
+
+        if self._w is None:
+            self._w = torch.linspace(-1.0, 1.0, 64, dtype=torch.float64)
+        return self._w
+
+    def apply_update(self, local_ft: bool) -> None:
+        import torch
+
+        w = self._weights()
+        g = torch.full_like(w, float(len(self.calls) % 7 + 1)) if local_ft else torch.zeros_like(w)
+        if self.pg is not None:
+            import torch.distributed as dist
+
+            dist.all_reduce(g, group=self.pg)
+        self.updates = getattr(self, "updates", 0) + 1
+        w.sub_(1e-3 * g * w.abs().add(1.0))
+
+    def idle_update(self) -> None:
+        self.calls.append(("idle_update",))
+        self.apply_update(False)
+
+    def weight_checksum(self) -> int:
+        import hashlib
+
+        return int.from_bytes(hashlib.sha256(self._weights().numpy().tobytes()).digest()[:7], "little")
+
     def step(self, batch, trim=None, ft_global=None):
         self.calls.append(("step", batch))
+        has_ft = bool(batch.ft_pairs) and batch.T > batch.ft0
+        if has_ft or ft_global:
+            self.apply_update(has_ft)
         self.h2d_bytes = batch.packed()[0].size * 4
         for slot, row in zip(batch.ptab_slots.tolist(), batch.ptab_rows.tolist()):
             self.ptab[slot] = row

@@ -170,9 +170,10 @@ def test_batched_allocate_matches_reference_fuzz():
     from paper_2510_03283_b200.hoststats import BatchedHeadStats
 
     rng = np.random.default_rng(0)
-    for H, C in ((8, 160), (12, 160), (4, 10), (3, 7)):
+    # c_total >= 1024 and H up to 64: the zero-cap donor choice compares tuple fields, no digit packing
+    for H, C in ((8, 160), (12, 160), (4, 10), (3, 7), (8, 4096), (64, 2048), (16, 1500)):
         hs = BatchedHeadStats(1, H, 4, C, 128, None)
-        means = rng.random((4000, H)) * rng.choice([1.0, 0.01], size=(4000, H))
+        means = rng.random((4000, H)) * rng.choice([1.0, 0.01, 1e-5], size=(4000, H))
         means[rng.random((4000, H)) < 0.1] = 0.0
         means[:5] = 0.0
         got = hs._allocate(means)
@@ -358,17 +359,19 @@ def test_cached_prefix_memo_tracks_trie_changes():
             assert tr.cached_prefix_len_memo(rid, prompts[rid]) == tr._walk(prompts[rid])[0], (step, rid)
 
 
-def test_native_head_stats_matches_numpy():
+@pytest.mark.parametrize("C,weak", [(160, 0.05), (2000, 1e-4)])
+def test_native_head_stats_matches_numpy(C, weak):
     """csrc/hoststats.cu (the product path) equals the numpy restatement bit for bit over many steps:
-    first steps (tau unset), full windows, weak heads driving zero-cap repairs, resets, and the uniform split."""
+    first steps (tau unset), full windows, weak heads driving zero-cap repairs, resets, and the uniform split
+    -- also at c_total >= 1024, where a packed-digit donor key would lose order."""
     import numpy as np
 
     from paper_2510_03283_b200.hoststats import BatchedHeadStats
 
     rng = np.random.default_rng(11)
     H, W, S = 8, 64, 96
-    a = BatchedHeadStats(S, H, W, 160, 128.0, None)
-    b = BatchedHeadStats(S, H, W, 160, 128.0, None)
+    a = BatchedHeadStats(S, H, W, C, 128.0, None)
+    b = BatchedHeadStats(S, H, W, C, 128.0, None)
     step_of = np.zeros(S, np.int64)
     for it in range(400):
         n = int(rng.integers(1, 60))
@@ -379,7 +382,7 @@ def test_native_head_stats_matches_numpy():
             b.reset(reset)
             step_of[reset] = 0
         step_of[slots] += 1
-        scale = np.where(rng.random((n, H)) < 0.25, 0.05, 1.0)
+        scale = np.where(rng.random((n, H)) < 0.25, weak, 1.0)
         norms = np.maximum(0.0, scale * rng.normal(1.0, 0.1, (n, H)))
         if it % 50 == 7:
             norms[:3] = 0.0  # total <= 0: uniform split
