@@ -1,24 +1,32 @@
 #!/usr/bin/env python
 """Hybrid-iteration benchmark (BASELINE.json metric: hybrid-iter tokens/sec/GPU; p50/p99 TPOT; finetune samples/s).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c3|c2|c1] [--impl ours|reference]
 
-A *step* is one hybrid iteration (one packed bin of Alg. 1: prefill + decode + DPO fine-tune rows in
-one ragged batch, through every decoder layer, plus the masked AdamW update on fine-tune ticks).
-Default workload = BASELINE configs[1] (GPT-2 small hybrid serving + DPO, 1 B200, Poisson trace), bins
-decided by the UNMODIFIED reference scheduler on its own clock (GpuEngine mode "P", so the bins are the
-reference's exactly). Tokens counted per tick = effective (uncached) prefill tokens + decode tokens +
-fine-tune tokens processed.
+A *step* is one hybrid iteration: one packed bin of Alg. 1 (prefill + decode + DPO fine-tune rows in one
+ragged batch) through every decoder layer, plus the masked AdamW update on fine-tune ticks. Default workload
+= C4 (BASELINE configs[3]: Llama-3-8B hybrid serving, prefill-heavy trace, one request stream per GPU + NCCL
+gradient all-reduce) -- the config the 1/2/4/8-GPU metric is quoted on; one C4 rank fits one B200. Bins are
+decided by the UNMODIFIED reference scheduler on its own clock (GpuEngine mode "P": the bins are the
+reference's exactly). Tokens per tick = effective (uncached) prefill tokens + decode tokens + fine-tune tokens.
+
+Timed window: ticks [skip + W, skip + W + K) of each rank's trace, with skip chosen from the reference's own
+timeline (a cost-model-only run of the unmodified Engine, no execution) so that the window holds fine-tune
+ticks at no less than half the trace's steady-state rate -- the window is the hybrid iteration, not a
+decode-only stretch. Both arms time exactly these ticks (same ``config``).
 
 Legs (ours):
-  e2e    K ticks through the public API (GpuEngine, i.e. the reference Engine.run loop with the
-         override): host scheduling, H2D of the tick tables, device work, D2H of every greedy token.
-  value  the same K ticks re-issued from a device snapshot with the tick tables pre-packed
-         (inputs resident), timed with CUDA events on the launch stream, max over ranks.
-  roofline  the dominant kernel (paged decode attention) timed per launch with CUDA events over the
-         same ticks; achieved = algorithmic K/V+Q+O bytes / duration vs MEASURED_PEAKS.json hbm_gbs.
-  cpu_baseline  rank 0, N=1: the fp32 CPU oracle executing the reference scheduler's bins on all host
-         cores for a bounded sample (oracle/ref_arm.py).
+  e2e    the K ticks through the public API (GpuEngine = the reference Engine.run loop with the override):
+         host scheduling, H2D of the tick tables, device work, D2H of every greedy token and fine-tune
+         result. Also the measured TPOT: per-request time between tokens on the device clock.
+  value  the same K ticks re-issued from a device snapshot with the tick tables pre-packed (inputs
+         resident), timed with CUDA events on the launch stream, max over ranks.
+  roofline  the dominant kernel class timed per launch with CUDA events over the same ticks: the
+         projection GEMMs (tensor-bound) for C4, paged decode attention (HBM-bound) for C1-C3.
+  cpu_baseline  rank 0, N=1: the fp32 CPU oracle on a bounded row sample of the same timed ticks, all host
+         cores (oracle/sampled.py).
+--impl reference: rank 0 only -- the unmodified reference scheduler decides every bin of the same trace, and
+  the fp32 CPU oracle executes the same row sample of each timed tick (oracle/sampled.py); same config.
 """
 from __future__ import annotations
 
@@ -118,6 +126,7 @@ def snapshot(model):
     snap = {n: getattr(model, n).clone() for n in names}
     snap["w"] = {n: model.w[n].clone() for n in model.sel}  # AdamW writes only the selected parameters
     snap["adam_step"] = model.adam_step
+    snap["kv_mirror"] = model.kv_mirror.state()
     return snap
 
 
@@ -128,36 +137,98 @@ def restore(model, snap):
                 model.w[k].copy_(v)
         elif n == "adam_step":
             model.adam_step = t
+        elif n == "kv_mirror":
+            model.kv_mirror.restore(t)
         else:
             getattr(model, n).copy_(t)
 
 
-def make_workload(args, rank):
+def make_workload(name, rank, seed=None):
     """The workload's trace for this rank: one independent request stream per GPU, seed = base + rank."""
     from paper_2510_03283_b200.workloads import WORKLOADS
 
-    if args.workload == "c1":
+    if name == "c1":
         return WORKLOADS["c1"]()
-    base = WORKLOADS[args.workload]().seed if args.seed is None else args.seed
-    return WORKLOADS[args.workload](seed=base + rank)
+    base = WORKLOADS[name]().seed if seed is None else seed
+    return WORKLOADS[name](seed=base + rank)
+
+
+def reference_timeline(wl, n_ticks, capture=None):
+    """Run the UNMODIFIED reference Engine on the workload's trace with its own cost-model clock (no model
+    execution at all) for n_ticks executed ticks; per tick (n_prefill rows, n_decode, n_ft_pairs). In mode P
+    GpuEngine executes exactly these bins (tests/test_engine_c1_gpu.py, tests/test_host_cpu.py)."""
+    from macesim.engine import Engine
+    from macesim.workload import WorkloadType
+
+    class Probe(Engine):
+        def _execute(self, plan):
+            t = plan.bin.tasks
+            self.comp.append((sum(1 for r in t if r.workload is WorkloadType.PREFILL),
+                              sum(1 for r in t if r.workload is WorkloadType.DECODE),
+                              sum(1 for r in t if r.workload is WorkloadType.FINETUNE)))
+            if capture is not None:
+                capture(self, plan)
+            super()._execute(plan)
+            if len(self.comp) >= n_ticks:
+                raise StopIteration
+
+    eng = Probe(*wl.engine_args())
+    eng.comp = []
+    try:
+        eng.run()
+    except StopIteration:
+        pass
+    return eng.comp
+
+
+def plan_window(wl, steps, warmup, min_skip):
+    """skip >= min_skip such that the timed ticks [skip + W, skip + W + K) hold fine-tune ticks at no less than half
+    the trace's rate over the scanned steady state (and at least one), from the reference's own timeline."""
+    scan = max(4 * steps, 200)
+    comp = reference_timeline(wl, min_skip + warmup + steps + scan)
+    ft = np.array([c[2] > 0 for c in comp], bool)
+    tail = ft[min_skip:]
+    rate = float(tail.mean()) if tail.size else 0.0
+    need = max(1, int(np.floor(0.5 * rate * steps)))
+    for skip in range(min_skip, max(min_skip + 1, len(comp) - warmup - steps + 1)):
+        if ft[skip + warmup: skip + warmup + steps].sum() >= need:
+            return skip, comp
+    return min_skip, comp
+
+
+def bench_config(wl, args, skip, world):
+    """The ``config`` object -- identical in both arms (the driver compares them)."""
+    cfg = wl.model
+    a, b = skip + args.warmup, skip + args.warmup + args.steps
+    return {"workload": f"{wl.name}: {cfg.name} hybrid serving + DPO fine-tune ({wl.name.upper()})", "model": cfg.name,
+            "trace": {"arrival_rate": wl.trace_cfg.arrival_rate, "retrain_rate": wl.trace_cfg.retrain_rate,
+                      "prompt_len": str(wl.trace_cfg.prompt_len_dist), "output_len": str(wl.trace_cfg.output_len_dist),
+                      "seed_rank0": wl.seed, "seeds": "base + rank"},
+            "max_decode_batch": wl.sched.max_decode_batch, "max_ft_batch": wl.sched.max_ft_batch,
+            "selected_layers": wl.train.n_selected_layers,
+            "clock": "reference cost model (mode P: bins identical to the unmodified scheduler)",
+            "timed_ticks": [a, b], "warmup_ticks": [skip, a],
+            "parallelism": f"request-stream replicas x{world} + NCCL bf16 grad all-reduce",
+            "l2": "inputs larger than L2 (weights + KV pages per tick >> 126 MB)"}
 
 
 def run_ours(args, rank, world, lock):
     import torch
 
-    from paper_2510_03283_b200 import ops
     from paper_2510_03283_b200.build import build
-    from paper_2510_03283_b200.config import TrainConfig
     from paper_2510_03283_b200.engine import GpuEngine
     from paper_2510_03283_b200.model import HybridModel
     from paper_2510_03283_b200.weights import init_weights
-    from paper_2510_03283_b200.workloads import WORKLOADS
 
     build()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    wl = make_workload(args, rank)
+    wl = make_workload(args.workload, rank, args.seed)
     cfg = wl.model
+    # the timed window from the reference's own timeline (host only); every rank agrees on the largest skip
+    min_skip = wl.bench_skip if args.skip is None else args.skip
+    skip, comp = plan_window(wl, args.steps, args.warmup, min_skip)
+    skip = int(lock.max_over_ranks(float(skip)))
     w = init_weights(cfg, seed=0, device=f"cuda:{local}")
     torch.cuda.synchronize()
     kvtok = args.kv_tokens or wl.kv_tokens
@@ -168,15 +239,15 @@ def run_ours(args, rank, world, lock):
     del w
     eng = GpuEngine(*wl.engine_args(), model=model, mode="P", lockstep=lock if world > 1 else None)
     eng.keep_outputs = False
-    # ---- ramp the trace to steady state (untimed), then warm up
-    args.skip = wl.bench_skip if args.skip is None else args.skip
-    eng.run_ticks(args.skip)
+    # ---- ramp the trace to the window (untimed), then warm up
+    eng.run_ticks(skip)
     eng.run_ticks(args.warmup)
     torch.cuda.synchronize()
     snap = snapshot(model)
-    # ---- e2e: K ticks through the public API (host scheduling + H2D tables + D2H tokens)
+    # ---- e2e: K ticks through the public API (host scheduling + H2D tables + D2H tokens / FT results)
     eng.keep_outputs = True
     eng._dec_out.clear()
+    eng.time_ticks = True
     model.tape = []
     h2d0, d2h0 = eng.h2d_bytes, eng.d2h_bytes
     tok0 = len(eng.tick_tokens)
@@ -185,16 +256,21 @@ def run_ours(args, rank, world, lock):
     t0 = time.perf_counter()
     done = eng.run_ticks(args.steps)
     toks_by_req = eng.decoded_tokens()  # D2H of every greedy token of the timed ticks (synchronizes)
+    eng._resolve_ref()                  # D2H of the fine-tune pi_ref log-probs
     torch.cuda.synchronize()
     e2e_s = lock.max_over_ranks(time.perf_counter() - t0)
+    eng.time_ticks = False
+    tbt = eng.measured_tbt_ms()
     tape = model.tape
     model.tape = None
+    n_coll = model.tape_collectives(tape)
+    if lock.max_over_ranks(float(n_coll)) != lock.min_over_ranks(float(n_coll)):
+        raise RuntimeError("ranks recorded different numbers of gradient all-reduces: the replay would deadlock")
     tick_tokens = eng.tick_tokens[tok0:]
     n_tokens = lock.sum_over_ranks(float(sum(tick_tokens)))
     h2d = (eng.h2d_bytes - h2d0) / max(done, 1)
     d2h = (eng.d2h_bytes - d2h0) / max(done, 1)
     # ---- value: replay the same device calls from the snapshot (inputs resident), CUDA events
-    launches0 = model.ctx.launches
     clk = ClockSampler(local).__enter__()  # sampling runs through the warm replay and the timed region
     restore(model, snap)
     model.replay(tape)  # warm replay
@@ -215,7 +291,7 @@ def run_ours(args, rank, world, lock):
     clk.__exit__()
     dev_ms = lock.max_over_ranks(ev0.elapsed_time(ev1))
     clocks = clk.summary(t_on, t_off)
-    # ---- roofline of the dominant kernel: paged decode attention, per-launch CUDA events
+    # ---- roofline of the decode attention (HBM-bound): per-launch CUDA events
     restore(model, snap)
     hbm_peak, tc_peak, peak_src = _peaks()
     model.instrument = []
@@ -241,12 +317,12 @@ def run_ours(args, rank, world, lock):
     roof_gemm = {"bound": "tensor", "kernel": "gemm_tc_kernel / gemm_tc2_kernel (all projections, fwd + FT bwd)",
                  "achieved": g_tflops, "peak": tc_peak, "unit": "TFLOP/s", "frac": g_tflops / tc_peak if tc_peak else None,
                  "peak_source": peak_src, "traffic": None, "share_of_step": g_ms / dev_ms if dev_ms else None,
-                 "flops_per_launch_mean": g_flops / max(g_n, 1), "launches": g_n}
-    one_tick_ms = dev_ms / max(done, 1)
+                 "flops_per_launch_mean": g_flops / max(g_n, 1), "launches": g_n,
+                 "share_note": "per-launch events break the PDL overlap of the value replay: shares are upper bounds"}
     value = n_tokens / (dev_ms / 1e3)
     e2e = n_tokens / e2e_s
-    # TPOT proxies: per-tick device time of the timed ticks (decode tokens emitted once per tick)
-    lat = eng.metrics.latency_summary()
+    n_ft_ticks = sum(1 for op in tape if op[0] == "step" and op[1].ft_pairs)
+    n_pairs = sum(len(op[1].ft_pairs) for op in tape if op[0] == "step")
     out = {
         "metric": "hybrid_iter_tokens_per_s",
         "value": value,
@@ -260,156 +336,150 @@ def run_ours(args, rank, world, lock):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (reference generate_trace Poisson trace; seeded random-init weights at the real shapes)",
-        "config": {"workload": f"{wl.name}: {cfg.name} hybrid serving + DPO ({args.workload})", "model": cfg.name,
-                   "arrival_rate": wl.trace_cfg.arrival_rate, "retrain_rate": wl.trace_cfg.retrain_rate,
-                   "max_decode_batch": wl.sched.max_decode_batch, "selected_layers": wl.train.n_selected_layers,
-                   "clock": "reference cost model (mode P: bins identical to the unmodified scheduler)",
-                   "skip_ticks": args.skip, "parallelism": f"request-stream replicas x{world} + NCCL grad all-reduce",
-                   "l2": "inputs larger than L2 (weights + KV pages per tick >> 126 MB)",
-                   "kv_pool_restored_for_replay": "k_pool" in snap,
-                   "per_gpu_tokens_per_s": value / world,
-                   "rows_per_tick_mean": float(np.mean(tick_tokens)) if tick_tokens else 0.0},
+        "config": bench_config(wl, args, skip, world),
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
         "roofline": None,
         "clocks": clocks,
-        "tpot_reference_clock_ms": {"p50": lat["tbt_p50"], "p99": lat["tbt_p99"]},
-        "device_ms_per_tick": one_tick_ms,
+        "tpot_ms": {"p50": float(np.percentile(tbt, 50)) if tbt else None,
+                    "p99": float(np.percentile(tbt, 99)) if tbt else None, "n": len(tbt),
+                    "clock": "measured: device end-of-tick events of the e2e run (reference TBT, engine.py:130-143, "
+                             "on the B200 clock; rank 0)"},
+        "finetune_samples_per_s": lock.sum_over_ranks(n_pairs) / (dev_ms / 1e3),
+        "ft_ticks_in_timed_region": n_ft_ticks,
+        "ft_pairs_in_timed_region": n_pairs,
+        "per_gpu_tokens_per_s": value / world,
+        "rows_per_tick_mean": float(np.mean(tick_tokens)) if tick_tokens else 0.0,
+        "device_ms_per_tick": dev_ms / max(done, 1),
         "host_issue_ms_per_tick": (t_issued - t_on) * 1e3 / max(done, 1),
-        "finetune_samples_per_s": None,
+        "kv_pool_restored_for_replay": "k_pool" in snap,
+        "idle_lockstep_rounds": eng.idle_rounds,
     }
-    roof_attn = {"bound": "hbm", "kernel": "attn_decode_kernel (paged decode attention)",
+    roof_attn = {"bound": "hbm", "kernel": "paged decode attention (attn_decode2_kernel / attn_decode_tc_kernel)",
                  "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                  "peak_source": peak_src, "traffic": None,
                  "share_of_step": attn_ms_total / dev_ms if dev_ms else None,
                  "bytes_per_launch_mean": float(np.mean(byts)) if byts else 0.0,
                  "launches": len(durs)}
-    # the roofline line is the workload's dominant single kernel: decode attention for the decode-carrying
-    # C1-C3 ticks (the largest single kernel of the step; the GEMM line aggregates ~60 launches of several GEMM
-    # shapes), the projection GEMMs for the prefill-heavy C4; the other one rides along
+    # the roofline line is the workload's dominant kernel class: decode attention for the decode-carrying C1-C3
+    # ticks, the projection GEMMs for the prefill-heavy C4; the other one rides along
     dominant_gemm = wl.name == "c4"
-    # DRAM traffic per launch of the same kernel from the committed ncu --set full capture of this workload
-    # (tools/ncu_capture.sh -> profiles/r1final_ncu_full_summary.json; cold-cache, serialised)
     cap = {"c2": "attn_decode", "c3": "attn_decode_tc", "c4": "gemm_pair"}.get(wl.name)
-    prof = ROOT / "profiles" / "r1final_ncu_full_summary.json"
+    prof = ROOT / "profiles" / "r2_ncu_full_summary.json"
+    if not prof.exists():
+        prof = ROOT / "profiles" / "r1final_ncu_full_summary.json"
     if cap and prof.exists():
         rows = [r for r in json.loads(prof.read_text()).get(cap, []) if "dram_read" in r]
         if rows:
             tr = float(np.mean([r["dram_read"] + r["dram_write"] for r in rows]))
             target = roof_gemm if dominant_gemm else roof_attn
             target["traffic"] = tr
-            target["traffic_source"] = f"profiles/r1final_ncu_full_summary.json[{cap}] ({rows[0]['kernel']})"
+            target["traffic_source"] = f"profiles/{prof.name}[{cap}] ({rows[0]['kernel']}; one ncu --set full capture)"
             if rows[0].get("algorithmic_bytes"):
                 target["traffic_over_algorithmic_in_capture"] = tr / float(np.mean([r["algorithmic_bytes"] for r in rows]))
     out["roofline"] = roof_gemm if dominant_gemm else roof_attn
     out["roofline_other"] = roof_attn if dominant_gemm else roof_gemm
-    n_ft_ticks = sum(1 for op in tape if op[0] == "step" and op[1].ft_pairs)
-    n_pairs = sum(len(op[1].ft_pairs) for op in tape if op[0] == "step")
-    out["finetune_samples_per_s"] = lock.sum_over_ranks(n_pairs) / (dev_ms / 1e3)
-    out["config"]["ft_ticks_in_timed_region"] = n_ft_ticks
-    if args.workload == "c4" and not args.no_cpu_baseline:
-        # the fp32 CPU oracle of Llama-3-8B needs 32 GB of host weights and ~200 s per prefill-heavy tick
-        out["cpu_baseline"] = {"unavailable": "c4 (Llama-3-8B): one fp32 CPU oracle tick exceeds the bounded "
-                                              "sample; the c2 line carries the CPU baseline"}
-    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args, wl, budget_s=args.cpu_seconds)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, wl, skip, model, budget_s=args.cpu_seconds)
     if rank == 0:
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
 
 
-def cpu_baseline(args, wl, budget_s=20.0):
-    """fp32 CPU oracle on the reference scheduler's bins, all host threads, bounded sample."""
+def _window_compositions(wl, skip, warmup, steps, max_pos):
+    """Row compositions (oracle/sampled.composition) of the reference's warm-up and timed ticks."""
+    from oracle.sampled import composition
+
+    comps = []
+
+    def cap(engine, plan):
+        if len(engine.comp) > skip:  # engine.comp already holds this tick
+            comps.append(composition(engine, plan, max_pos))
+
+    reference_timeline(wl, skip + warmup + steps, capture=cap)
+    return comps[:warmup], comps[warmup: warmup + steps]
+
+
+def cpu_baseline(args, wl, skip, model, budget_s=20.0):
+    """fp32 CPU oracle on a bounded row sample of the same timed ticks, all host threads (oracle/sampled.py);
+    the weights are the GPU arm's own (bf16 -> fp32 on the host)."""
     import torch
 
-    from oracle.ref_arm import make_reference_engine_cls
-    from paper_2510_03283_b200.config import selected_param_names
-    from paper_2510_03283_b200.weights import init_weights
+    from oracle.sampled import SampledTickCPU, sample_rows
 
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
-    Eng = make_reference_engine_cls()
-    cfg = wl.model
-    w = init_weights(cfg, seed=0)
-    eng = Eng(*wl.engine_args())
-    eng.setup(cfg, w, wl.train, selected_param_names(cfg, wl.train), wl.seed)
-    t0 = time.perf_counter()
-    while time.perf_counter() - t0 < budget_s:
-        before = eng._done
-        eng.run_ticks(1)
-        if eng._done == before:
+    _, timed = _window_compositions(wl, skip, args.warmup, args.steps, wl.model.max_pos)
+    w = {n: t.float().cpu() for n, t in model.w.items()}
+    ex = SampledTickCPU(wl.model, w)
+    ex.run(sample_rows(timed[0], min(16, args.cpu_rows)))  # warm (threads, allocator)
+    secs = rows = ticks = 0
+    for comp in timed:
+        rs = sample_rows(comp, args.cpu_rows)
+        secs += ex.run(rs)
+        rows += len(rs)
+        ticks += 1
+        if secs > budget_s:
             break
-    secs = sum(eng.tick_secs)
-    toks = sum(eng.tick_tokens)
-    return {"value": toks / secs if secs else 0.0, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"first {eng._done} ticks of the {wl.name} trace (reference bins from tick 0, incl. ramp-up), "
-                      f"{toks} tokens in {secs:.1f} s of oracle compute"}
+    return {"value": rows / secs if secs else 0.0, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{rows} rows of timed ticks {skip + args.warmup}..{skip + args.warmup + ticks - 1} "
+                      f"({args.cpu_rows} per tick, proportional to the tick's prefill / decode / fine-tune rows) "
+                      f"through all {wl.model.n_layers} layers of the fp32 oracle, synthetic KV of each row's real "
+                      f"context length, no DPO backward (oracle/sampled.py); {secs:.1f} s"}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU path (unmodified macesim scheduler + fp32 oracle math)."""
+    """--impl reference: the reference's CPU path -- the unmodified macesim scheduler decides every bin, the fp32
+    CPU oracle executes a bounded row sample of each timed tick (oracle/sampled.py). Rank 0 only."""
     if rank != 0:
         return
     import torch
 
-    from oracle.ref_arm import make_reference_engine_cls
-    from paper_2510_03283_b200.config import selected_param_names
-    from paper_2510_03283_b200.weights import init_weights
-    from paper_2510_03283_b200.workloads import WORKLOADS
+    from oracle.sampled import SampledTickCPU, host_weights, sample_rows
 
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
-    wl = make_workload(args, 0)
-    cfg = wl.model
-    Eng = make_reference_engine_cls()
-    eng = Eng(*wl.engine_args())
-    eng.setup(cfg, init_weights(cfg, seed=0), wl.train, selected_param_names(cfg, wl.train), wl.seed)
-    # bounded sample: the fp32 CPU path needs ~10-80 s for one early (prefill / fine-tune heavy) C2 tick, so the
-    # warm-up is one tick (tick 0: oracle caches and threads warm) and the timed ticks stop at a wall-clock
-    # budget; the same ticks-from-0 sample as the cpu_baseline leg of the GPU arm (the whole arm ends in minutes)
-    t_w = time.perf_counter()
-    while eng._done < min(args.warmup, 1) and time.perf_counter() - t_w < args.ref_seconds / 6:
-        before = eng._done
-        eng.run_ticks(1)
-        if eng._done == before:
-            break
-    n0 = len(eng.tick_tokens)
-    t0 = time.perf_counter()
-    while len(eng.tick_tokens) - n0 < args.steps and time.perf_counter() - t0 < args.ref_seconds:
-        before = eng._done
-        eng.run_ticks(1)
-        if eng._done == before:
-            break
-    wall = time.perf_counter() - t0
-    toks = sum(eng.tick_tokens[n0:])
-    k = len(eng.tick_tokens) - n0
-    v = toks / wall if wall else 0.0
+    wl = make_workload(args.workload, 0, args.seed)
+    min_skip = wl.bench_skip if args.skip is None else args.skip
+    skip, _ = plan_window(wl, args.steps, args.warmup, min_skip)
+    warm, timed = _window_compositions(wl, skip, args.warmup, args.steps, wl.model.max_pos)
+    ex = SampledTickCPU(wl.model, host_weights(wl.model, seed=0, threads=threads))
+    for comp in warm[:2]:  # bounded warm-up: threads, allocator, caches
+        ex.run(sample_rows(comp, args.cpu_rows))
+    secs = rows = 0
+    for comp in timed:
+        rs = sample_rows(comp, args.cpu_rows)
+        secs += ex.run(rs)
+        rows += len(rs)
+    v = rows / secs if secs else 0.0
+    k = len(timed)
     print(json.dumps({
         "impl": "reference", "metric": "hybrid_iter_tokens_per_s", "value": v, "unit": "tokens/s", "n_gpus": world,
-        "steps": k, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(k, 1), "higher_is_better": True,
+        "steps": k, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(k, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{wl.name}: {cfg.name} hybrid serving + DPO ({args.workload})", "model": cfg.name,
-                   "path": "unmodified macesim Engine bins + fp32 CPU oracle arithmetic (oracle/ref_arm.py)"},
+        "config": bench_config(wl, args, skip, world),
+        "path": "unmodified macesim Engine bins + fp32 CPU oracle on a row sample of each timed tick (oracle/sampled.py)",
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
-                         "sample": f"ticks {n0}..{n0 + k} of the trace (from tick 0; warm-up and timed ticks "
-                                   f"bounded by {args.ref_seconds:.0f} s of wall clock), {toks} tokens"},
+                         "sample": f"{rows} rows of the {k} timed ticks ({args.cpu_rows} per tick, proportional to the "
+                                   f"tick's prefill / decode / fine-tune rows) through all {wl.model.n_layers} layers, "
+                                   f"synthetic KV of each row's real context length, no DPO backward; {secs:.1f} s"},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+    }), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=None, help="trace seed of rank 0 (default: the workload's); rank r uses seed + r")
-    ap.add_argument("--skip", type=int, default=None, help="ticks to reach steady state before warm-up (default: the workload's)")
+    ap.add_argument("--skip", type=int, default=None, help="minimum ticks before warm-up (default: the workload's)")
     ap.add_argument("--max-slots", type=int, default=1024)
     ap.add_argument("--kv-tokens", type=int, default=None, help="prompt KV capacity in tokens (default: the workload's)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--cpu-rows", type=int, default=128, help="rows of each timed tick the CPU arms execute")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-seconds", type=float, default=120.0, help="--impl reference: wall-clock bound of the timed ticks")
     args = ap.parse_args()
     from paper_2510_03283_b200.dist import init_from_env
 

@@ -170,12 +170,24 @@ int mace_attn_fwd(mace_ctx* ctx, const MaceAttnArgs* args, void* stream);
 int mace_dpo_fused(mace_ctx* ctx, const float* logits, int R, int V, int ld, const int* targets, const int* pair_rows,
                    int n_pairs, const int* row_ps, const float* ref_lp, float beta, float* row_lse, float* row_lp,
                    float* lp_out, float* loss, float* margin, float* coef, void* dlogits, int ldd, void* stream);
+/* the scalar stage alone, fp64 (same device function the pair stage of mace_dpo_fused uses): per sample
+ * margin = delta_plus - delta_minus, loss = dpo_loss(margin, beta) (alignment.py:39-47, same branches and
+ * expression order), sig = sigma(-beta*margin). margin / sig may be NULL.                                  */
+int mace_dpo_scalar(mace_ctx* ctx, const double* delta_plus, const double* delta_minus, const double* beta, int n,
+                    double* loss, double* margin, double* sig, void* stream);
 /* masked AdamW over the selected-parameter segments: flat fp32 master/m/v/grad [n]; segment s covers
  * [seg_offsets[s], seg_offsets[s+1]) and its bf16 working copy is seg_weights[s] (device array of
  * device pointers). torch.optim.AdamW update order; step is 1-based.                               */
 int mace_adamw_masked(mace_ctx* ctx, float* master, float* m, float* v, const float* grad, long long n,
                       const long long* seg_offsets, void* const* seg_weights, int n_seg, float lr, float beta1,
                       float beta2, float eps, float weight_decay, int step, void* stream);
+/* same update with double hyper-parameters (the fp32 scalars of the update are derived from them in double and
+ * rounded once, as torch.optim.AdamW does from its Python floats); vec4 != 0 selects the float4 streaming kernel
+ * when n and the fp32 buffers allow it -- the caller guarantees every seg_offsets[s] % 4 == 0 and every bf16 copy
+ * 8-byte aligned. Bit-identical to vec4 = 0.                                                                 */
+int mace_adamw_masked2(mace_ctx* ctx, float* master, float* m, float* v, const float* grad, long long n,
+                       const long long* seg_offsets, void* const* seg_weights, int n_seg, double lr, double beta1,
+                       double beta2, double eps, double weight_decay, int step, int vec4, void* stream);
 
 /* ---------------------------------------------------------------- FT-row backward pieces */
 int mace_norm_bwd(mace_ctx* ctx, const float* x, int ldx, const int* xrows, const float* dy, int lddy, int n, int d,

@@ -26,6 +26,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 import torch.nn.functional as F
 
@@ -59,8 +60,8 @@ def gelu_tanh(x):
 def rope(x, pos, theta):
     """x [n, H, hd]; rotate-half convention (Llama); pos int64 [n]."""
     hd = x.shape[-1]
-    inv = theta ** (-torch.arange(0, hd // 2, dtype=torch.float64) * 2.0 / hd)
-    ang = pos.to(torch.float64)[:, None] * inv[None, :]
+    inv = theta ** (-torch.arange(0, hd // 2, dtype=torch.float64, device=x.device) * 2.0 / hd)
+    ang = pos.to(x.device, torch.float64)[:, None] * inv[None, :]
     cos = torch.cos(ang).to(x.dtype)[:, None, :]
     sin = torch.sin(ang).to(x.dtype)[:, None, :]
     x1, x2 = x[..., : hd // 2], x[..., hd // 2:]
@@ -79,9 +80,10 @@ class _Seq:
 class OracleModel:
     """fp32 CPU decoder: Llama (RMSNorm/RoPE/GQA/SwiGLU) or GPT-2 (LayerNorm/learned pos/GELU/bias)."""
 
-    def __init__(self, cfg, weights: dict[str, torch.Tensor]):
+    def __init__(self, cfg, weights: dict[str, torch.Tensor], device: str | torch.device = "cpu"):
         self.cfg = cfg
-        self.w = {k: v.detach().float().clone() for k, v in weights.items()}
+        self.dev = torch.device(device)
+        self.w = {k: v.detach().to(self.dev, torch.float32).clone() for k, v in weights.items()}
 
     # -- one decoder layer over rows x [n, d]; kv_ctx(l, k_new, v_new) -> (K [m,Hkv,hd], V, mask [n,Hkv?,m])
     def _norm(self, x, name, params):
@@ -98,9 +100,9 @@ class OracleModel:
 
     def embed(self, tokens, pos, params=None):
         params = params or self.w
-        x = params["embed"][torch.as_tensor(tokens, dtype=torch.long)]
+        x = params["embed"][torch.as_tensor(tokens, dtype=torch.long, device=self.dev)]
         if self.cfg.family == "gpt2":
-            x = x + params["pos_embed"][torch.as_tensor(pos, dtype=torch.long)]
+            x = x + params["pos_embed"][torch.as_tensor(pos, dtype=torch.long, device=self.dev)]
         return x
 
     def layer(self, l, x, pos, attend, params=None):
@@ -115,7 +117,7 @@ class OracleModel:
         k = qkv[:, Hq * hd: (Hq + Hk) * hd].reshape(-1, Hk, hd)
         v = qkv[:, (Hq + Hk) * hd:].reshape(-1, Hk, hd)
         if c.family == "llama":
-            pos_t = torch.as_tensor(pos, dtype=torch.long)
+            pos_t = torch.as_tensor(pos, dtype=torch.long, device=self.dev)
             q = rope(q, pos_t, c.rope_theta)
             k = rope(k, pos_t, c.rope_theta)
         o = attend(l, q, k, v)
@@ -149,7 +151,7 @@ class OracleModel:
         n = len(tokens)
         pos = list(range(pos0, pos0 + n))
         x = self.embed(tokens, pos, params)
-        causal = torch.tril(torch.ones(n, n, dtype=torch.bool))
+        causal = torch.tril(torch.ones(n, n, dtype=torch.bool, device=self.dev))
         kvs = []
 
         def attend(l, q, k, v):
@@ -169,17 +171,17 @@ class OracleModel:
         P = len(prompt)
         logits = self.final(h[P - 1: P - 1 + len(response)], params)
         lp = torch.log_softmax(logits, dim=-1)
-        tgt = torch.as_tensor(response, dtype=torch.long)
+        tgt = torch.as_tensor(response, dtype=torch.long, device=self.dev)
         return lp.gather(1, tgt[:, None]).sum()
 
 
 class OracleExecutor:
     """Request-level restatement of the GPU hybrid step (prefill / decode / DPO fine-tune)."""
 
-    def __init__(self, cfg, weights, tcfg, selected_names):
+    def __init__(self, cfg, weights, tcfg, selected_names, device: str | torch.device = "cpu"):
         self.cfg = cfg
         self.tcfg = tcfg
-        self.model = OracleModel(cfg, weights)
+        self.model = OracleModel(cfg, weights, device)
         self.selected = list(selected_names)
         self.ref_params = {n: self.model.w[n].clone() for n in self.selected}  # pi_ref frozen at init
         self.master = {n: self.model.w[n].clone() for n in self.selected}
@@ -223,7 +225,7 @@ class OracleExecutor:
             K = torch.cat([Kp, Kd])
             V = torch.cat([Vp, Vd])
             m = K.shape[0]
-            mask = torch.zeros(1, c.n_kv_heads, m, dtype=torch.bool)
+            mask = torch.zeros(1, c.n_kv_heads, m, dtype=torch.bool, device=K.device)
             mask[:, :, : P - 1] = True
             for h in range(c.n_kv_heads):
                 keep = (k_idx - 1) if kept_pre is None else min(kept_pre[h], k_idx - 1)
@@ -281,9 +283,10 @@ class OracleExecutor:
         for n in self.selected:
             k = self.master[n].numel()
             shape = self.master[n].shape
-            self.master[n] = master_flat[off: off + k].view(shape).clone()
-            self.m[n] = m_flat[off: off + k].view(shape).clone()
-            self.v[n] = v_flat[off: off + k].view(shape).clone()
+            dev = self.model.dev
+            self.master[n] = master_flat[off: off + k].view(shape).to(dev).clone()
+            self.m[n] = m_flat[off: off + k].view(shape).to(dev).clone()
+            self.v[n] = v_flat[off: off + k].view(shape).to(dev).clone()
             self.model.w[n] = self.master[n].to(torch.bfloat16).float()
             off += k
 
@@ -316,36 +319,52 @@ class TickOracle:
     decode windows): the oracle reads it the way the device does, so prefix KV shared through the
     trie is the KV the sharing request actually sees (computed by whichever earlier prefill, under
     the weights of that time), exactly like the device pages.
+
+    ``device``: where the fp32 restatement executes. CPU for the small configs; the full-shape sampled
+    replays of Llama-3.2-1B / Llama-3-8B (tests/test_parity_shapes_gpu.py) run the SAME fp32 code through
+    torch on the GPU (cuBLAS fp32 with TF32 disabled -- an independent implementation from the product's
+    bf16 tcgen05 kernels), because a CPU fp32 replay of an 8B model exceeds the test budget.
     """
 
     PAGE = 16
 
-    def __init__(self, cfg, weights, tcfg, selected_names):
+    def __init__(self, cfg, weights, tcfg, selected_names, device: str | torch.device = "cpu"):
         self.cfg = cfg
-        self.ex = OracleExecutor(cfg, weights, tcfg, selected_names)
+        self.dev = torch.device(device)
+        self.ex = OracleExecutor(cfg, weights, tcfg, selected_names, self.dev)
         self.model = self.ex.model
         L, H, hd = cfg.n_layers, cfg.n_kv_heads, cfg.head_dim
         self._shape = (L, H, self.PAGE, hd)
-        self.kstore: dict[int, torch.Tensor] = {}
-        self.vstore: dict[int, torch.Tensor] = {}
+        # prompt page groups: group id -> row of a dense store [n, L, H, 16, hd] (grown on demand)
+        self.gslot: dict[int, int] = {}
+        self.kstore = torch.zeros((0,) + self._shape, device=self.dev)
+        self.vstore = torch.zeros((0,) + self._shape, device=self.dev)
         self.ptab: dict[int, list[int]] = {}
         self.dec: dict[int, dict] = {}
         self.last_token: dict[int, int] = {}
 
-    def _page(self, store, g):
-        if g not in store:
-            store[g] = torch.zeros(self._shape)
-        return store[g]
+    def _slots(self, groups: list[int]) -> torch.Tensor:
+        """Store rows of the given groups (new groups get zero pages, like the device's zeroed pool)."""
+        new = [g for g in dict.fromkeys(groups) if g not in self.gslot]
+        if new:
+            n0 = self.kstore.shape[0]
+            for i, g in enumerate(new):
+                self.gslot[g] = n0 + i
+            z = torch.zeros((len(new),) + self._shape, device=self.dev)
+            self.kstore = torch.cat([self.kstore, z])
+            self.vstore = torch.cat([self.vstore, z.clone()])
+        return torch.tensor([self.gslot[g] for g in groups], dtype=torch.long, device=self.dev)
 
     def run_tick(self, batch, gpu_tokens, kept_post):
         """Returns (decode logits [n_dec, V], FT (losses, margins, grads) or None)."""
         c = self.cfg
-        H, G = c.n_kv_heads, c.group
+        H, P16 = c.n_kv_heads, self.PAGE
         for slot, row in zip(batch.ptab_slots.tolist(), batch.ptab_rows.tolist()):
             self.ptab[slot] = row
         for src, dst, n, _ in batch.page_copies.tolist():
-            for st in (self.kstore, self.vstore):
-                self._page(st, dst)[:, :, :n] = self._page(st, src)[:, :, :n]
+            si, di = self._slots([src, dst]).tolist()
+            self.kstore[di, :, :, :n] = self.kstore[si, :, :, :n]
+            self.vstore[di, :, :, :n] = self.vstore[si, :, :, :n]
         ft0 = batch.ft0
         seqs = batch.seqs.tolist()
         inf = [s for s in seqs if s[0] != 2]
@@ -363,45 +382,51 @@ class TickOracle:
                     if j == 0 or s[3] not in self.dec:
                         self.dec[s[3]] = {"k": [[] for _ in range(c.n_layers)], "v": [[] for _ in range(c.n_layers)],
                                           "first": [0] * H}
+            # per prefill sequence: the (store row, page row) of each written prompt index and of each visible one
+            wr, rd = {}, {}
+            for s in inf:
+                kind, q0, ql, slot, n_pv = s[:5]
+                tab = self.ptab[slot]
+                if kind == 0:
+                    t = batch.row_kvi[q0: q0 + ql].astype(np.int64)
+                    wr[q0] = (self._slots([tab[i] for i in (t // P16).tolist()]), torch.as_tensor(t % P16, device=self.dev))
+                if n_pv:
+                    t = np.arange(n_pv)
+                    rd[q0] = (self._slots([tab[i] for i in (t // P16).tolist()]), torch.as_tensor(t % P16, device=self.dev))
 
             def attend(l, q, k, v):
                 # 1) write this layer's K/V for every row (prefill -> pages, decode -> slot lists)
                 for s in inf:
                     kind, q0, ql, slot, n_pv = s[:5]
-                    for i in range(ql):
-                        r = q0 + i
-                        t = int(batch.row_kvi[r])
-                        if kind == 0:
-                            g = self.ptab[slot][t // self.PAGE]
-                            self._page(self.kstore, g)[l, :, t % self.PAGE] = k[r]
-                            self._page(self.vstore, g)[l, :, t % self.PAGE] = v[r]
-                        else:
-                            d = self.dec[slot]
-                            assert len(d["k"][l]) == t, "decode slot index mismatch"
-                            d["k"][l].append(k[r].clone())
-                            d["v"][l].append(v[r].clone())
+                    if kind == 0:
+                        gs, rr = wr[q0]
+                        self.kstore[gs, l, :, rr] = k[q0: q0 + ql]
+                        self.vstore[gs, l, :, rr] = v[q0: q0 + ql]
+                    else:
+                        d = self.dec[slot]
+                        assert len(d["k"][l]) == int(batch.row_kvi[q0]), "decode slot index mismatch"
+                        d["k"][l].append(k[q0].clone())
+                        d["v"][l].append(v[q0].clone())
                 # 2) attention per sequence over its visible KV
-                o = torch.zeros(q.shape[0], c.n_heads, c.head_dim)
+                o = torch.zeros(q.shape[0], c.n_heads, c.head_dim, device=self.dev)
                 for s in inf:
                     kind, q0, ql, slot, n_pv = s[:5]
-                    tab = self.ptab[slot]
-                    Kp = torch.stack([self.kstore[tab[t // self.PAGE]][l, :, t % self.PAGE] for t in range(n_pv)]) \
-                        if n_pv else torch.zeros(0, H, c.head_dim)
-                    Vp = torch.stack([self.vstore[tab[t // self.PAGE]][l, :, t % self.PAGE] for t in range(n_pv)]) \
-                        if n_pv else torch.zeros(0, H, c.head_dim)
+                    if n_pv:
+                        gs, rr = rd[q0]
+                        Kp, Vp = self.kstore[gs, l, :, rr], self.vstore[gs, l, :, rr]  # [n_pv, H, hd]
+                    else:
+                        Kp = Vp = torch.zeros(0, H, c.head_dim, device=self.dev)
                     if kind == 0:
                         m = n_pv
-                        qlog = torch.arange(ql)[:, None] + (n_pv - ql)
-                        mask = (torch.arange(m)[None, :] <= qlog)[:, None, :].expand(ql, H, m)
+                        qlog = torch.arange(ql, device=self.dev)[:, None] + (n_pv - ql)
+                        mask = (torch.arange(m, device=self.dev)[None, :] <= qlog)[:, None, :].expand(ql, H, m)
                         o[q0: q0 + ql] = self.model.attention(q[q0: q0 + ql], Kp, Vp, mask)
                     else:
                         d = self.dec[slot]
                         j = int(batch.row_kvi[q0])
-                        Kd = torch.stack(d["k"][l])
-                        Vd = torch.stack(d["v"][l])
-                        K = torch.cat([Kp, Kd])
-                        V = torch.cat([Vp, Vd])
-                        mask = torch.zeros(1, H, K.shape[0], dtype=torch.bool)
+                        K = torch.cat([Kp, torch.stack(d["k"][l])])
+                        V = torch.cat([Vp, torch.stack(d["v"][l])])
+                        mask = torch.zeros(1, H, K.shape[0], dtype=torch.bool, device=self.dev)
                         mask[:, :, :n_pv] = True
                         for h in range(H):
                             mask[0, h, n_pv + d["first"][h]: n_pv + j + 1] = True
@@ -411,7 +436,7 @@ class TickOracle:
             for l in range(c.n_layers):
                 x = self.model.layer(l, x, pos, attend)
             if batch.n_dec:
-                logits = self.model.final(x[batch.dec_rows.tolist()])
+                logits = self.model.final(x[batch.dec_rows.tolist()]).cpu()
         # teacher forcing: the next decode input of each slot is the GPU's greedy token
         for slot, tok in zip(batch.dec_slots.tolist(), gpu_tokens):
             self.last_token[slot] = int(tok)
@@ -424,6 +449,7 @@ class TickOracle:
         if batch.ft_pairs:
             pairs = [(p.rid, p.prompt, p.chosen, p.rejected) for p in batch.ft_pairs]
             losses, margins, grads = self.ex.dpo_step(pairs)
-            self.ex.adamw(grads)
+            grads = {n: g.cpu() for n, g in grads.items()}
+            self.ex.adamw({n: g.to(self.dev) for n, g in grads.items()})
             ft = (losses, margins, grads)
         return logits, ft

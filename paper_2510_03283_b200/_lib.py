@@ -155,7 +155,10 @@ SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_attn_fwd": (C.c_int, [_vp, C.POINTER(MaceAttnArgs), _vp]),
     "mace_dpo_fused": (C.c_int, [_vp, _vp, _i, _i, _i, _ip, _ip, _i, _ip, _vp, _f, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _i, _vp]),
+    "mace_dpo_scalar": (C.c_int, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
     "mace_adamw_masked": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_longlong, _vp, _vp, _i, _f, _f, _f, _f, _f, _i, _vp]),
+    "mace_adamw_masked2": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_longlong, _vp, _vp, _i] + [C.c_double] * 5
+                           + [_i, _i, _vp]),
     "mace_norm_bwd": (C.c_int, [_vp, _vp, _i, _ip, _vp, _i, _i, _i, _vp, _i, _f, _vp, _i, _ip, _vp, _vp, _vp,
                                 C.c_size_t, _vp]),
     "mace_colsum_bf16": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp, C.c_size_t, _vp]),

@@ -12,6 +12,9 @@ Alg. 1 (scheduler.py:133-188). ``GpuEngine`` subclasses the UNMODIFIED reference
   4. it mirrors the reference's post-tick KV decisions onto the device (per-head prune trims,
      retirements -> page release; trie evictions via GpuPrefixTrie).
 
+Env: the reference's synthetic AlignmentEnv (decisions bit-identical to the reference), or mode R:
+alignenv.DeviceAlignmentEnv, whose pair_loss / ft_step / check_end answers are the device's DPO losses.
+
 Clock modes:
   "P"  parity: the reference cost model drives the clock -> scheduler decisions are bit-identical
        to an unmodified reference run; the GPU executes the same bins for real.
@@ -153,7 +156,8 @@ class GpuEngine(Engine):
         self.record = record
         self.records: list[dict] = []
         self.tick_tokens: list[int] = []
-        self.tick_device_ms: list[float] = []
+        self.tick_device_ms: list = []      # (start, end) CUDA events per tick (mode M / time_ticks)
+        self.tick_decode_ids: list = []     # decode request ids per timed tick (measured TPOT)
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self._planned_shared: dict[int, int] = {}
@@ -436,6 +440,10 @@ class GpuEngine(Engine):
         if timed:
             ev1.record()
         self.h2d_bytes += m.h2d_bytes
+        observe = getattr(self.env, "observe", None)  # mode R (alignenv.DeviceAlignmentEnv): the device DPO losses
+        if observe is not None and fts and out.ft_loss is not None:
+            observe([r.id for r in fts], out.ft_loss, out.ft_margin)
+            self.d2h_bytes += 8 * len(fts)
         if self.mode == "M":
             ev1.synchronize()
             self.profile._clock[0] = ev0.elapsed_time(ev1)
@@ -480,6 +488,7 @@ class GpuEngine(Engine):
         self.tick_tokens.append(batch.total_tokens)
         if timed:
             self.tick_device_ms.append((ev0, ev1))
+            self.tick_decode_ids.append([r.id for r in decodes])
         self.last_batch = batch
         if self.record:  # host copies for the oracle replay (tests only; synchronizes)
             torch.cuda.current_stream().synchronize()
@@ -653,6 +662,21 @@ class GpuEngine(Engine):
             arr = host.numpy()
             for i, rid in enumerate(ids):
                 out.setdefault(rid, []).append(int(arr[i]))
+        return out
+
+    def measured_tbt_ms(self, first: int = 0) -> list[float]:
+        """Time between consecutive tokens of every request, measured on the device clock: the gap between the
+        end events of the two ticks that emitted them (includes any time the device waited on the host). The
+        reference's TBT (engine.py:130-143) on the measured clock; ticks from index ``first`` of the timed list."""
+        torch.cuda.current_stream().synchronize()
+        last: dict[int, int] = {}
+        out = []
+        for i in range(first, len(self.tick_device_ms)):
+            for rid in self.tick_decode_ids[i]:
+                j = last.get(rid)
+                if j is not None:
+                    out.append(self.tick_device_ms[j][1].elapsed_time(self.tick_device_ms[i][1]))
+                last[rid] = i
         return out
 
     def device_ms(self) -> list[float]:

@@ -83,7 +83,16 @@ class HybridModel:
         self.seg_offsets = torch.from_numpy(offs).to(self.dev)
         self.seg_ptrs = torch.tensor([self.w[n].data_ptr() for n in self.sel], dtype=torch.int64, device=self.dev)
         self.adam_step = 0
+        # the float4 AdamW kernel needs every segment to start on a 4-element boundary of the flat buffers and
+        # every bf16 working copy 8-byte aligned (true for every preset: all widths are multiples of 4)
+        self.adam_vec4 = bool((offs % 4 == 0).all() and all(self.w[n].data_ptr() % 8 == 0 for n in self.sel))
         self.ref_w = {n: self.w[n].clone() for n in self.sel}  # pi_ref frozen at init
+        # pi_ref log-probs are recomputed in every fine-tune tick by default: the pi_ref and policy sub-passes then
+        # start from the SAME tick's layer-l_min activations, so the bf16 noise of the rows below l_min cancels in
+        # the margin (lp - ref). A pi_ref cached from the pair's first tick was computed inside a different batch
+        # (other tile shapes / accumulation orders below l_min) and left ~0.1 nat of noise in m on later steps.
+        # The cost is one sub-pass over the selected layers only; most ticks need it anyway (a new pair).
+        self.ref_every_tick = True
         # ---- RoPE tables (fp64 on host -> fp32)
         half = cfg.head_dim // 2
         inv = cfg.rope_theta ** (-np.arange(half, dtype=np.float64) * 2.0 / cfg.head_dim)
@@ -390,7 +399,7 @@ class HybridModel:
         if self.instrument is not None and n_dec:
             self._attn_bytes = self.decode_attn_bytes(batch)
         d = MaceTickDesc(T=T, ft0=ft0, n_dec=n_dec, R=R, n_pairs=P,
-                         need_ref=int(any(p.ref_lp is None for p in batch.ft_pairs)))
+                         need_ref=int(self.ref_every_tick or any(p.ref_lp is None for p in batch.ft_pairs)))
         for name in ("tokens", "pos", "row_seq", "row_kvi", "seqs", "dec_slots", "dec_rows", "ptab_slots",
                      "ptab_rows", "page_copies", "ft_local_rows", "ft_targets", "pair_rows", "row_ps", "ref_cached",
                      "ft_seqs", "ft_row_seq"):
@@ -551,7 +560,7 @@ class HybridModel:
                 torch.distributed.all_reduce(self.grad, group=self.pg)
         self.adam_step += 1
         t = self.tcfg
-        self._chk(L.mace_adamw_masked(self.ctx.h, self.master.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
-                                      self.grad.data_ptr(), self.n_sel, self.seg_offsets.data_ptr(),
-                                      self.seg_ptrs.data_ptr(), len(self.sel), t.lr, t.beta1, t.beta2, t.eps,
-                                      t.weight_decay, self.adam_step, s), "adamw")
+        self._chk(L.mace_adamw_masked2(self.ctx.h, self.master.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
+                                       self.grad.data_ptr(), self.n_sel, self.seg_offsets.data_ptr(),
+                                       self.seg_ptrs.data_ptr(), len(self.sel), t.lr, t.beta1, t.beta2, t.eps,
+                                       t.weight_decay, self.adam_step, int(self.adam_vec4), s), "adamw")

@@ -107,3 +107,26 @@ class FakeModel:
 
     def release_slots(self, slots):
         self.calls.append(("release", list(slots)))
+
+
+class LossFakeModel(FakeModel):
+    """FakeModel whose fine-tune ticks return per-pair DPO losses / margins from ``loss_of(rid, step)`` (CPU
+    tensors), the way HybridModel.step returns the fused DPO kernel's outputs."""
+
+    def __init__(self, *a, loss_of, **k):
+        super().__init__(*a, **k)
+        self.loss_of = loss_of
+        self.ft_seen: dict[int, int] = {}
+
+    def step(self, batch, trim=None, ft_global=None):
+        import torch
+
+        super().step(batch, trim, ft_global)
+        if not batch.ft_pairs:
+            return StepOutputs(None, None, None, None, None, None)
+        ls = []
+        for p in batch.ft_pairs:
+            k = self.ft_seen[p.rid] = self.ft_seen.get(p.rid, 0) + 1
+            ls.append(self.loss_of(p.rid, k))
+        loss = torch.tensor(ls, dtype=torch.float32)
+        return StepOutputs(None, loss, -loss, None, None, None)
