@@ -64,8 +64,11 @@ def make_reference_engine_cls():
                 for r in fts:
                     P = len(r.prompt_tokens)
                     room = max(1, self.mcfg.max_pos - P)
-                    c, j = _pair_tokens(self.seed, r.id, min(r.pair.tokens_chosen, room),
-                                        min(r.pair.tokens_rejected, room), self.mcfg.vocab)
+                    n_c, n_r = min(r.pair.tokens_chosen, room), min(r.pair.tokens_rejected, room)
+                    if getattr(r.pair, "chosen", None):  # trace v2 content
+                        c, j = list(r.pair.chosen[:n_c]), list(r.pair.rejected[:n_r])
+                    else:
+                        c, j = _pair_tokens(self.seed, r.id, n_c, n_r, self.mcfg.vocab)
                     pairs.append((r.id, r.prompt_tokens, c, j))
                     n_tok += 2 * P + len(c) + len(j)
                 _, _, grads = self.ox.dpo_step(pairs)

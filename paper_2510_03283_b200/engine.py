@@ -125,9 +125,11 @@ class TickBudgetReached(Exception):
 class GpuEngine(Engine):
     def __init__(self, trace, profile, sched_cfg, priority_params, cache_cfg, env, engine_cfg, metrics_horizon=None,
                  *, model: HybridModel, mode: str = "P", seed: int | None = None, record: bool = False,
-                 lockstep=None, fast_host: bool = True):
+                 lockstep=None, fast_host: bool = True, norms: str = "synthetic", page_budget: bool | None = None):
         if mode not in ("P", "M"):
             raise ValueError("mode must be 'P' (parity clock) or 'M' (measured clock)")
+        if norms not in ("synthetic", "device"):
+            raise ValueError("norms must be 'synthetic' (the reference's draws, engine.py:433-442) or 'device'")
         if mode == "M":
             profile = measured_profile(profile)
             engine_cfg = replace(engine_cfg, scheduler_overhead_ms=0.0)
@@ -182,6 +184,14 @@ class GpuEngine(Engine):
         self._release_later: list | None = None   # KV slots retired by the executing bin (released after it)
         self._tok_arena: torch.Tensor | None = None  # pinned arena for the per-tick greedy-token copies
         self._tok_off = 0
+        # head norms feeding HeadStats (engine.py:433-442, cache.py:276-315): the reference's synthetic draws, or the
+        # device's real per-head attention-output norms of the tick's last layer (query heads of a KV group
+        # combined as sqrt(mean ||o_h||^2)), read back after the tick
+        self.norm_source = norms
+        self._dev_norms: dict[int, np.ndarray] = {}
+        # budget from the page allocator (mode M default): min(the reference's MB budget, the MB the free device
+        # pages hold, minus one partial page per live request and head) -- the real pools can never be overrun
+        self.page_budget = (mode == "M") if page_budget is None else page_budget
 
     # ------------------------------------------------------------------ helpers
     def _slot(self, rid: int) -> int:
@@ -348,7 +358,12 @@ class GpuEngine(Engine):
             key = (req.id, n_c, n_r)
             hit = self._pair_tokens.get(req.id)
             if hit is None or hit[0] != key:
-                hit = self._pair_tokens[req.id] = (key, synthetic_pair_tokens(self.seed, req.id, n_c, n_r, c.vocab))
+                content = getattr(req.pair, "chosen", None)
+                if content:  # trace v2 (tracev2.ContentPair): the pair's own responses
+                    toks = (list(req.pair.chosen[:n_c]), list(req.pair.rejected[:n_r]))
+                else:        # mace-trace-v1 carries lengths only: builder-defined synthetic content
+                    toks = synthetic_pair_tokens(self.seed, req.id, n_c, n_r, c.vocab)
+                hit = self._pair_tokens[req.id] = (key, toks)
             chs, rjs = hit[1]
             pairs.append(FtPair(req.id, req.prompt_tokens, chs, rjs, self.ref_lp.get(req.id)))
             pr = []
@@ -440,6 +455,12 @@ class GpuEngine(Engine):
         if timed:
             ev1.record()
         self.h2d_bytes += m.h2d_bytes
+        if self.norm_source == "device" and out.head_norm is not None:
+            hn = out.head_norm.double().cpu().numpy()  # synchronizes: [n_dec, Hq]
+            G = self.mcfg.group
+            per_kv = np.sqrt((hn.reshape(hn.shape[0], -1, G) ** 2).mean(-1))
+            self._dev_norms = {r.id: per_kv[i] for i, r in enumerate(decodes)}
+            self.d2h_bytes += hn.size * 4
         observe = getattr(self.env, "observe", None)  # mode R (alignenv.DeviceAlignmentEnv): the device DPO losses
         if observe is not None and fts and out.ft_loss is not None:
             observe([r.id for r in fts], out.ft_loss, out.ft_margin)
@@ -604,7 +625,10 @@ class GpuEngine(Engine):
         if first.any():
             self.hstats.reset(slots[first])
         steps = info[:, 1] + 1
-        norms = self.norm_stream.norms_many(rows, slots)
+        if self.norm_source == "device":
+            norms = np.stack([self._dev_norms[r.id] for r in rows]).astype(np.float64)
+        else:
+            norms = self.norm_stream.norms_many(rows, slots)
         kept, released = self.hstats.step(slots, steps, norms)
         return dict(zip([r.id for r in rows], zip(kept.tolist(), released.tolist())))
 
@@ -612,7 +636,28 @@ class GpuEngine(Engine):
         return fast_schedule_iteration(queue, *args, dec_est=self._dec_est, **kw)
 
     def _synth_norms(self, req, rs):  # engine.py:433 — same draws, served from the per-request block stream
+        if self.norm_source == "device":
+            return self._dev_norms[req.id].tolist()
         return self.norm_stream.norms(req, rs).tolist()
+
+    def _budget(self):  # engine.py:268 — the reference's MB budget, capped by the device pools in page terms
+        b = super()._budget()
+        if self.page_budget and hasattr(self.model, "kv_mirror"):
+            b = min(b, self.page_budget_mb())
+        return b
+
+    def page_budget_mb(self) -> float:
+        """MB of KV the free device pages can still take, in the profile's units (decode_kv_mem_per_token = the
+        model's KV bytes per token / 2^20 in every workload): free prompt groups x 16 tokens plus free decode head
+        pages x 16 tokens / H, less one partial prompt group and one partial decode page per head for every live
+        request (page rounding)."""
+        m = self.model
+        kv = self.profile.decode_kv_mem_per_token
+        H = m.cfg.n_kv_heads
+        live = len(self.live)
+        groups = max(0, len(self.pool.free) - live)
+        dec = max(0, m.kv_mirror.free - live * H)
+        return groups * PAGE * kv + dec * PAGE * kv / H
 
     def _estimate(self, req):  # engine.py:262 -> cost_model.get_workload (cost_model.py:92-106), same arithmetic
         w = req.workload

@@ -67,6 +67,11 @@ class HybridModel:
         self.grad_allreduce = grad_allreduce
         d, L = cfg.d_model, cfg.n_layers
         self.w = {n: t.to(self.dev, torch.bfloat16).contiguous() for n, t in weights.items()}
+        # the masked AdamW rewrites the selected parameters' bf16 working copies in place: never alias the caller's
+        # tensors (a bf16 dict already on this device would otherwise be trained under the caller's feet)
+        for n in selected_param_names(cfg, tcfg):
+            if self.w[n].data_ptr() == weights[n].data_ptr():
+                self.w[n] = self.w[n].clone()
         # ---- selected parameters: flat fp32 master / m / v / grad + segment table for masked AdamW
         self.sel = selected_param_names(cfg, tcfg)
         self.sel_layers = tcfg.selected_layers(cfg)
@@ -443,6 +448,8 @@ class HybridModel:
         out = StepOutputs(None, None, None, None, None, None)
         if n_dec and T:
             out.dec_tokens = self.dec_tok[:n_dec]
+            d0 = int(batch.dec_rows[0])  # decode rows are contiguous in the batch (engine.build_batch)
+            out.head_norm = self.hn[d0: d0 + n_dec]  # ||o_{t,h}|| of the last layer's attention, per query head
         if trim is not None and trim[0].size:
             self.apply_trim(*trim)
         if has_ft:

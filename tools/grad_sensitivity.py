@@ -98,7 +98,8 @@ def main():
         lf, mf, gf = f32.dpo_step(pairs)
         lb, mb, gb = b16.dpo_step(pairs)
         print(f"tick {rec['tick']}: pairs {len(pairs)} loss gpu {list(map(float, rec['ft_loss']))} f32 {lf} b16 {lb}")
-        print(f"   margin gpu {list(map(float, rec['ft_margin']))} f32 {mf} b16 {mb}")
+        print(f"   margin gpu {[round(float(x), 5) for x in rec['ft_margin']]} f32 {[round(x, 5) for x in mf]} "
+              f"b16 {[round(x, 5) for x in mb]}")
         for n in sel:
             g = rec["grad"][n].cuda().float()
             rel = lambda a, c: float((a - c).norm() / (c.norm() + 1e-30))  # noqa: E731
