@@ -175,6 +175,14 @@ int mace_dpo_fused(mace_ctx* ctx, const float* logits, int R, int V, int ld, con
  * expression order), sig = sigma(-beta*margin). margin / sig may be NULL.                                  */
 int mace_dpo_scalar(mace_ctx* ctx, const double* delta_plus, const double* delta_minus, const double* beta, int n,
                     double* loss, double* margin, double* sig, void* stream);
+/* AdamW over arbitrary segments of the flat fp32 buffers (per-tenant LoRA adapters: one tenant's rows of every
+ * stacked adapter): segment s covers master[seg_flat[s] .. + len_s) with len_s = seg_vstart[s+1] - seg_vstart[s]
+ * (device int64 arrays; seg_vstart[0] = 0), bf16 copy seg_weights[s]. Same per-element arithmetic as
+ * mace_adamw_masked2; float4 path when every offset / length is a multiple of 4 (vec4 != 0).                 */
+int mace_adamw_segments(mace_ctx* ctx, float* master, float* m, float* v, const float* grad, int n_seg,
+                        const long long* seg_vstart, const long long* seg_flat, void* const* seg_weights, long long n,
+                        double lr, double beta1, double beta2, double eps, double weight_decay, int step, int vec4,
+                        void* stream);
 /* masked AdamW over the selected-parameter segments: flat fp32 master/m/v/grad [n]; segment s covers
  * [seg_offsets[s], seg_offsets[s+1]) and its bf16 working copy is seg_weights[s] (device array of
  * device pointers). torch.optim.AdamW update order; step is 1-based.                               */
@@ -199,6 +207,10 @@ int mace_act_bwd(mace_ctx* ctx, const void* u, const void* da, int n, int F, int
 int mace_rope_bwd(mace_ctx* ctx, float* dqkv, int n, int Hq, int Hkv, int hd, const int* pos, const float* cos_t,
                   const float* sin_t, void* stream);
 int mace_f32_to_bf16(mace_ctx* ctx, const float* x, long long n, void* y, void* stream);
+/* LoRA row mask: out[i, c] = bf16(scale * z[i, c]) if c / rank == tenant[i] else 0, for c < R (tenant NULL:
+ * every column 0 -- the pi_ref pass). z fp32 [n, ldz], out bf16 [n, ldo]; R % 8 == 0.                       */
+int mace_lora_mask(mace_ctx* ctx, const float* z, int ldz, const int* tenant, int n, int rank, int R, float scale,
+                   void* out, int ldo, void* stream);
 /* widening copy; with mace_f32_to_bf16 it brackets the bf16 gradient all-reduce of lockstep replicas */
 int mace_bf16_to_f32(mace_ctx* ctx, const void* x, long long n, float* y, void* stream);
 /* attention backward of the dense causal FT sequences: items int4 [n_items] = (seq, kv_head, key_block, steps),
@@ -238,6 +250,15 @@ typedef struct MaceLayerGrads {            /* fp32 views into the flat gradient 
   float *attn_norm_w, *attn_norm_b, *qkv_w, *qkv_b, *o_w, *o_b;
   float *mlp_norm_w, *mlp_norm_b, *up_w, *up_b, *down_w, *down_b;
 } MaceLayerGrads;
+typedef struct MaceLoraLayer {             /* per-tenant LoRA adapters of one selected layer, tenants stacked:
+                                              R = tenants x rank rows, tenant u owns rows [u*rank, (u+1)*rank)  */
+  const void *a_qkv, *a_o, *a_up, *a_down;  /* bf16 [R, in]: the shrink  Z = X A^T                             */
+  const void *bt_o, *bt_down;               /* bf16 [R, out]: the expand x += Zm B^T, B^T stored MN-major      */
+  /* qkv / up: B^T lives in the last R columns of the AUGMENTED base weight layers[l].qkv_w / up_w
+   * ([out, in + R]): [X | Zm] . [W | B]^T is one GEMM that keeps the fused bias / GELU / SwiGLU epilogue     */
+  float *g_a_qkv, *g_a_o, *g_a_up, *g_a_down;       /* fp32 [R, in] grads (views of the flat gradient)       */
+  float *g_bt_qkv, *g_bt_o, *g_bt_up, *g_bt_down;   /* fp32 [R, out]                                        */
+} MaceLoraLayer;
 typedef struct MaceModelDesc {
   int family;                              /* 0 llama (RMSNorm, RoPE, SwiGLU), 1 gpt2 (LayerNorm, GELU) */
   int n_layers, d_model, n_heads, n_kv_heads, head_dim, ffn, up_dim, vocab;
@@ -256,9 +277,14 @@ typedef struct MaceModelDesc {
   int* last_token;                         /* [slots] previous greedy token of each slot           */
   int* dec_counters; unsigned long long* dec_work;
   int decode_impl;                         /* see MaceAttnArgs */
+  /* per-tenant LoRA (lora_R > 0): the selected layers carry adapters; their base weights (and the norms) are
+   * frozen, grads are NULL except the adapters'; pi_ref = the base model (every adapter masked to zero) */
+  int lora_R, lora_rank; float lora_scale;
+  const MaceLoraLayer* lora;               /* [n_sel] */
 } MaceModelDesc;
 typedef struct MaceSavedActs {             /* policy activations of one selected layer (FT rows)   */
   float* x_in; void* h1; void* qkv; void* o; float* lse; float* x_mid; void* h2; void* u; void* a;
+  void *zm_o, *zm_d;                       /* LoRA: masked shrink outputs of the o / down projections [n, R] bf16 */
 } MaceSavedActs;
 typedef struct MaceTickBuffers {           /* device scratch sized by the caller for this tick;    */
                                            /* ld_vocab: row stride (>= vocab, multiple of 8) of     */
@@ -272,6 +298,8 @@ typedef struct MaceTickBuffers {           /* device scratch sized by the caller
   void* dec_h; float* dec_logits; int* dec_tok; float* dec_ws; size_t dec_ws_bytes;        /* [n_dec, .] */
   float *lp, *ref_lp, *loss, *margin, *coef;  /* [n_pairs][2] / [n_pairs] DPO outputs           */
   float* ws; size_t ws_bytes;              /* split-K / reduction scratch                          */
+  int ld_h;                                /* row stride of h and the saved h1 / h2 (d_model + lora_R; 0 = d)   */
+  float* lz; void *lzm, *ldz;              /* LoRA scratch: Z fp32 [rows, R], Zm / dZ bf16 [rows, R]            */
 } MaceTickBuffers;
 typedef struct MaceTickDesc {              /* device row tables of one tick (see TickBatch)        */
   int T, ft0, n_dec, R, n_pairs, need_ref; /* need_ref 0: ref_cached holds pi_ref log-probs       */
@@ -287,6 +315,7 @@ typedef struct MaceTickDesc {              /* device row tables of one tick (see
   void** attn_events;                      /* optional cudaEvent_t[2*n_layers] around decode attention */
   void** gemm_events; int gemm_events_cap; /* optional cudaEvent_t[2*cap] around every GEMM launch     */
   long long* gemm_flops; int* gemm_count;  /* host: 2*M*N*K per instrumented GEMM, number recorded    */
+  const int* row_tenant;                   /* [T] adapter (tenant) of every row; LoRA only              */
 } MaceTickDesc;
 int mace_model_create(mace_ctx* ctx, const MaceModelDesc* desc, mace_model** out);
 int mace_model_destroy(mace_model* model);

@@ -175,13 +175,39 @@ class OracleModel:
         return lp.gather(1, tgt[:, None]).sum()
 
 
+class Bf16EmulationModel(OracleModel):
+    """The same restatement with every GEMM / attention operand and output rounded to bf16 where the B200 path
+    stores bf16 (norm outputs, projections, attention q/k/v and output, lm_head input) and the residual stream,
+    norm statistics and softmax kept in fp32 -- an INDEPENDENT bf16 implementation (torch) of the same numerics
+    class. The parity tests use its distance to the fp32 oracle as the noise floor of bf16 arithmetic: the
+    device must be no further from fp32 than this (tests/parity_util.py). Autograd through the casts rounds the
+    backward's activations gradients to bf16 as well."""
+
+    def _lin(self, x, name, params):
+        y = (x.to(torch.bfloat16) @ params[name + ".w"].to(torch.bfloat16).t()).float()
+        if self.cfg.has_bias:
+            y = y + params[name + ".b"]
+        return y.to(torch.bfloat16).float()
+
+    def _norm(self, x, name, params):
+        return super()._norm(x, name, params).to(torch.bfloat16).float()
+
+    def attention(self, q, K, V, mask):
+        r = lambda t: t.to(torch.bfloat16).float()  # noqa: E731
+        return r(super().attention(r(q), r(K), r(V), mask))
+
+    def final(self, x, params=None):
+        params = params or self.w
+        return self._norm(x, "final_norm", params) @ params["embed"].to(torch.bfloat16).float().t()
+
+
 class OracleExecutor:
     """Request-level restatement of the GPU hybrid step (prefill / decode / DPO fine-tune)."""
 
-    def __init__(self, cfg, weights, tcfg, selected_names, device: str | torch.device = "cpu"):
+    def __init__(self, cfg, weights, tcfg, selected_names, device: str | torch.device = "cpu", emulate_bf16=False):
         self.cfg = cfg
         self.tcfg = tcfg
-        self.model = OracleModel(cfg, weights, device)
+        self.model = (Bf16EmulationModel if emulate_bf16 else OracleModel)(cfg, weights, device)
         self.selected = list(selected_names)
         self.ref_params = {n: self.model.w[n].clone() for n in self.selected}  # pi_ref frozen at init
         self.master = {n: self.model.w[n].clone() for n in self.selected}
@@ -328,10 +354,10 @@ class TickOracle:
 
     PAGE = 16
 
-    def __init__(self, cfg, weights, tcfg, selected_names, device: str | torch.device = "cpu"):
+    def __init__(self, cfg, weights, tcfg, selected_names, device: str | torch.device = "cpu", emulate_bf16=False):
         self.cfg = cfg
         self.dev = torch.device(device)
-        self.ex = OracleExecutor(cfg, weights, tcfg, selected_names, self.dev)
+        self.ex = OracleExecutor(cfg, weights, tcfg, selected_names, self.dev, emulate_bf16)
         self.model = self.ex.model
         L, H, hd = cfg.n_layers, cfg.n_kv_heads, cfg.head_dim
         self._shape = (L, H, self.PAGE, hd)

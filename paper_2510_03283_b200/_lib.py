@@ -68,6 +68,12 @@ class MaceLayerGrads(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in _LAYER_FIELDS]
 
 
+class MaceLoraLayer(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("a_qkv", "a_o", "a_up", "a_down", "bt_o", "bt_down",
+                                          "g_a_qkv", "g_a_o", "g_a_up", "g_a_down",
+                                          "g_bt_qkv", "g_bt_o", "g_bt_up", "g_bt_down")]
+
+
 class MaceModelDesc(C.Structure):
     _fields_ = [
         ("family", C.c_int), ("n_layers", C.c_int), ("d_model", C.c_int), ("n_heads", C.c_int),
@@ -86,11 +92,13 @@ class MaceModelDesc(C.Structure):
         ("k_pool", C.c_void_p), ("v_pool", C.c_void_p), ("pages_per_layer", C.c_longlong),
         ("last_token", C.c_void_p), ("dec_counters", C.c_void_p), ("dec_work", C.c_void_p),
         ("decode_impl", C.c_int),
+        ("lora_R", C.c_int), ("lora_rank", C.c_int), ("lora_scale", C.c_float),
+        ("lora", C.POINTER(MaceLoraLayer)),
     ]
 
 
 class MaceSavedActs(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in ("x_in", "h1", "qkv", "o", "lse", "x_mid", "h2", "u", "a")]
+    _fields_ = [(n, C.c_void_p) for n in ("x_in", "h1", "qkv", "o", "lse", "x_mid", "h2", "u", "a", "zm_o", "zm_d")]
 
 
 class MaceTickBuffers(C.Structure):
@@ -105,6 +113,8 @@ class MaceTickBuffers(C.Structure):
         ("dec_ws_bytes", C.c_size_t),
         *[(n, C.c_void_p) for n in ("lp", "ref_lp", "loss", "margin", "coef", "ws")],
         ("ws_bytes", C.c_size_t),
+        ("ld_h", C.c_int),
+        *[(n, C.c_void_p) for n in ("lz", "lzm", "ldz")],
     ]
 
 
@@ -124,6 +134,7 @@ class MaceTickDesc(C.Structure):
         ("attn_events", C.c_void_p),
         ("gemm_events", C.c_void_p), ("gemm_events_cap", C.c_int), ("gemm_flops", C.c_void_p),
         ("gemm_count", C.c_void_p),
+        ("row_tenant", C.c_void_p),
     ]
 
 
@@ -155,6 +166,9 @@ SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_attn_fwd": (C.c_int, [_vp, C.POINTER(MaceAttnArgs), _vp]),
     "mace_dpo_fused": (C.c_int, [_vp, _vp, _i, _i, _i, _ip, _ip, _i, _ip, _vp, _f, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _i, _vp]),
+    "mace_lora_mask": (C.c_int, [_vp, _vp, _i, _ip, _i, _i, _i, _f, _vp, _i, _vp]),
+    "mace_adamw_segments": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, C.c_longlong] + [C.c_double] * 5
+                            + [_i, _i, _vp]),
     "mace_dpo_scalar": (C.c_int, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
     "mace_adamw_masked": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_longlong, _vp, _vp, _i, _f, _f, _f, _f, _f, _i, _vp]),
     "mace_adamw_masked2": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_longlong, _vp, _vp, _i] + [C.c_double] * 5

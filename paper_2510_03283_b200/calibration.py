@@ -75,6 +75,10 @@ def measure_rows(model, wl, prefill_tokens=(128, 256, 512, 1024, 2048), decode_b
                  seed=0) -> list[tuple]:
     cfg = model.cfg
     rng = np.random.default_rng(seed)
+    lim = min(model.max_prompt_len, cfg.max_pos - 8)  # prompts the model's page tables / positions can hold
+    prefill_tokens = [n for n in prefill_tokens if n <= lim]
+    decode_ctx = min(decode_ctx, lim)
+    ft_prompt = min(ft_prompt, lim // 2)
     kv = cfg.kv_bytes_per_token()
     rows: list[tuple] = []
     rid = 0

@@ -97,9 +97,27 @@ class TrainConfig:
     eps: float = 1e-8
     weight_decay: float = 0.0
     dpo_beta: float = 1.0             # = AlignmentEnv.beta default (alignment.py:99)
+    # alignment-sensitivity selection (SURVEY §8(c) "optional top-k by ||grad W_l|| / ||W_l||"): when set, the
+    # n_selected_layers top layers are the backward SPAN, and the masked AdamW updates only the k layers of the
+    # span with the largest DPO-gradient-to-weight norm ratio, chosen on the first fine-tune update (after the
+    # gradient all-reduce, so every replica chooses the same) and kept from then on. The final norm stays updated.
+    sensitivity_topk: int | None = None
 
     def selected_layers(self, cfg: ModelConfig) -> list[int]:
         return list(range(cfg.n_layers - self.n_selected_layers, cfg.n_layers))
+
+
+def sensitivity_ranking(grads: dict, weights: dict, layers: list[int]) -> list[tuple[int, float]]:
+    """(layer, ||grad W_l|| / ||W_l||) over the layers' parameter tensors, most sensitive first (ties: lower layer).
+    ``grads`` / ``weights``: name -> tensor (any device); the norms are fp64 sums of squares over every tensor
+    of the layer."""
+    out = []
+    for l in layers:
+        pre = f"layers.{l}."
+        g2 = sum(float(t.double().pow(2).sum()) for n, t in grads.items() if n.startswith(pre))
+        w2 = sum(float(t.double().pow(2).sum()) for n, t in weights.items() if n.startswith(pre))
+        out.append((l, (g2 ** 0.5) / max(w2 ** 0.5, 1e-30)))
+    return sorted(out, key=lambda x: (-x[1], x[0]))
 
 
 def selected_param_names(cfg: ModelConfig, tcfg: TrainConfig) -> list[str]:

@@ -44,6 +44,75 @@ __global__ void embed_kernel(const int* __restrict__ tokens, const int* __restri
   }
 }
 
+// ------------------------------------------------------------------ norm, wide rows (d >= 2048)
+// One 256-thread CTA per row: thread t owns columns 4 (t + 256 j), j < kVec (d = 1024 kVec) -- a few float4 of the
+// row in registers (the warp-per-row kernel below would hold d / 32 floats per lane: 128 at d 4096, which
+// spills or starves occupancy). Statistics through a two-level (warp, then CTA) reduction in fixed order.
+template <int kVec>
+__global__ void __launch_bounds__(256) norm_wide_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ rows,
+                                                        int n_rows, int d, const __nv_bfloat16* __restrict__ w,
+                                                        const __nv_bfloat16* __restrict__ b, int layernorm, float eps,
+                                                        __nv_bfloat16* __restrict__ out, int ldo,
+                                                        float* __restrict__ rstd_out) {
+  __shared__ float red[2][8];
+  const int i = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  uint2 wr[kVec], br[kVec];
+#pragma unroll
+  for (int j = 0; j < kVec; ++j) {  // weights: independent of the previous kernel, fetched before the PDL wait
+    const int c = 4 * (t + 256 * j);
+    wr[j] = *reinterpret_cast<const uint2*>(w + c);
+    br[j] = layernorm ? *reinterpret_cast<const uint2*>(b + c) : make_uint2(0u, 0u);
+  }
+  pdl_wait();
+  pdl_trigger();
+  const float* xr = x + (size_t)(rows ? rows[i] : i) * ldx;
+  float4 v[kVec];
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < kVec; ++j) {
+    v[j] = *reinterpret_cast<const float4*>(xr + 4 * (t + 256 * j));
+    s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+  }
+  float mean = 0.f;
+  if (layernorm) {
+    s = warp_sum(s);
+    if (lane == 0) red[0][warp] = s;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tot += red[0][k];
+    mean = tot / d;
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < kVec; ++j) {
+    const float a = v[j].x - mean, bq = v[j].y - mean, c = v[j].z - mean, e = v[j].w - mean;
+    ss += (a * a + bq * bq) + (c * c + e * e);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) red[1][warp] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) tot += red[1][k];
+  const float rstd = rsqrtf(tot / d + eps);
+  if (rstd_out && t == 0) rstd_out[i] = rstd;
+  __nv_bfloat16* o = out + (size_t)i * ldo;
+#pragma unroll
+  for (int j = 0; j < kVec; ++j) {
+    const __nv_bfloat16* wk = reinterpret_cast<const __nv_bfloat16*>(&wr[j]);
+    const __nv_bfloat16* bk = reinterpret_cast<const __nv_bfloat16*>(&br[j]);
+    const float f[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+    float y[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      y[q] = (f[q] - mean) * rstd * __bfloat162float(wk[q]);
+      if (layernorm) y[q] += __bfloat162float(bk[q]);
+    }
+    *reinterpret_cast<uint2*>(o + 4 * (t + 256 * j)) = make_uint2(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]));
+  }
+}
+
 // ------------------------------------------------------------------ norm (fp32 in -> bf16 out)
 // out[i] = norm(x[rows ? rows[i] : i]); LayerNorm when bias != nullptr semantics chosen by `layernorm`.
 template <int kPerLane>
@@ -122,77 +191,87 @@ __global__ void norm_kernel(const float* __restrict__ x, int ldx, const int* __r
 }
 
 // ------------------------------------------------------------------ RoPE + paged KV write
-// qkv row layout: [q heads | k heads | v heads] x hd (bf16). cos/sin tables [max_pos, hd/2] fp32.
+// qkv row layout: [q heads | k heads | v heads] x hd (bf16). cos/sin tables [n_pos, hd/2] fp32.
 // Row kinds come from the tick's sequence table (MaceSeq). Paged destinations:
 //   prefill row (kind 0), prompt index t: head page = ptab[slot][t/16] * Hkv + h, row t % 16
 //   decode row  (kind 1), decode slot j:  head page = dtab[slot][h][(j - dec_base)/16],  row j % 16
 //   fine-tune row (kind 2): attention reads K/V straight from the qkv rows (no write)
-__global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int T, int Hq, int Hkv, int hd,
-                               const int* __restrict__ row_pos, const int* __restrict__ row_seq,
-                               const int* __restrict__ row_kvi, const MaceSeq* __restrict__ seqs,
-                               const float* __restrict__ cos_t, const float* __restrict__ sin_t, int apply_rope,
-                               const MaceKvLayout kv, __nv_bfloat16* __restrict__ k_pool,
-                               __nv_bfloat16* __restrict__ v_pool) {
-  const int row = blockIdx.x;
-  // the row tables and page tables were written before this tick's first kernel (H2D upload, page
-  // allocation): the destination of each thread's 16-byte chunk is resolved before the PDL wait
-  constexpr int kMaxChunks = 4;  // chunks per thread (Hkv * hd / 8 <= 4 * blockDim.x; checked at launch)
-  long long dst[kMaxChunks];
-  int src[kMaxChunks];
-  int n_chunks = 0;
-  bool paged = false;
-  if (row < T) {
-    const MaceSeq sq = seqs[row_seq[row]];
-    paged = sq.kind != 2 && k_pool != nullptr;
-    if (paged) {
-      const int t = row_kvi[row];
-#pragma unroll
-      for (int j = 0; j < kMaxChunks; ++j) {
-        const int idx = threadIdx.x + j * blockDim.x;
-        dst[j] = 0;
-        src[j] = 0;
-        if (idx < Hkv * (hd / 8)) {
-          const int h = idx / (hd / 8), c = (idx % (hd / 8)) * 8;
-          int page;
-          if (sq.kind == 0) {
-            page = kv.ptab[(size_t)sq.slot * kv.max_prompt_pages + t / kPageTokens] * Hkv + h;
-          } else {
-            const int base = kv.dec_base[sq.slot * Hkv + h];
-            page = kv.dtab[((size_t)sq.slot * Hkv + h) * kv.max_dec_pages + (t - base) / kPageTokens];
-          }
-          dst[j] = ((long long)page * kPageTokens + (t % kPageTokens)) * hd + c;
-          src[j] = h * hd + c;
-          n_chunks = j + 1;
-        }
-      }
-    }
+// One CTA per row; every memory access is 16 bytes. Work items of a row:
+//   rotation items (q and k heads; only with RoPE): 8 consecutive pairs (i, i + hd/2) of one head -- two uint4
+//     loads, two float4 pairs of cos / sin, two uint4 stores back into the row; a k item also stores both rotated
+//     chunks straight into its KV page (no re-read of the row)
+//   copy items: the v heads' 16-byte chunks (and, without RoPE, the k heads' too) -> KV pages
+__device__ __forceinline__ long long kv_page_row(const MaceSeq& sq, const MaceKvLayout& kv, int Hkv, int h, int t,
+                                                 int hd) {
+  int page;
+  if (sq.kind == 0) {
+    page = kv.ptab[(size_t)sq.slot * kv.max_prompt_pages + t / kPageTokens] * Hkv + h;
+  } else {
+    const int base = kv.dec_base[sq.slot * Hkv + h];
+    page = kv.dtab[((size_t)sq.slot * Hkv + h) * kv.max_dec_pages + (t - base) / kPageTokens];
   }
+  return ((long long)page * kPageTokens + (t % kPageTokens)) * hd;
+}
+
+__global__ void __launch_bounds__(128) rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int T, int Hq, int Hkv, int hd,
+                                                      const int* __restrict__ row_pos, const int* __restrict__ row_seq,
+                                                      const int* __restrict__ row_kvi, const MaceSeq* __restrict__ seqs,
+                                                      const float* __restrict__ cos_t, const float* __restrict__ sin_t,
+                                                      int apply_rope, const MaceKvLayout kv,
+                                                      __nv_bfloat16* __restrict__ k_pool,
+                                                      __nv_bfloat16* __restrict__ v_pool) {
+  const int row = blockIdx.x;
+  // row metadata and page tables are written before the tick's first layer: read under the PDL overlap
+  const MaceSeq sq = seqs[row_seq[row]];
+  const bool paged = sq.kind != 2 && k_pool != nullptr;
+  const int t = paged ? row_kvi[row] : 0;
+  const int pos = row_pos[row];
   pdl_wait();
   pdl_trigger();
-  if (row >= T) return;
-  const int W = (Hq + 2 * Hkv) * hd;
-  __nv_bfloat16* r = qkv + (size_t)row * W;
-  const int pos = row_pos[row];
-  const int half = hd / 2;
-  if (apply_rope) {
-    // rotate-half on every (q and k) head; one thread per (head, i < hd/2)
-    const int nh = Hq + Hkv;
-    for (int idx = threadIdx.x; idx < nh * half; idx += blockDim.x) {
-      const int h = idx / half, i = idx % half;
+  const int half = hd / 2, cph = half / 8;  // rotation chunks per head
+  __nv_bfloat16* r = qkv + (size_t)row * (Hq + 2 * Hkv) * hd;
+  const int n_rot = apply_rope ? (Hq + Hkv) * cph : 0;
+  const int n_copy = paged ? (apply_rope ? Hkv : 2 * Hkv) * (hd / 8) : 0;
+  for (int it = threadIdx.x; it < n_rot + n_copy; it += blockDim.x) {
+    if (it < n_rot) {
+      const int h = it / cph, i0 = (it % cph) * 8;
       __nv_bfloat16* base = r + h * hd;
-      const float c = cos_t[(size_t)pos * half + i], s = sin_t[(size_t)pos * half + i];
-      const float x1 = __bfloat162float(base[i]), x2 = __bfloat162float(base[i + half]);
-      base[i] = __float2bfloat16(x1 * c - x2 * s);
-      base[i + half] = __float2bfloat16(x2 * c + x1 * s);
-    }
-    __syncthreads();
-  }
-  if (!paged) return;
+      uint4 a = *reinterpret_cast<const uint4*>(base + i0);
+      uint4 b = *reinterpret_cast<const uint4*>(base + half + i0);
+      const float4* cp = reinterpret_cast<const float4*>(cos_t + (size_t)pos * half + i0);
+      const float4* sp = reinterpret_cast<const float4*>(sin_t + (size_t)pos * half + i0);
+      const float4 c0 = cp[0], c1 = cp[1], s0 = sp[0], s1 = sp[1];
+      const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      const __nv_bfloat16* ah = reinterpret_cast<const __nv_bfloat16*>(&a);
+      const __nv_bfloat16* bh = reinterpret_cast<const __nv_bfloat16*>(&b);
+      float o1[8], o2[8];
 #pragma unroll
-  for (int j = 0; j < kMaxChunks; ++j) {
-    if (j < n_chunks) {
-      *reinterpret_cast<uint4*>(k_pool + dst[j]) = *reinterpret_cast<const uint4*>(r + Hq * hd + src[j]);
-      *reinterpret_cast<uint4*>(v_pool + dst[j]) = *reinterpret_cast<const uint4*>(r + (Hq + Hkv) * hd + src[j]);
+      for (int j = 0; j < 8; ++j) {
+        const float x1 = __bfloat162float(ah[j]), x2 = __bfloat162float(bh[j]);
+        o1[j] = x1 * cs[j] - x2 * sn[j];
+        o2[j] = x2 * cs[j] + x1 * sn[j];
+      }
+      const uint4 p1 = make_uint4(pack_bf16(o1[0], o1[1]), pack_bf16(o1[2], o1[3]), pack_bf16(o1[4], o1[5]),
+                                  pack_bf16(o1[6], o1[7]));
+      const uint4 p2 = make_uint4(pack_bf16(o2[0], o2[1]), pack_bf16(o2[2], o2[3]), pack_bf16(o2[4], o2[5]),
+                                  pack_bf16(o2[6], o2[7]));
+      *reinterpret_cast<uint4*>(base + i0) = p1;
+      *reinterpret_cast<uint4*>(base + half + i0) = p2;
+      if (paged && h >= Hq) {  // a k head: the rotated chunks go to its page as well
+        const long long dst = kv_page_row(sq, kv, Hkv, h - Hq, t, hd);
+        *reinterpret_cast<uint4*>(k_pool + dst + i0) = p1;
+        *reinterpret_cast<uint4*>(k_pool + dst + half + i0) = p2;
+      }
+    } else {
+      const int c = it - n_rot, per = hd / 8;
+      // with RoPE only v heads are copied; without it k heads first, then v heads
+      const int hh = c / per, e = (c % per) * 8;
+      const bool is_v = apply_rope || hh >= Hkv;
+      const int h = apply_rope ? hh : (hh % Hkv);
+      const long long dst = kv_page_row(sq, kv, Hkv, h, t, hd);
+      const uint4 u = *reinterpret_cast<const uint4*>(r + (Hq + (is_v ? Hkv : 0) + h) * hd + e);
+      *reinterpret_cast<uint4*>((is_v ? v_pool : k_pool) + dst + e) = u;
     }
   }
 }
@@ -302,7 +381,19 @@ extern "C" int mace_norm(mace_ctx* ctx, const float* x, int ldx, const int* rows
   auto* B = (const __nv_bfloat16*)b;
   auto* O = (__nv_bfloat16*)out;
   cudaStream_t s = (cudaStream_t)stream;
-  if (per_lane <= 8)
+  if (d % 1024 == 0 && d >= 2048 && d <= 8192 && (ldx % 4) == 0 && (ldo % 4) == 0) {
+#define MACE_NW(K) launch_k(norm_wide_kernel<K>, dim3(n_rows), 256, 0, s, x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out)
+    switch (d / 1024) {
+      case 2: MACE_NW(2); break;
+      case 3: MACE_NW(3); break;
+      case 4: MACE_NW(4); break;
+      case 5: MACE_NW(5); break;
+      case 6: MACE_NW(6); break;
+      case 7: MACE_NW(7); break;
+      default: MACE_NW(8); break;
+    }
+#undef MACE_NW
+  } else if (per_lane <= 8)
     launch_k(norm_kernel<8>, grid, 256, 0, s, x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
   else if (per_lane <= 24)
     launch_k(norm_kernel<24>, grid, 256, 0, s, x, ldx, rows, n_rows, d, W, B, layernorm, eps, O, ldo, rstd_out);
@@ -321,8 +412,7 @@ extern "C" int mace_rope_kv(mace_ctx* ctx, void* qkv, int T, int Hq, int Hkv, in
                             const float* sin_t, int apply_rope, const MaceKvLayout* kv, void* k_pool, void* v_pool,
                             void* stream) {
   if (T <= 0) return 0;
-  if (hd % 8) return mace_fail(ctx, MACE_ERR_ARG, "rope_kv: hd % 8");
-  if (Hkv * (hd / 8) > 4 * 128) return mace_fail(ctx, MACE_ERR_ARG, "rope_kv: Hkv * hd / 8 > 512");
+  if (hd % 16) return mace_fail(ctx, MACE_ERR_ARG, "rope_kv: hd % 16");
   launch_k(rope_kv_kernel, T, 128, 0, (cudaStream_t)stream, (__nv_bfloat16*)qkv, T, Hq, Hkv, hd, row_pos, row_seq, row_kvi,
                                                       seqs, cos_t, sin_t, apply_rope, *kv, (__nv_bfloat16*)k_pool,
                                                       (__nv_bfloat16*)v_pool);

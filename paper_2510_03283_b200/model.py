@@ -24,7 +24,7 @@ import torch
 from ._lib import (Ctx, MaceKvLayout, MaceLayerGrads, MaceLayerWeights, MaceModelDesc, MaceSavedActs,
                    MaceTickBuffers, MaceTickDesc)
 from .batch import PAGE, TickBatch
-from .config import ModelConfig, TrainConfig, selected_param_names
+from .config import ModelConfig, TrainConfig, selected_param_names, sensitivity_ranking
 from .kvmanager import DecodePageMirror
 
 
@@ -88,6 +88,9 @@ class HybridModel:
         self.seg_offsets = torch.from_numpy(offs).to(self.dev)
         self.seg_ptrs = torch.tensor([self.w[n].data_ptr() for n in self.sel], dtype=torch.int64, device=self.dev)
         self.adam_step = 0
+        self.update_layers: list[int] | None = None  # sensitivity selection (TrainConfig.sensitivity_topk)
+        self.update_names = list(self.sel)
+        self.sensitivity: list | None = None
         # the float4 AdamW kernel needs every segment to start on a 4-element boundary of the flat buffers and
         # every bf16 working copy 8-byte aligned (true for every preset: all widths are multiples of 4)
         self.adam_vec4 = bool((offs % 4 == 0).all() and all(self.w[n].data_ptr() % 8 == 0 for n in self.sel))
@@ -533,6 +536,30 @@ class HybridModel:
         return d.data_ptr()
 
     # ------------------------------------------------------------------ fine-tune update
+    def _build_update_runs(self) -> None:
+        """Contiguous runs of the flat optimizer buffers covering the updated parameters (the chosen layers + the
+        final norm), each with its own device segment table: AdamW touches nothing else."""
+        names = [n for n in self.sel if not n.startswith("layers.") or int(n.split(".")[1]) in self.update_layers]
+        idx = {n: i for i, n in enumerate(self.sel)}
+        offs = np.concatenate([[0], np.cumsum([self.w[n].numel() for n in self.sel])]).astype(np.int64)
+        runs, cur = [], []
+        for n in self.sel:
+            if n in names:
+                cur.append(n)
+            elif cur:
+                runs.append(cur)
+                cur = []
+        if cur:
+            runs.append(cur)
+        self._update_runs = []
+        for run in runs:
+            a = int(offs[idx[run[0]]])
+            ro = np.array([offs[idx[n]] - a for n in run] + [offs[idx[run[-1]] + 1] - a], np.int64)
+            self._update_runs.append((a, int(ro[-1]), torch.from_numpy(ro).to(self.dev),
+                                      torch.tensor([self.w[n].data_ptr() for n in run], dtype=torch.int64,
+                                                   device=self.dev), len(run)))
+        self.update_names = names
+
     def idle_update(self) -> None:
         """A lockstep round this replica joins with a drained trace while another replica fine-tunes: zero
         gradients into the same all-reduce, then the same AdamW step (engine.run_ticks)."""
@@ -567,6 +594,19 @@ class HybridModel:
                 torch.distributed.all_reduce(self.grad, group=self.pg)
         self.adam_step += 1
         t = self.tcfg
+        if t.sensitivity_topk is not None:
+            if self.update_layers is None:  # first update: rank the span by ||grad W_l|| / ||W_l|| (host, once)
+                rank = sensitivity_ranking(self.gview, {n: self.w[n] for n in self.sel}, self.sel_layers)
+                self.sensitivity = rank
+                self.update_layers = sorted(l for l, _ in rank[: t.sensitivity_topk])
+                self._build_update_runs()
+            for off, n, offs_dev, ptrs_dev, nseg in self._update_runs:
+                self._chk(L.mace_adamw_masked2(self.ctx.h, self.master.data_ptr() + 4 * off,
+                                               self.m.data_ptr() + 4 * off, self.v.data_ptr() + 4 * off,
+                                               self.grad.data_ptr() + 4 * off, n, offs_dev.data_ptr(),
+                                               ptrs_dev.data_ptr(), nseg, t.lr, t.beta1, t.beta2, t.eps,
+                                               t.weight_decay, self.adam_step, int(self.adam_vec4), s), "adamw")
+            return
         self._chk(L.mace_adamw_masked2(self.ctx.h, self.master.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
                                        self.grad.data_ptr(), self.n_sel, self.seg_offsets.data_ptr(),
                                        self.seg_ptrs.data_ptr(), len(self.sel), t.lr, t.beta1, t.beta2, t.eps,

@@ -52,7 +52,7 @@ def test_ctypes_struct_layouts_match_the_header(tmp_path):
     from paper_2510_03283_b200 import _lib
 
     structs = [_lib.MaceGemmArgs, _lib.MaceKvLayout, _lib.MaceAttnArgs, _lib.MaceLayerWeights, _lib.MaceLayerGrads,
-               _lib.MaceModelDesc, _lib.MaceSavedActs, _lib.MaceTickBuffers, _lib.MaceTickDesc]
+               _lib.MaceModelDesc, _lib.MaceSavedActs, _lib.MaceTickBuffers, _lib.MaceTickDesc, _lib.MaceLoraLayer]
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "mace_b200.h"', "int main(void) {"]
     expect = []
     for st in structs:

@@ -98,7 +98,8 @@ def test_prefix_sharing_splits_and_lru_eviction():
     assert set(int(g) for g in (eng.pool.ref > 0).nonzero()[0]) == trie_groups
 
 
-@pytest.mark.parametrize("policy", ["HybridNoPrefix", "HybridNoPrune", "Periodic", "Sync", "HybridNoBin"])
+@pytest.mark.parametrize("policy", ["Hybrid", "HybridNoPrefix", "HybridNoPrune", "Periodic", "Sync", "HybridNoBin",
+                                    "NoRetrain"])
 def test_baseline_policies_share_execute(policy):
     """Every policy shares _execute: the drop-in runs them unchanged and the
     timeline equals an unmodified reference run."""

@@ -54,7 +54,8 @@ def raw(rep):
 def main():
     OUT.mkdir(exist_ok=True)
     summary = {}
-    for name in ("attn_decode", "gemm", "attn_fa", "attn_decode_tc", "gemm_pair", "attn_fa_c4", "attn_bwd_c4"):
+    for name in ("attn_decode", "gemm", "attn_fa", "attn_decode_tc", "gemm_pair", "attn_fa_c4", "attn_bwd_c4", "adamw",
+                 "paging"):
         rep = SRC / f"{name}.ncu-rep"
         if rep.exists():
             summary[name] = raw(rep)
