@@ -220,6 +220,61 @@ __global__ void __launch_bounds__(256) adamw_vec_kernel(float4* __restrict__ mas
   }
 }
 
+// Sparse segments (per-tenant adapters): virtual index v in [0, n) -> segment s (vstart[s] <= v < vstart[s+1]) ->
+// flat element flat[s] + (v - vstart[s]). VEC: every vstart / flat offset a multiple of 4, float4 streams.
+struct AdamSparse {
+  const long long* vstart;  // [n_seg + 1]
+  const long long* flat;    // [n_seg]
+  __nv_bfloat16* const* weights;
+  int n_seg;
+};
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) adamw_sparse_kernel(float* __restrict__ master, float* __restrict__ m,
+                                                           float* __restrict__ v, const float* __restrict__ grad,
+                                                           long long n, AdamSparse sg, float decay, float w1, float b2,
+                                                           float w2, float step_size, float sbc2, float eps) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ long long vs[65], fl[64];
+  for (int i = threadIdx.x; i <= sg.n_seg && i < 65; i += blockDim.x) {
+    vs[i] = sg.vstart[i];
+    if (i < sg.n_seg) fl[i] = sg.flat[i];
+  }
+  __syncthreads();
+  const int W = VEC ? 4 : 1;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q * W < n; q += (long long)gridDim.x * blockDim.x) {
+    const long long vi = q * W;
+    const int s = seg_of(vs, sg.n_seg, vi);
+    const long long f = fl[s] + (vi - vs[s]);
+    __nv_bfloat16* wp = sg.weights[s] + (vi - vs[s]);
+    if (VEC) {
+      float4 p = *reinterpret_cast<float4*>(master + f), mm = *reinterpret_cast<float4*>(m + f),
+             vv = *reinterpret_cast<float4*>(v + f);
+      const float4 g = *reinterpret_cast<const float4*>(grad + f);
+      adamw_elem(p.x, mm.x, vv.x, g.x, decay, w1, b2, w2, step_size, sbc2, eps);
+      adamw_elem(p.y, mm.y, vv.y, g.y, decay, w1, b2, w2, step_size, sbc2, eps);
+      adamw_elem(p.z, mm.z, vv.z, g.z, decay, w1, b2, w2, step_size, sbc2, eps);
+      adamw_elem(p.w, mm.w, vv.w, g.w, decay, w1, b2, w2, step_size, sbc2, eps);
+      *reinterpret_cast<float4*>(master + f) = p;
+      *reinterpret_cast<float4*>(m + f) = mm;
+      *reinterpret_cast<float4*>(v + f) = vv;
+      __nv_bfloat162 lo = __floats2bfloat162_rn(p.x, p.y), hi = __floats2bfloat162_rn(p.z, p.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(wp) = pk;
+    } else {
+      float p = master[f], mm = m[f], vv = v[f];
+      adamw_elem(p, mm, vv, grad[f], decay, w1, b2, w2, step_size, sbc2, eps);
+      master[f] = p;
+      m[f] = mm;
+      v[f] = vv;
+      *wp = __float2bfloat16_rn(p);
+    }
+  }
+}
+
 // Scalar path (any segment layout)
 __global__ void adamw_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
                              const float* __restrict__ grad, long long n, AdamSeg seg, float decay, float w1,
@@ -308,4 +363,29 @@ extern "C" int mace_adamw_masked2(mace_ctx* ctx, float* master, float* m, float*
   }
   ctx->launches++;
   return mace_check_launch(ctx, "adamw");
+}
+
+extern "C" int mace_adamw_segments(mace_ctx* ctx, float* master, float* m, float* v, const float* grad, int n_seg,
+                                   const long long* seg_vstart, const long long* seg_flat, void* const* seg_weights,
+                                   long long n, double lr, double beta1, double beta2, double eps, double weight_decay,
+                                   int step, int vec4, void* stream) {
+  if (n <= 0 || n_seg <= 0) return 0;
+  if (n_seg > 64) return mace_fail(ctx, MACE_ERR_ARG, "adamw_segments: at most 64 segments");
+  if (step < 1) return mace_fail(ctx, MACE_ERR_ARG, "adamw_segments: step is 1-based");
+  const double bc1 = 1.0 - pow(beta1, step), bc2 = 1.0 - pow(beta2, step);
+  AdamSparse sg{seg_vstart, seg_flat, reinterpret_cast<__nv_bfloat16* const*>(seg_weights), n_seg};
+  const float decay = (float)(1.0 - lr * weight_decay), w1 = (float)(1.0 - beta1), b2 = (float)beta2,
+              w2 = (float)(1.0 - beta2), ss = (float)(lr / bc1), sb = (float)sqrt(bc2), ep = (float)eps;
+  const bool vec = vec4 && n % 4 == 0;  // caller guarantees 4-aligned segments (offsets, lengths, bf16 copies)
+  long long work = vec ? n / 4 : n;
+  long long grid = (work + 255) / 256;
+  if (grid > (long long)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+  if (vec)
+    launch_k(adamw_sparse_kernel<true>, (int)grid, 256, 0, (cudaStream_t)stream, master, m, v, grad, n, sg, decay, w1, b2,
+             w2, ss, sb, ep);
+  else
+    launch_k(adamw_sparse_kernel<false>, (int)grid, 256, 0, (cudaStream_t)stream, master, m, v, grad, n, sg, decay, w1, b2,
+             w2, ss, sb, ep);
+  ctx->launches++;
+  return mace_check_launch(ctx, "adamw_segments");
 }
