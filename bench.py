@@ -143,14 +143,19 @@ def restore(model, snap):
             getattr(model, n).copy_(t)
 
 
-def make_workload(name, rank, seed=None):
-    """The workload's trace for this rank: one independent request stream per GPU, seed = base + rank."""
-    from paper_2510_03283_b200.workloads import WORKLOADS
+def make_workload(name, rank, seed=None, lora_tenants=0, lora_rank=16):
+    """The workload's trace for this rank: one independent request stream per GPU, seed = base + rank. With
+    lora_tenants > 0: that many tenants (the reference's multi-tenant config), each with its own LoRA adapter."""
+    from paper_2510_03283_b200.workloads import WORKLOADS, with_tenants
 
     if name == "c1":
-        return WORKLOADS["c1"]()
-    base = WORKLOADS[name]().seed if seed is None else seed
-    return WORKLOADS[name](seed=base + rank)
+        wl = WORKLOADS["c1"]()
+    else:
+        base = WORKLOADS[name]().seed if seed is None else seed
+        wl = WORKLOADS[name](seed=base + rank)
+    if lora_tenants:
+        wl = with_tenants(wl, [(0.5 - 0.25 * (u % 5), 0.01 * (1 + u % 3)) for u in range(lora_tenants)], lora_rank)
+    return wl
 
 
 def reference_timeline(wl, n_ticks, capture=None):
@@ -209,7 +214,9 @@ def bench_config(wl, args, skip, world):
             "clock": "reference cost model (mode P: bins identical to the unmodified scheduler)",
             "timed_ticks": [a, b], "warmup_ticks": [skip, a],
             "parallelism": f"request-stream replicas x{world} + NCCL bf16 grad all-reduce",
-            "l2": "inputs larger than L2 (weights + KV pages per tick >> 126 MB)"}
+            "l2": "inputs larger than L2 (weights + KV pages per tick >> 126 MB)",
+            **({"lora": {"tenants": wl.n_tenants, "rank": wl.train.lora_rank, "layers": wl.train.n_selected_layers,
+                         "trained": "per-tenant adapters only (base frozen)"}} if wl.train.lora_rank else {})}
 
 
 def run_ours(args, rank, world, lock):
@@ -223,7 +230,7 @@ def run_ours(args, rank, world, lock):
     build()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    wl = make_workload(args.workload, rank, args.seed)
+    wl = make_workload(args.workload, rank, args.seed, args.lora_tenants, args.lora_rank)
     cfg = wl.model
     # the timed window from the reference's own timeline (host only); every rank agrees on the largest skip
     min_skip = wl.bench_skip if args.skip is None else args.skip
@@ -235,7 +242,7 @@ def run_ours(args, rank, world, lock):
     model = HybridModel(cfg, wl.train, w, device=local, max_slots=args.max_slots, max_prompt_len=wl.max_prompt_len,
                         max_decode_steps=wl.sched.max_decode_steps, prompt_groups=kvtok // 16,
                         decode_pages=args.max_slots * cfg.n_kv_heads * wl.decode_pages_per_head,
-                        process_group=lock.grad_group if world > 1 else None)
+                        process_group=lock.grad_group if world > 1 else None, n_tenants=wl.n_tenants)
     del w
     eng = GpuEngine(*wl.engine_args(), model=model, mode="P", lockstep=lock if world > 1 else None)
     eng.keep_outputs = False
@@ -438,7 +445,7 @@ def run_reference(args, rank, world):
 
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
-    wl = make_workload(args.workload, 0, args.seed)
+    wl = make_workload(args.workload, 0, args.seed, args.lora_tenants, args.lora_rank)
     min_skip = wl.bench_skip if args.skip is None else args.skip
     skip, _ = plan_window(wl, args.steps, args.warmup, min_skip)
     warm, timed = _window_compositions(wl, skip, args.warmup, args.steps, wl.model.max_pos)
@@ -457,7 +464,9 @@ def run_reference(args, rank, world):
         "steps": k, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(k, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": bench_config(wl, args, skip, world),
-        "path": "unmodified macesim Engine bins + fp32 CPU oracle on a row sample of each timed tick (oracle/sampled.py)",
+        "path": "unmodified macesim Engine bins + fp32 CPU oracle on a row sample of each timed tick (oracle/sampled.py)"
+                + ("; base-model rows (the tenants' LoRA adapters, ~1-3% of the FLOPs, are not sampled)"
+                   if wl.train.lora_rank else ""),
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
                          "sample": f"{rows} rows of the {k} timed ticks ({args.cpu_rows} per tick, proportional to the "
                                    f"tick's prefill / decode / fine-tune rows) through all {wl.model.n_layers} layers, "
@@ -480,6 +489,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--cpu-rows", type=int, default=128, help="rows of each timed tick the CPU arms execute")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lora-tenants", type=int, default=0, help="per-tenant LoRA adapters: number of tenants (0: off)")
+    ap.add_argument("--lora-rank", type=int, default=16)
     args = ap.parse_args()
     from paper_2510_03283_b200.dist import init_from_env
 

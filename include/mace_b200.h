@@ -211,6 +211,10 @@ int mace_f32_to_bf16(mace_ctx* ctx, const float* x, long long n, void* y, void* 
  * every column 0 -- the pi_ref pass). z fp32 [n, ldz], out bf16 [n, ldo]; R % 8 == 0.                       */
 int mace_lora_mask(mace_ctx* ctx, const float* z, int ldz, const int* tenant, int n, int rank, int R, float scale,
                    void* out, int ldo, void* stream);
+/* LoRA helpers: strided fp32 -> bf16 ([n, cols], cols % 8 == 0), and the scatter of adapter B^T rows [rows, out]
+ * (bf16, row-major) into columns [col0, col0 + rows) of an augmented weight [out, ldd] ([W | B])               */
+int mace_f32_to_bf16_2d(mace_ctx* ctx, const float* x, int ldx, int n, int cols, void* y, int ldy, void* stream);
+int mace_lora_bt_scatter(mace_ctx* ctx, const void* bt, int rows, int out, void* dst, int ldd, int col0, void* stream);
 /* widening copy; with mace_f32_to_bf16 it brackets the bf16 gradient all-reduce of lockstep replicas */
 int mace_bf16_to_f32(mace_ctx* ctx, const void* x, long long n, float* y, void* stream);
 /* attention backward of the dense causal FT sequences: items int4 [n_items] = (seq, kv_head, key_block, steps),
@@ -254,8 +258,10 @@ typedef struct MaceLoraLayer {             /* per-tenant LoRA adapters of one se
                                               R = tenants x rank rows, tenant u owns rows [u*rank, (u+1)*rank)  */
   const void *a_qkv, *a_o, *a_up, *a_down;  /* bf16 [R, in]: the shrink  Z = X A^T                             */
   const void *bt_o, *bt_down;               /* bf16 [R, out]: the expand x += Zm B^T, B^T stored MN-major      */
-  /* qkv / up: B^T lives in the last R columns of the AUGMENTED base weight layers[l].qkv_w / up_w
-   * ([out, in + R]): [X | Zm] . [W | B]^T is one GEMM that keeps the fused bias / GELU / SwiGLU epilogue     */
+  /* qkv / up: B lives in the last R columns of the AUGMENTED base weight layers[l].qkv_w / up_w
+   * ([out, in + R], row stride in + R): [X | Zm] . [W | B]^T is one GEMM that keeps the fused bias / GELU /
+   * SwiGLU epilogue.  o / down: A is STACKED under the base weight (a_o == o_w + d_model * in, same for down):
+   * the backward's dX = [dY | dZ] . [W; A] is one GEMM into the bf16 activation gradient.                   */
   float *g_a_qkv, *g_a_o, *g_a_up, *g_a_down;       /* fp32 [R, in] grads (views of the flat gradient)       */
   float *g_bt_qkv, *g_bt_o, *g_bt_up, *g_bt_down;   /* fp32 [R, out]                                        */
 } MaceLoraLayer;

@@ -80,10 +80,28 @@ class _Seq:
 class OracleModel:
     """fp32 CPU decoder: Llama (RMSNorm/RoPE/GQA/SwiGLU) or GPT-2 (LayerNorm/learned pos/GELU/bias)."""
 
-    def __init__(self, cfg, weights: dict[str, torch.Tensor], device: str | torch.device = "cpu"):
+    def __init__(self, cfg, weights: dict[str, torch.Tensor], device: str | torch.device = "cpu", lora_rank: int = 0,
+                 lora_scale: float = 0.0):
         self.cfg = cfg
         self.dev = torch.device(device)
         self.w = {k: v.detach().to(self.dev, torch.float32).clone() for k, v in weights.items()}
+        # per-tenant LoRA (weights hold "lora.{l}.a_{p}" [R, in] / "lora.{l}.bt_{p}" [R, out], tenants stacked)
+        self.lora_rank, self.lora_scale = lora_rank, lora_scale
+
+    def _adapter(self, X, l, proj, params, tenant):
+        """(alpha / r) * mask_tenant(X A^T) B^T: each row uses only its own tenant's rank-r block (LoRA,
+        PAPER.md:440-441); tenant None (pi_ref, the frozen base model) -> no adapter."""
+        key = f"lora.{l}.a_{proj}"
+        if tenant is None or not self.lora_rank or key not in params:
+            return None
+        A, Bt = params[key], params[f"lora.{l}.bt_{proj}"]
+        Z = X @ A.t()
+        cols = torch.arange(A.shape[0], device=X.device) // self.lora_rank
+        mask = (cols[None, :] == tenant[:, None]).to(Z.dtype)
+        return self._round_z(self.lora_scale * Z * mask) @ Bt
+
+    def _round_z(self, z):
+        return z
 
     # -- one decoder layer over rows x [n, d]; kv_ctx(l, k_new, v_new) -> (K [m,Hkv,hd], V, mask [n,Hkv?,m])
     def _norm(self, x, name, params):
@@ -92,8 +110,10 @@ class OracleModel:
             return rms_norm(x, params[name + ".w"], c.norm_eps)
         return layer_norm(x, params[name + ".w"], params[name + ".b"], c.norm_eps)
 
-    def _lin(self, x, name, params):
+    def _lin(self, x, name, params, extra=None):
         y = x @ params[name + ".w"].t()
+        if extra is not None:
+            y = y + extra
         if self.cfg.has_bias:
             y = y + params[name + ".b"]
         return y
@@ -105,13 +125,13 @@ class OracleModel:
             x = x + params["pos_embed"][torch.as_tensor(pos, dtype=torch.long, device=self.dev)]
         return x
 
-    def layer(self, l, x, pos, attend, params=None):
-        """attend(l, q[n,Hq,hd], k[n,Hkv,hd], v) -> o [n, Hq, hd]"""
+    def layer(self, l, x, pos, attend, params=None, tenant=None):
+        """attend(l, q[n,Hq,hd], k[n,Hkv,hd], v) -> o [n, Hq, hd]; tenant: LongTensor [n] (LoRA rows) or None"""
         c = self.cfg
         params = params or self.w
         p = f"layers.{l}."
         h = self._norm(x, p + "attn_norm", params)
-        qkv = self._lin(h, p + "qkv", params)
+        qkv = self._lin(h, p + "qkv", params, self._adapter(h, l, "qkv", params, tenant))
         Hq, Hk, hd = c.n_heads, c.n_kv_heads, c.head_dim
         q = qkv[:, : Hq * hd].reshape(-1, Hq, hd)
         k = qkv[:, Hq * hd: (Hq + Hk) * hd].reshape(-1, Hk, hd)
@@ -120,15 +140,20 @@ class OracleModel:
             pos_t = torch.as_tensor(pos, dtype=torch.long, device=self.dev)
             q = rope(q, pos_t, c.rope_theta)
             k = rope(k, pos_t, c.rope_theta)
-        o = attend(l, q, k, v)
-        x = x + self._lin(o.reshape(-1, Hq * hd), p + "o", params)
+        o = attend(l, q, k, v).reshape(-1, Hq * hd)
+        x = x + self._lin(o, p + "o", params)
+        ad = self._adapter(o, l, "o", params, tenant)
+        if ad is not None:
+            x = x + ad
         h = self._norm(x, p + "mlp_norm", params)
-        u = self._lin(h, p + "up", params)
+        u = self._lin(h, p + "up", params, self._adapter(h, l, "up", params, tenant))
         if c.family == "llama":
             a = F.silu(u[:, : c.ffn]) * u[:, c.ffn:]
         else:
             a = gelu_tanh(u)
-        return x + self._lin(a, p + "down", params)
+        x = x + self._lin(a, p + "down", params)
+        ad = self._adapter(a, l, "down", params, tenant)
+        return x if ad is None else x + ad
 
     def final(self, x, params=None):
         params = params or self.w
@@ -147,8 +172,10 @@ class OracleModel:
         return torch.einsum("nhm,mhd->nhd", p, Vx)
 
     # -- full causal sequence (prefill, fine-tune); returns hidden [n, d] and per-layer (k, v)
-    def forward_seq(self, tokens, pos0=0, params=None, collect_kv=False):
+    def forward_seq(self, tokens, pos0=0, params=None, collect_kv=False, tenant=None):
         n = len(tokens)
+        if tenant is not None:
+            tenant = torch.full((n,), int(tenant), dtype=torch.long, device=self.dev)
         pos = list(range(pos0, pos0 + n))
         x = self.embed(tokens, pos, params)
         causal = torch.tril(torch.ones(n, n, dtype=torch.bool, device=self.dev))
@@ -161,13 +188,14 @@ class OracleModel:
             return self.attention(q, k, v, mask)
 
         for l in range(self.cfg.n_layers):
-            x = self.layer(l, x, pos, attend, params)
+            x = self.layer(l, x, pos, attend, params, tenant)
         return x, kvs
 
-    def seq_logprob(self, prompt, response, params=None):
-        """Sum of log p(response | prompt) under ``params``; response token i predicted at P+i-1."""
+    def seq_logprob(self, prompt, response, params=None, tenant=None):
+        """Sum of log p(response | prompt) under ``params`` (and the tenant's adapter, LoRA); response token i
+        predicted at P+i-1."""
         toks = list(prompt) + list(response)
-        h, _ = self.forward_seq(toks, params=params)
+        h, _ = self.forward_seq(toks, params=params, tenant=tenant)
         P = len(prompt)
         logits = self.final(h[P - 1: P - 1 + len(response)], params)
         lp = torch.log_softmax(logits, dim=-1)
@@ -183,14 +211,19 @@ class Bf16EmulationModel(OracleModel):
     device must be no further from fp32 than this (tests/parity_util.py). Autograd through the casts rounds the
     backward's activations gradients to bf16 as well."""
 
-    def _lin(self, x, name, params):
+    def _lin(self, x, name, params, extra=None):
         y = (x.to(torch.bfloat16) @ params[name + ".w"].to(torch.bfloat16).t()).float()
+        if extra is not None:
+            y = y + extra
         if self.cfg.has_bias:
             y = y + params[name + ".b"]
         return y.to(torch.bfloat16).float()
 
     def _norm(self, x, name, params):
         return super()._norm(x, name, params).to(torch.bfloat16).float()
+
+    def _round_z(self, z):
+        return z.to(torch.bfloat16).float()
 
     def attention(self, q, K, V, mask):
         r = lambda t: t.to(torch.bfloat16).float()  # noqa: E731
@@ -207,9 +240,13 @@ class OracleExecutor:
     def __init__(self, cfg, weights, tcfg, selected_names, device: str | torch.device = "cpu", emulate_bf16=False):
         self.cfg = cfg
         self.tcfg = tcfg
-        self.model = (Bf16EmulationModel if emulate_bf16 else OracleModel)(cfg, weights, device)
+        self.lora_rank = getattr(tcfg, "lora_rank", None) or 0
+        self.model = (Bf16EmulationModel if emulate_bf16 else OracleModel)(
+            cfg, weights, device, self.lora_rank, tcfg.lora_alpha / self.lora_rank if self.lora_rank else 0.0)
         self.selected = list(selected_names)
-        self.ref_params = {n: self.model.w[n].clone() for n in self.selected}  # pi_ref frozen at init
+        # pi_ref frozen at init; LoRA: pi_ref is the frozen base model (every adapter off)
+        self.ref_params = {} if self.lora_rank else {n: self.model.w[n].clone() for n in self.selected}
+        self.tenant_steps: dict[int, int] = {}
         self.master = {n: self.model.w[n].clone() for n in self.selected}
         self.m = {n: torch.zeros_like(self.master[n]) for n in self.selected}
         self.v = {n: torch.zeros_like(self.master[n]) for n in self.selected}
@@ -267,11 +304,16 @@ class OracleExecutor:
         self.seqs.pop(rid, None)
 
     # ---------------------------------------------------------------- fine-tune rows
-    def dpo_step(self, pairs: list[tuple[int, list[int], list[int], list[int]]]):
+    def dpo_step(self, pairs: list[tuple[int, list[int], list[int], list[int]]], coef_margins=None):
         """One optimizer step on mean_i softplus(-beta * m_i) over the tick's FT pairs.
 
-        pairs: (rid, prompt, chosen, rejected). m_i = (lp_c - ref_c) - (lp_r - ref_r) with ref log-probs
-        under the frozen pi_ref, computed once per pair (alignment.py:39-47 for the scalar stage).
+        pairs: (rid, prompt, chosen, rejected[, tenant]). m_i = (lp_c - ref_c) - (lp_r - ref_r) with ref log-probs
+        under the frozen pi_ref, computed once per pair (alignment.py:39-47 for the scalar stage). LoRA: the policy
+        runs with the pair's tenant adapter, pi_ref without adapters.
+        coef_margins: when given (the device's per-pair margins), the gradient is taken at THOSE margins -- the
+        loss's outer derivative -beta * sigma(-beta * m_i) / n uses m_i = coef_margins[i] -- so a gradient comparison
+        isolates the backward from the forward's margin rounding noise (the reported losses / margins stay the
+        oracle's own).
         Returns per-pair (loss, margin) and the gradients of the selected parameters.
         """
         beta = self.tcfg.dpo_beta
@@ -282,7 +324,9 @@ class OracleExecutor:
         ref.update(self.ref_params)
         losses, margins, total = [], [], 0.0
         self.last_lp = []
-        for rid, prompt, chosen, rejected in pairs:
+        for pr in pairs:
+            rid, prompt, chosen, rejected = pr[:4]
+            ten = (pr[4] if len(pr) > 4 else 0) if self.lora_rank else None
             if rid not in self.ref_lp_cache:
                 with torch.no_grad():
                     self.ref_lp_cache[rid] = (
@@ -290,11 +334,15 @@ class OracleExecutor:
                         float(self.model.seq_logprob(prompt, rejected, ref)),
                     )
             rc, rr = self.ref_lp_cache[rid]
-            lc = self.model.seq_logprob(prompt, chosen, params)
-            lr_ = self.model.seq_logprob(prompt, rejected, params)
+            lc = self.model.seq_logprob(prompt, chosen, params, tenant=ten)
+            lr_ = self.model.seq_logprob(prompt, rejected, params, tenant=ten)
             m = (lc - rc) - (lr_ - rr)
             loss = F.softplus(-beta * m)
-            total = total + loss / len(pairs)
+            if coef_margins is None:
+                total = total + loss / len(pairs)
+            else:  # d softplus(-beta m) / dm at the given margin, times m (a surrogate with that gradient)
+                mi = float(coef_margins[len(losses)])
+                total = total + (-beta * torch.sigmoid(torch.tensor(-beta * mi, dtype=m.dtype))) * m / len(pairs)
             losses.append(float(loss.detach()))
             margins.append(float(m.detach()))
             self.last_lp.append((float(lc.detach()), float(lr_.detach()), rc, rr))
@@ -316,9 +364,21 @@ class OracleExecutor:
             self.model.w[n] = self.master[n].to(torch.bfloat16).float()
             off += k
 
-    def adamw(self, grads: dict[str, torch.Tensor]) -> None:
-        """torch.optim.AdamW update order on fp32 masters; working weights = bf16(master)."""
+    def adamw(self, grads: dict[str, torch.Tensor], tenants=None) -> None:
+        """torch.optim.AdamW update order on fp32 masters; working weights = bf16(master). LoRA: one optimizer per
+        tenant -- only the stepping tenants' adapter rows move, each with its own step count."""
         t = self.tcfg
+        if self.lora_rank:
+            r = self.lora_rank
+            for u in sorted(set(tenants or [])):
+                k = self.tenant_steps[u] = self.tenant_steps.get(u, 0) + 1
+                bc1, bc2 = 1.0 - t.beta1 ** k, 1.0 - t.beta2 ** k
+                rows = slice(u * r, (u + 1) * r)
+                for n in self.selected:
+                    adamw_reference(self.master[n][rows], self.m[n][rows], self.v[n][rows], grads[n][rows], t.lr,
+                                    t.beta1, t.beta2, t.eps, t.weight_decay, bc1, bc2)
+                    self.model.w[n] = self.master[n].to(torch.bfloat16).float()
+            return
         self.step += 1
         bc1 = 1.0 - t.beta1 ** self.step
         bc2 = 1.0 - t.beta2 ** self.step
@@ -381,8 +441,9 @@ class TickOracle:
             self.vstore = torch.cat([self.vstore, z.clone()])
         return torch.tensor([self.gslot[g] for g in groups], dtype=torch.long, device=self.dev)
 
-    def run_tick(self, batch, gpu_tokens, kept_post):
-        """Returns (decode logits [n_dec, V], FT (losses, margins, grads) or None)."""
+    def run_tick(self, batch, gpu_tokens, kept_post, ft_margins=None):
+        """Returns (decode logits [n_dec, V], FT (losses, margins, grads) or None). ft_margins: the device's
+        per-pair margins -- gradients are then taken at them (OracleExecutor.dpo_step coef_margins)."""
         c = self.cfg
         H, P16 = c.n_kv_heads, self.PAGE
         for slot, row in zip(batch.ptab_slots.tolist(), batch.ptab_rows.tolist()):
@@ -459,8 +520,11 @@ class TickOracle:
                         o[q0: q0 + 1] = self.model.attention(q[q0: q0 + 1], K, V, mask)
                 return o
 
+            rt = getattr(batch, "row_tenant", None)
+            ten = (torch.as_tensor(rt[:ft0].astype(np.int64), device=self.dev)
+                   if self.ex.lora_rank and rt is not None and rt.size else None)
             for l in range(c.n_layers):
-                x = self.model.layer(l, x, pos, attend)
+                x = self.model.layer(l, x, pos, attend, tenant=ten)
             if batch.n_dec:
                 logits = self.model.final(x[batch.dec_rows.tolist()]).cpu()
         # teacher forcing: the next decode input of each slot is the GPU's greedy token
@@ -473,9 +537,9 @@ class TickOracle:
             d["first"] = [max(f, end - kk) for f, kk in zip(d["first"], kept)]
         ft = None
         if batch.ft_pairs:
-            pairs = [(p.rid, p.prompt, p.chosen, p.rejected) for p in batch.ft_pairs]
-            losses, margins, grads = self.ex.dpo_step(pairs)
+            pairs = [(p.rid, p.prompt, p.chosen, p.rejected, getattr(p, "tenant", 0)) for p in batch.ft_pairs]
+            losses, margins, grads = self.ex.dpo_step(pairs, coef_margins=ft_margins)
             grads = {n: g.cpu() for n, g in grads.items()}
-            self.ex.adamw({n: g.to(self.dev) for n, g in grads.items()})
+            self.ex.adamw({n: g.to(self.dev) for n, g in grads.items()}, tenants=[p[4] for p in pairs])
             ft = (losses, margins, grads)
         return logits, ft

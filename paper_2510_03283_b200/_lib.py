@@ -167,6 +167,8 @@ SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_dpo_fused": (C.c_int, [_vp, _vp, _i, _i, _i, _ip, _ip, _i, _ip, _vp, _f, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _i, _vp]),
     "mace_lora_mask": (C.c_int, [_vp, _vp, _i, _ip, _i, _i, _i, _f, _vp, _i, _vp]),
+    "mace_f32_to_bf16_2d": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _i, _vp]),
+    "mace_lora_bt_scatter": (C.c_int, [_vp, _vp, _i, _i, _vp, _i, _i, _vp]),
     "mace_adamw_segments": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, C.c_longlong] + [C.c_double] * 5
                             + [_i, _i, _vp]),
     "mace_dpo_scalar": (C.c_int, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp]),

@@ -25,6 +25,7 @@ class FtPair:
     chosen: list[int]
     rejected: list[int]
     ref_lp: tuple[float, float] | None = None   # cached pi_ref log-probs (None: computed this tick)
+    tenant: int = 0                              # Request.tenant (workload.py:71): whose adapter it trains (LoRA)
 
 
 @dataclass
@@ -52,6 +53,7 @@ class TickBatch:
     ft_tc_items: np.ndarray = field(default_factory=lambda: np.zeros((0, 4), np.int32))
     ft_row_seq: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
     bwd_items: np.ndarray = field(default_factory=lambda: np.zeros((0, 4), np.int32))  # (ft seq, kv_head, kblock, 0)
+    row_tenant: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))  # [T] Request.tenant per row
     # accounting (tokens processed by the hybrid iteration)
     n_prefill_tokens: int = 0
     n_decode_tokens: int = 0
@@ -90,6 +92,7 @@ class TickBatch:
             ("row_ps", self.row_ps), ("ft_seqs", self.ft_seqs), ("ft_tc_items", self.ft_tc_items),
             ("ft_row_seq", self.ft_row_seq), ("bwd_items", self.bwd_items),
             ("ft_local_rows", local_rows), ("ref_cached", ref_cached),  # fp32 bits of cached pi_ref log-probs
+            ("row_tenant", self.row_tenant),
         ]
         layout = {}
         off = 0

@@ -102,9 +102,39 @@ class TrainConfig:
     # span with the largest DPO-gradient-to-weight norm ratio, chosen on the first fine-tune update (after the
     # gradient all-reduce, so every replica chooses the same) and kept from then on. The final norm stays updated.
     sensitivity_topk: int | None = None
+    # per-tenant LoRA adapters (the paper's per-user adapter phi_u over a frozen shared base,
+    # PAPER.md:440-441): when set, every selected layer's qkv / o / up / down projection carries one rank-r adapter
+    # per tenant (y = x W^T + (alpha / r) (x A_u^T) B_u^T for the rows of tenant u), the base model and the norms are
+    # frozen, pi_ref is the base model (every adapter off), and each tenant's adapter is trained only by that
+    # tenant's preference pairs with its own AdamW step count. B starts at zero, so pi_theta == pi_ref at first.
+    lora_rank: int | None = None
+    lora_alpha: float = 16.0
+    lora_init_std: float = 0.02
 
     def selected_layers(self, cfg: ModelConfig) -> list[int]:
         return list(range(cfg.n_layers - self.n_selected_layers, cfg.n_layers))
+
+    @property
+    def lora_scale(self) -> float:
+        return self.lora_alpha / self.lora_rank if self.lora_rank else 0.0
+
+
+LORA_PROJ = ("qkv", "o", "up", "down")
+
+
+def lora_shapes(cfg: ModelConfig, tcfg: TrainConfig, n_tenants: int) -> dict[str, tuple[int, int]]:
+    """Stacked adapters of every selected layer, flat-buffer order: a_* [R, in] then bt_* [R, out] per projection,
+    R = n_tenants * rank; tenant u owns rows [u * rank, (u + 1) * rank) of each."""
+    R = n_tenants * tcfg.lora_rank
+    d, ho = cfg.d_model, cfg.n_heads * cfg.head_dim
+    io = {"qkv": (d, cfg.qkv_dim), "o": (ho, d), "up": (d, cfg.up_dim), "down": (cfg.ffn, d)}
+    out = {}
+    for l in tcfg.selected_layers(cfg):
+        for p in LORA_PROJ:
+            i, o = io[p]
+            out[f"lora.{l}.a_{p}"] = (R, i)
+            out[f"lora.{l}.bt_{p}"] = (R, o)
+    return out
 
 
 def sensitivity_ranking(grads: dict, weights: dict, layers: list[int]) -> list[tuple[int, float]]:
@@ -118,6 +148,13 @@ def sensitivity_ranking(grads: dict, weights: dict, layers: list[int]) -> list[t
         w2 = sum(float(t.double().pow(2).sum()) for n, t in weights.items() if n.startswith(pre))
         out.append((l, (g2 ** 0.5) / max(w2 ** 0.5, 1e-30)))
     return sorted(out, key=lambda x: (-x[1], x[0]))
+
+
+def trainable_param_names(cfg: ModelConfig, tcfg: TrainConfig, n_tenants: int = 1) -> list[str]:
+    """Names of the flat optimizer buffers: the per-tenant adapters (LoRA mode) or the selected base parameters."""
+    if tcfg.lora_rank:
+        return list(lora_shapes(cfg, tcfg, n_tenants))
+    return selected_param_names(cfg, tcfg)
 
 
 def selected_param_names(cfg: ModelConfig, tcfg: TrainConfig) -> list[str]:

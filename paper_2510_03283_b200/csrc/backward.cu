@@ -430,8 +430,11 @@ extern "C" int mace_norm_bwd(mace_ctx* ctx, const float* x, int ldx, const int* 
   else if (per_lane <= 128) MACE_NB(128);
   else return mace_fail(ctx, MACE_ERR_ARG, "norm_bwd: d too large");
 #undef MACE_NB
-  launch_k(col_reduce_kernel, (d + 31) / 32, 256, 0, s, workspace, nb, 2 * d, d, dw);
-  ctx->launches += 2;
+  ctx->launches++;
+  if (dw) {  // NULL: frozen norm (LoRA mode trains only the adapters)
+    launch_k(col_reduce_kernel, (d + 31) / 32, 256, 0, s, workspace, nb, 2 * d, d, dw);
+    ctx->launches++;
+  }
   if (layernorm && db) {
     launch_k(col_reduce_kernel, (d + 31) / 32, 256, 0, s, workspace + d, nb, 2 * d, d, db);
     ctx->launches++;

@@ -28,6 +28,7 @@ struct ModelState {
   std::vector<MaceLayerWeights> layers, ref_layers;
   std::vector<MaceLayerGrads> grads;
   std::vector<int> sel;
+  std::vector<MaceLoraLayer> lora;     // [n_sel] per-tenant adapters (LoRA mode), else empty
   const MaceTickDesc* tick = nullptr;  // the tick being issued (optional GEMM event instrumentation)
 };
 
@@ -45,6 +46,10 @@ struct LayerIO {
   float* x_in;    // != NULL: copy of the layer input (backward)
   float* x_mid;   // != NULL: copy of the residual after attention (backward)
   bool keep_u;    // pre-activation needed (backward): no GELU fusion
+  const MaceLoraLayer* lora;  // != NULL: this layer carries the tenants' adapters (h1 / h2 rows are d + R wide)
+  const int* tenant;          // LoRA: adapter of each row; NULL masks every adapter (the base model = pi_ref)
+  void* zm_o;                 // LoRA: masked shrink outputs of the o / down projections [rows, R] (saved: backward)
+  void* zm_d;
 };
 
 struct AttnRows {
@@ -102,6 +107,15 @@ static int gemm(ModelState& m, const MaceTickBuffers* b, cudaStream_t s, const v
   return rc;
 }
 
+// LoRA shrink of `rows` rows: Zm = bf16(scale * mask_tenant(X A_all^T)) into out (ld ldo). One GEMM for every
+// tenant's block at once (N = R), then the row mask keeps each row's own tenant block (lora.cu).
+static int lora_shrink(ModelState& m, const MaceTickBuffers* b, cudaStream_t s, const void* X, int ldx, const void* A,
+                       int K, int rows, const int* tenant, void* out, int ldo) {
+  const int R = m.d.lora_R;
+  MACE_TRY(gemm(m, b, s, X, ldx, false, A, K, false, rows, R, K, b->lz, R, MACE_EPI_F32, nullptr));
+  return mace_lora_mask(m.ctx, b->lz, R, tenant, rows, m.d.lora_rank, R, m.d.lora_scale, out, ldo, s);
+}
+
 static int copy(ModelState& m, void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return 0;
   if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
@@ -121,12 +135,14 @@ static int layer_fwd(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc
   const MaceModelDesc& d = m.d;
   const int D = d.d_model, HO = d.n_heads * d.head_dim, QKV = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
   const int ln = d.family == 1;
+  const int R = io.lora ? d.lora_R : 0, ldh = D + R;  // LoRA: [h | Zm] rows feed the augmented qkv / up weights
   const size_t page_elems = (size_t)kPageTokens * d.head_dim;
   void* kp = ar.paged ? (void*)((char*)d.k_pool + (size_t)l * d.pages_per_layer * page_elems * kBf) : nullptr;
   void* vp = ar.paged ? (void*)((char*)d.v_pool + (size_t)l * d.pages_per_layer * page_elems * kBf) : nullptr;
   if (io.x_in) MACE_TRY(copy(m, io.x_in, io.x, (size_t)T * D * 4, s));
-  MACE_TRY(mace_norm(m.ctx, io.x, D, nullptr, T, D, W.attn_norm_w, W.attn_norm_b, ln, d.norm_eps, io.h1, D, nullptr, s));
-  MACE_TRY(gemm(m, b, s, io.h1, D, false, W.qkv_w, D, false, T, QKV, D, io.qkv, QKV, MACE_EPI_BF16, W.qkv_b));
+  MACE_TRY(mace_norm(m.ctx, io.x, D, nullptr, T, D, W.attn_norm_w, W.attn_norm_b, ln, d.norm_eps, io.h1, ldh, nullptr, s));
+  if (R) MACE_TRY(lora_shrink(m, b, s, io.h1, ldh, io.lora->a_qkv, D, T, io.tenant, (char*)io.h1 + D * kBf, ldh));
+  MACE_TRY(gemm(m, b, s, io.h1, ldh, false, W.qkv_w, ldh, false, T, QKV, D + R, io.qkv, QKV, MACE_EPI_BF16, W.qkv_b));
   MACE_TRY(mace_rope_kv(m.ctx, io.qkv, T, d.n_heads, d.n_kv_heads, d.head_dim, ar.pos, ar.row_seq, ar.row_kvi, ar.seqs,
                         d.cos_t, d.sin_t, d.family == 0, &d.kv, kp, vp, s));
   MaceAttnArgs a{};
@@ -171,17 +187,28 @@ static int layer_fwd(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc
     MACE_TRY(mace_attn_fwd(m.ctx, &a, s));
   }
   MACE_TRY(gemm(m, b, s, io.o, HO, false, W.o_w, HO, false, T, D, HO, io.x, D, MACE_EPI_F32_ADD, W.o_b));
+  if (R) {  // x += Zm_o B_o^T (B^T [R, D] read MN-major)
+    MACE_TRY(lora_shrink(m, b, s, io.o, HO, io.lora->a_o, HO, T, io.tenant, io.zm_o, R));
+    MACE_TRY(gemm(m, b, s, io.zm_o, R, false, io.lora->bt_o, D, true, T, D, R, io.x, D, MACE_EPI_F32_ADD, nullptr));
+  }
   if (io.x_mid) MACE_TRY(copy(m, io.x_mid, io.x, (size_t)T * D * 4, s));
-  MACE_TRY(mace_norm(m.ctx, io.x, D, nullptr, T, D, W.mlp_norm_w, W.mlp_norm_b, ln, d.norm_eps, io.h2, D, nullptr, s));
+  MACE_TRY(mace_norm(m.ctx, io.x, D, nullptr, T, D, W.mlp_norm_w, W.mlp_norm_b, ln, d.norm_eps, io.h2, ldh, nullptr, s));
+  if (R) MACE_TRY(lora_shrink(m, b, s, io.h2, ldh, io.lora->a_up, D, T, io.tenant, (char*)io.h2 + D * kBf, ldh));
   if (ln && !io.keep_u) {  // GPT-2: GELU fused into the up-projection epilogue
-    MACE_TRY(gemm(m, b, s, io.h2, D, false, W.up_w, D, false, T, d.ffn, D, io.a, d.ffn, MACE_EPI_BF16_GELU, W.up_b));
+    MACE_TRY(gemm(m, b, s, io.h2, ldh, false, W.up_w, ldh, false, T, d.ffn, D + R, io.a, d.ffn, MACE_EPI_BF16_GELU, W.up_b));
   } else if (!ln && !io.keep_u) {  // Llama: SwiGLU fused (gate / up halves of one accumulator tile)
-    MACE_TRY(gemm(m, b, s, io.h2, D, false, W.up_w, D, false, T, d.ffn, D, io.a, d.ffn, MACE_EPI_BF16_SWIGLU, nullptr));
+    MACE_TRY(gemm(m, b, s, io.h2, ldh, false, W.up_w, ldh, false, T, d.ffn, D + R, io.a, d.ffn, MACE_EPI_BF16_SWIGLU,
+                  nullptr));
   } else {
-    MACE_TRY(gemm(m, b, s, io.h2, D, false, W.up_w, D, false, T, d.up_dim, D, io.u, d.up_dim, MACE_EPI_BF16, W.up_b));
+    MACE_TRY(gemm(m, b, s, io.h2, ldh, false, W.up_w, ldh, false, T, d.up_dim, D + R, io.u, d.up_dim, MACE_EPI_BF16,
+                  W.up_b));
     MACE_TRY(mace_act(m.ctx, io.u, T, d.ffn, d.family == 0, io.a, s));
   }
   MACE_TRY(gemm(m, b, s, io.a, d.ffn, false, W.down_w, d.ffn, false, T, D, d.ffn, io.x, D, MACE_EPI_F32_ADD, W.down_b));
+  if (R) {
+    MACE_TRY(lora_shrink(m, b, s, io.a, d.ffn, io.lora->a_down, d.ffn, T, io.tenant, io.zm_d, R));
+    MACE_TRY(gemm(m, b, s, io.zm_d, R, false, io.lora->bt_down, D, true, T, D, R, io.x, D, MACE_EPI_F32_ADD, nullptr));
+  }
   return 0;
 }
 
@@ -195,6 +222,12 @@ static int sub_pass(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc*
   for (size_t i = 0; i < m.sel.size(); ++i) {
     LayerIO io{};
     io.x = x;
+    if (!m.lora.empty()) {  // pi_ref = the base model: every adapter masked (tenant NULL), same kernels
+      io.lora = &m.lora[i];
+      io.tenant = policy && t->row_tenant ? t->row_tenant + t->ft0 : nullptr;
+      io.zm_o = policy ? b->sav[i].zm_o : b->lzm;
+      io.zm_d = policy ? b->sav[i].zm_d : b->lzm;
+    }
     if (policy) {
       const MaceSavedActs& sv = b->sav[i];
       io.h1 = sv.h1;
@@ -230,8 +263,69 @@ static int colsum(ModelState& m, const MaceTickBuffers* b, const void* y16, int 
   return mace_colsum_bf16(m.ctx, y16, n, N, N, out, b->ws, b->ws_bytes, s);
 }
 
+// LoRA layer backward (base weights and norms frozen): dx -> grad wrt the layer input; the adapters' dA / dB^T into
+// the flat gradient. Per projection with input X, Zm = s * mask(X A^T), Y = X W^T + Zm B^T:
+//   dB^T += Zm^T dY,  dZ = s * mask(dY B),  dA += dZ^T X,  dX = dY W + dZ A
+// o / down: dY goes to the first d columns of dy16 ([n, d + R]) and dZ to the last R, so [dY | dZ] . [W; A] (A stacked
+// under W) is one GEMM into the bf16 dX; qkv / up: [dX | dZm] = dY . [W | B] is one GEMM, then dX += dZ A.
+static int layer_bwd_lora(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc* t, int i, cudaStream_t s) {
+  const MaceModelDesc& d = m.d;
+  const int l = m.sel[i];
+  const MaceLayerWeights& W = m.layers[l];
+  const MaceLoraLayer& lo = m.lora[i];
+  const MaceSavedActs& sv = b->sav[i];
+  const int n = t->T - t->ft0, D = d.d_model, F = d.ffn, UP = d.up_dim, R = d.lora_R, rk = d.lora_rank;
+  const int HO = d.n_heads * d.head_dim, QKV = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
+  const int ln = d.family == 1, ldh = D + R, ldy = D + R;
+  const float sc = d.lora_scale;
+  const int* ten = t->row_tenant ? t->row_tenant + t->ft0 : nullptr;
+  void* dz_y = (char*)b->dy16 + D * kBf;  // last R columns of [dY | dZ]
+  // MLP down
+  MACE_TRY(mace_f32_to_bf16_2d(m.ctx, b->dx, D, n, D, b->dy16, ldy, s));
+  MACE_TRY(gemm(m, b, s, b->dy16, ldy, false, lo.bt_down, D, false, n, R, D, b->lz, R, MACE_EPI_F32, nullptr));
+  MACE_TRY(mace_lora_mask(m.ctx, b->lz, R, ten, n, rk, R, sc, dz_y, ldy, s));
+  MACE_TRY(gemm(m, b, s, sv.zm_d, R, true, b->dy16, ldy, true, R, D, n, lo.g_bt_down, D, MACE_EPI_F32_ADD, nullptr, false));
+  MACE_TRY(gemm(m, b, s, dz_y, ldy, true, sv.a, F, true, R, F, n, lo.g_a_down, F, MACE_EPI_F32_ADD, nullptr, false));
+  MACE_TRY(gemm(m, b, s, b->dy16, ldy, false, W.down_w, F, true, n, F, D + R, b->da16, F, MACE_EPI_BF16, nullptr));
+  MACE_TRY(mace_act_bwd(m.ctx, sv.u, b->da16, n, F, d.family == 0, b->du16, s));
+  // MLP up (augmented)
+  MACE_TRY(gemm(m, b, s, (char*)sv.h2 + D * kBf, ldh, true, b->du16, UP, true, R, UP, n, lo.g_bt_up, UP, MACE_EPI_F32_ADD,
+                nullptr, false));
+  MACE_TRY(gemm(m, b, s, b->du16, UP, false, W.up_w, ldh, true, n, D + R, UP, b->df, b->ld_df, MACE_EPI_F32, nullptr));
+  MACE_TRY(mace_lora_mask(m.ctx, b->df + D, b->ld_df, ten, n, rk, R, sc, b->ldz, R, s));
+  MACE_TRY(gemm(m, b, s, b->ldz, R, true, sv.h2, ldh, true, R, D, n, lo.g_a_up, D, MACE_EPI_F32_ADD, nullptr, false));
+  MACE_TRY(gemm(m, b, s, b->ldz, R, false, lo.a_up, D, true, n, D, R, b->df, b->ld_df, MACE_EPI_F32_ADD, nullptr));
+  MACE_TRY(mace_norm_bwd(m.ctx, sv.x_mid, D, nullptr, b->df, b->ld_df, n, D, W.mlp_norm_w, ln, d.norm_eps, b->dx, D,
+                         nullptr, nullptr, nullptr, b->ws, b->ws_bytes, s));
+  // attention: o projection
+  MACE_TRY(mace_f32_to_bf16_2d(m.ctx, b->dx, D, n, D, b->dy16, ldy, s));
+  MACE_TRY(gemm(m, b, s, b->dy16, ldy, false, lo.bt_o, D, false, n, R, D, b->lz, R, MACE_EPI_F32, nullptr));
+  MACE_TRY(mace_lora_mask(m.ctx, b->lz, R, ten, n, rk, R, sc, dz_y, ldy, s));
+  MACE_TRY(gemm(m, b, s, sv.zm_o, R, true, b->dy16, ldy, true, R, D, n, lo.g_bt_o, D, MACE_EPI_F32_ADD, nullptr, false));
+  MACE_TRY(gemm(m, b, s, dz_y, ldy, true, sv.o, HO, true, R, HO, n, lo.g_a_o, HO, MACE_EPI_F32_ADD, nullptr, false));
+  MACE_TRY(gemm(m, b, s, b->dy16, ldy, false, W.o_w, HO, true, n, HO, D + R, b->do16, HO, MACE_EPI_BF16, nullptr));
+  // attention core (dense causal FT sequences)
+  MACE_TRY(zero(m, b->dqkv, (size_t)n * QKV * 4, s));
+  MACE_TRY(mace_attn_bwd(m.ctx, sv.qkv, sv.o, b->do16, sv.lse, n, d.n_heads, d.n_kv_heads, d.head_dim, t->ft_seqs,
+                         t->bwd_items, t->n_bwd, 0, b->Dbuf, b->dqkv, s));
+  if (d.family == 0)
+    MACE_TRY(mace_rope_bwd(m.ctx, b->dqkv, n, d.n_heads, d.n_kv_heads, d.head_dim, t->pos + t->ft0, d.cos_t, d.sin_t, s));
+  MACE_TRY(mace_f32_to_bf16(m.ctx, b->dqkv, (long long)n * QKV, b->dqkv16, s));
+  // qkv (augmented)
+  MACE_TRY(gemm(m, b, s, (char*)sv.h1 + D * kBf, ldh, true, b->dqkv16, QKV, true, R, QKV, n, lo.g_bt_qkv, QKV,
+                MACE_EPI_F32_ADD, nullptr, false));
+  MACE_TRY(gemm(m, b, s, b->dqkv16, QKV, false, W.qkv_w, ldh, true, n, D + R, QKV, b->df, b->ld_df, MACE_EPI_F32, nullptr));
+  MACE_TRY(mace_lora_mask(m.ctx, b->df + D, b->ld_df, ten, n, rk, R, sc, b->ldz, R, s));
+  MACE_TRY(gemm(m, b, s, b->ldz, R, true, sv.h1, ldh, true, R, D, n, lo.g_a_qkv, D, MACE_EPI_F32_ADD, nullptr, false));
+  MACE_TRY(gemm(m, b, s, b->ldz, R, false, lo.a_qkv, D, true, n, D, R, b->df, b->ld_df, MACE_EPI_F32_ADD, nullptr));
+  MACE_TRY(mace_norm_bwd(m.ctx, sv.x_in, D, nullptr, b->df, b->ld_df, n, D, W.attn_norm_w, ln, d.norm_eps, b->dx, D,
+                         nullptr, nullptr, nullptr, b->ws, b->ws_bytes, s));
+  return 0;
+}
+
 // dx (grad wrt the layer output, FT rows) -> grad wrt its input; dW of the layer into the flat grad
 static int layer_bwd(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc* t, int i, cudaStream_t s) {
+  if (!m.lora.empty()) return layer_bwd_lora(m, b, t, i, s);
   const MaceModelDesc& d = m.d;
   const int l = m.sel[i];
   const MaceLayerWeights& W = m.layers[l];
@@ -313,6 +407,7 @@ static int tick_run(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc*
   MACE_TRY(mace_embed(ctx, t->tokens, t->pos, d.last_token, d.embed, d.pos_embed, T, D, b->x, s));
   const bool has_ft = n_ft > 0 && t->n_pairs > 0;
   const int l_min = m.sel.empty() ? d.n_layers : m.sel[0];
+  const int l_sel0 = l_min;  // LoRA: the selected layers are contiguous (the top n_sel), adapter i = layer l_sel0 + i
   for (int l = 0; l < d.n_layers; ++l) {
     const bool top = has_ft && l >= l_min;
     const int T_l = top ? ft0 : T;
@@ -328,6 +423,11 @@ static int tick_run(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc*
     io.hn = l == d.n_layers - 1 ? b->hn : nullptr;
     io.u = b->u;
     io.a = b->a;
+    if (!m.lora.empty() && l >= l_sel0) {  // a selected layer: every row runs with its own tenant's adapter
+      io.lora = &m.lora[l - l_sel0];
+      io.tenant = t->row_tenant;
+      io.zm_o = io.zm_d = b->lzm;
+    }
     MACE_TRY(layer_fwd(m, b, t, l, m.layers[l], T_l, io, ar, s));
   }
   // ---- decode rows: final norm on gathered rows -> lm_head -> greedy token -> last_token
@@ -370,6 +470,25 @@ extern "C" int mace_model_create(mace_ctx* ctx, const MaceModelDesc* desc, mace_
       return mace_fail(ctx, MACE_ERR_ARG, "model: selected layers must be ascending");
     }
   }
+  if (desc->lora_R > 0) {
+    const int D = desc->d_model, HO = desc->n_heads * desc->head_dim;
+    const char* why = nullptr;
+    if (!desc->lora || desc->lora_rank <= 0 || desc->lora_R % 8 || desc->lora_R % desc->lora_rank)
+      why = "model: LoRA needs adapters, rank > 0 and R = tenants x rank with R % 8 == 0";
+    for (size_t i = 0; !why && i < m->sel.size(); ++i) {
+      if (i && m->sel[i] != m->sel[i - 1] + 1) why = "model: LoRA layers must be contiguous";
+      const MaceLayerWeights& W = desc->layers[m->sel[i]];
+      const MaceLoraLayer& lo = desc->lora[i];
+      if (lo.a_o != (const char*)W.o_w + (size_t)D * HO * 2 || lo.a_down != (const char*)W.down_w + (size_t)D * desc->ffn * 2)
+        why = "model: LoRA a_o / a_down must be stacked directly under o_w / down_w";
+    }
+    if (why) {
+      delete m;
+      return mace_fail(ctx, MACE_ERR_ARG, why);
+    }
+    m->lora.assign(desc->lora, desc->lora + desc->n_sel);
+  }
+  m->d.lora = nullptr;
   m->d.layers = nullptr;  // the copies above own the tables
   m->d.sel_layers = nullptr;
   m->d.ref_layers = nullptr;
@@ -389,6 +508,9 @@ extern "C" int mace_tick_run(mace_model* model, const MaceTickBuffers* bufs, con
     return mace_fail(model->ctx, MACE_ERR_ARG, "tick: missing activation buffers");
   if (tick->T - tick->ft0 > 0 && tick->n_pairs > 0 && !bufs->sav && model->sel.size())
     return mace_fail(model->ctx, MACE_ERR_ARG, "tick: FT rows need saved-activation buffers");
+  if (!model->lora.empty() && (!bufs->lz || !bufs->lzm || bufs->ld_h != model->d.d_model + model->d.lora_R ||
+                               (tick->T - tick->ft0 > 0 && (!bufs->ldz || !tick->row_tenant))))
+    return mace_fail(model->ctx, MACE_ERR_ARG, "tick: LoRA needs lz / lzm / ldz scratch, ld_h = d + R and row tenants");
   model->tick = tick;
   const int rc = tick_run(*model, bufs, tick, (cudaStream_t)stream);
   model->tick = nullptr;

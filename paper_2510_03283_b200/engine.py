@@ -226,7 +226,7 @@ class GpuEngine(Engine):
         c = self.mcfg
         Hq, Hkv = c.n_heads, c.n_kv_heads
         i32 = np.int32
-        tok_seg, pos_seg, seq_seg, kvi_seg = [], [], [], []
+        tok_seg, pos_seg, seq_seg, kvi_seg, ten_seg = [], [], [], [], []
         seqs: list[tuple] = []  # sequence rows not yet in seq_blocks
         seq_blocks: list[np.ndarray] = []
         n_seq = 0  # sequences before `seqs`
@@ -272,6 +272,7 @@ class GpuEngine(Engine):
             seqs.append((KIND_PREFILL, n_rows, q, slot, P, P, -1, 0))
             tc_seg.append(tc_block(si, q, P))
             tok_seg.append(np.asarray(req.prompt_tokens[start:], i32))
+            ten_seg.append(np.full(q, req.tenant, i32))
             r = np.arange(start, P, dtype=i32)
             pos_seg.append(r)
             kvi_seg.append(r)
@@ -302,6 +303,7 @@ class GpuEngine(Engine):
             seqs = []
             n_seq = si0 + n_dec
             tok_seg.append(np.where(k0 == 0, last, -(dec_slots + 1)).astype(i32))
+            ten_seg.append(np.fromiter((r.tenant for r in decodes), i32, n_dec))
             dpos = (P - 1 + k0).astype(i32)
             if c.family == "gpt2" and int(dpos.max()) >= c.max_pos:
                 raise ValueError(f"decode position {int(dpos.max())} >= {c.name}'s {c.max_pos} learned positions "
@@ -365,7 +367,7 @@ class GpuEngine(Engine):
                     toks = synthetic_pair_tokens(self.seed, req.id, n_c, n_r, c.vocab)
                 hit = self._pair_tokens[req.id] = (key, toks)
             chs, rjs = hit[1]
-            pairs.append(FtPair(req.id, req.prompt_tokens, chs, rjs, self.ref_lp.get(req.id)))
+            pairs.append(FtPair(req.id, req.prompt_tokens, chs, rjs, self.ref_lp.get(req.id), req.tenant))
             pr = []
             for side, resp in enumerate((chs, rjs)):
                 n = P + len(resp)
@@ -385,6 +387,7 @@ class GpuEngine(Engine):
                 bw[:, 3] = nkb - bw[:, 2]  # query blocks the key block walks (LPT key)
                 bwd_seg.append(bw)
                 tok_seg.append(np.asarray(list(req.prompt_tokens) + list(resp), i32))
+                ten_seg.append(np.full(n, req.tenant, i32))
                 pos_seg.append(np.arange(n, dtype=i32))
                 seq_seg.append(np.full(n, si, i32))
                 kvi_seg.append(np.full(n, -1, i32))
@@ -427,7 +430,7 @@ class GpuEngine(Engine):
             page_copies=arr(copies, 4), ft0=ft0, ft_pairs=pairs, ft_logit_rows=cat(lr_seg),
             ft_targets=cat(tg_seg), pair_rows=arr(pair_rows, 4), row_ps=cat(ps_seg),
             ft_seqs=arr(ft_seqs, 8), ft_tc_items=lpt(cat(ft_tc_seg, 4)), ft_row_seq=cat(ft_seq_seg),
-            bwd_items=lpt(cat(bwd_seg, 4)), n_prefill_tokens=n_pre, n_decode_tokens=n_dec, n_ft_tokens=n_ft,
+            bwd_items=lpt(cat(bwd_seg, 4)), row_tenant=cat(ten_seg), n_prefill_tokens=n_pre, n_decode_tokens=n_dec, n_ft_tokens=n_ft,
             meta={"n_tc_inference": n_tc_inference},
         )
 
@@ -521,6 +524,8 @@ class GpuEngine(Engine):
                 rec.update(ft_loss=out.ft_loss.cpu().numpy().copy(), ft_margin=out.ft_margin.cpu().numpy().copy(),
                            ft_lp=out.ft_lp.cpu().numpy().copy(), ref_lp=out.ref_lp.cpu().numpy().copy(),
                            grad={n: t.cpu().clone() for n, t in m.gview.items()},
+                           tenants=list(getattr(m, "last_tenants", [])),
+                           tenant_steps=m.tenant_steps.copy() if m.lora else None,
                            master=m.master.cpu().clone(), adam_m=m.m.cpu().clone(), adam_v=m.v.cpu().clone())
             self.records.append(rec)
         self._after_tick()

@@ -21,11 +21,13 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from ._lib import (Ctx, MaceKvLayout, MaceLayerGrads, MaceLayerWeights, MaceModelDesc, MaceSavedActs,
+from ._lib import (Ctx, MaceKvLayout, MaceLayerGrads, MaceLayerWeights, MaceLoraLayer, MaceModelDesc, MaceSavedActs,
                    MaceTickBuffers, MaceTickDesc)
 from .batch import PAGE, TickBatch
-from .config import ModelConfig, TrainConfig, selected_param_names, sensitivity_ranking
+from .config import (LORA_PROJ, ModelConfig, TrainConfig, selected_param_names, sensitivity_ranking,
+                     trainable_param_names)
 from .kvmanager import DecodePageMirror
+from .weights import init_lora
 
 
 @dataclass
@@ -58,6 +60,9 @@ class HybridModel:
         ctx: Ctx | None = None,
         process_group=None,
         grad_allreduce: str = "bf16",
+        n_tenants: int = 1,
+        lora_weights: dict[str, torch.Tensor] | None = None,
+        lora_seed: int = 0,
     ):
         self.cfg, self.tcfg = cfg, tcfg
         self.ctx = ctx or Ctx(device)
@@ -72,29 +77,47 @@ class HybridModel:
         for n in selected_param_names(cfg, tcfg):
             if self.w[n].data_ptr() == weights[n].data_ptr():
                 self.w[n] = self.w[n].clone()
-        # ---- selected parameters: flat fp32 master / m / v / grad + segment table for masked AdamW
-        self.sel = selected_param_names(cfg, tcfg)
+        # ---- per-tenant LoRA adapters (TrainConfig.lora_rank): the selected layers' projections carry them, the base
+        # model is frozen and shared by every tenant
+        self.lora = bool(tcfg.lora_rank)
+        self.n_tenants = n_tenants
+        self.lora_R = 0
         self.sel_layers = tcfg.selected_layers(cfg)
+        if self.lora:
+            if tcfg.sensitivity_topk is not None:
+                raise ValueError("LoRA adapters and sensitivity-selected layers are exclusive")
+            self.lora_R = n_tenants * tcfg.lora_rank
+            if self.lora_R % 8:
+                raise ValueError("LoRA: tenants x rank must be a multiple of 8")
+            lw = lora_weights if lora_weights is not None else init_lora(cfg, tcfg, n_tenants, lora_seed)
+            self.lora_init = {n: t.float().cpu().clone() for n, t in lw.items()}
+            self._build_lora(lw)
+        # ---- trainable parameters: flat fp32 master / m / v / grad + segment table for masked AdamW
+        self.sel = trainable_param_names(cfg, tcfg, n_tenants)
         self.l_min = min(self.sel_layers)
-        sizes = [self.w[n].numel() for n in self.sel]
+        src = self.lw if self.lora else self.w
+        sizes = [src[n].numel() for n in self.sel]
         offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
         self.n_sel = int(offs[-1])
-        self.master = torch.cat([self.w[n].float().reshape(-1) for n in self.sel])
+        self.master = torch.cat([src[n].float().reshape(-1) for n in self.sel])
         self.m = torch.zeros_like(self.master)
         self.v = torch.zeros_like(self.master)
         self.grad = torch.zeros_like(self.master)
         self._g16 = torch.empty(self.n_sel, dtype=torch.bfloat16, device=self.dev) if process_group is not None else None
-        self.gview = {n: self.grad[offs[i]: offs[i + 1]].view(self.w[n].shape) for i, n in enumerate(self.sel)}
+        self.gview = {n: self.grad[offs[i]: offs[i + 1]].view(src[n].shape) for i, n in enumerate(self.sel)}
         self.seg_offsets = torch.from_numpy(offs).to(self.dev)
-        self.seg_ptrs = torch.tensor([self.w[n].data_ptr() for n in self.sel], dtype=torch.int64, device=self.dev)
+        self.seg_ptrs = torch.tensor([src[n].data_ptr() for n in self.sel], dtype=torch.int64, device=self.dev)
         self.adam_step = 0
         self.update_layers: list[int] | None = None  # sensitivity selection (TrainConfig.sensitivity_topk)
         self.update_names = list(self.sel)
         self.sensitivity: list | None = None
         # the float4 AdamW kernel needs every segment to start on a 4-element boundary of the flat buffers and
         # every bf16 working copy 8-byte aligned (true for every preset: all widths are multiples of 4)
-        self.adam_vec4 = bool((offs % 4 == 0).all() and all(self.w[n].data_ptr() % 8 == 0 for n in self.sel))
-        self.ref_w = {n: self.w[n].clone() for n in self.sel}  # pi_ref frozen at init
+        self.adam_vec4 = bool((offs % 4 == 0).all() and all(src[n].data_ptr() % 8 == 0 for n in self.sel))
+        # pi_ref frozen at init; with LoRA the frozen base IS pi_ref (adapters masked off)
+        self.ref_w = {} if self.lora else {n: self.w[n].clone() for n in self.sel}
+        if self.lora:
+            self._build_tenant_segments(offs)
         # pi_ref log-probs are recomputed in every fine-tune tick by default: the pi_ref and policy sub-passes then
         # start from the SAME tick's layer-l_min activations, so the bf16 noise of the rows below l_min cancels in
         # the margin (lp - ref). A pi_ref cached from the pair's first tick was computed inside a different batch
@@ -168,6 +191,55 @@ class HybridModel:
         self._bufs = MaceTickBuffers()
         self.mh = self._create_native()
 
+    def _build_lora(self, lw: dict[str, torch.Tensor]) -> None:
+        """Device layout of the adapters (include/mace_b200.h MaceLoraLayer):
+          qkv / up   augmented base weight [out, d + R] = [W | B]: the forward [h | Zm] . [W | B]^T is one GEMM
+          o / down   A stacked under the base weight [d + R, in] = [W; A]: the backward [dY | dZ] . [W; A] is one GEMM
+        Every adapter also has a contiguous bf16 working copy per name (self.lw: AdamW's per-tenant targets); for
+        a_o / a_down that copy IS the stacked block, for bt_qkv / bt_up it is scattered into the augmented weight
+        after each update (mace_lora_bt_scatter)."""
+        c, dev, R = self.cfg, self.dev, self.lora_R
+        D = c.d_model
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        self.lw: dict[str, torch.Tensor] = {}
+        for l in self.sel_layers:
+            p, q = f"layers.{l}.", f"lora.{l}."
+            for proj in ("qkv", "up"):
+                W = self.w[p + proj + ".w"]
+                aug = torch.empty(W.shape[0], D + R, **bf)
+                aug[:, :D] = W
+                bt = lw[q + "bt_" + proj].to(dev, torch.bfloat16).contiguous()
+                aug[:, D:] = bt.t()
+                self.w[p + proj + ".w"] = aug
+                self.lw[q + "a_" + proj] = lw[q + "a_" + proj].to(dev, torch.bfloat16).contiguous()
+                self.lw[q + "bt_" + proj] = bt
+            for proj in ("o", "down"):
+                W = self.w[p + proj + ".w"]
+                st = torch.empty(D + R, W.shape[1], **bf)
+                st[:D] = W
+                st[D:] = lw[q + "a_" + proj].to(dev, torch.bfloat16)
+                self.w[p + proj + ".w"] = st
+                self.lw[q + "a_" + proj] = st[D:]
+                self.lw[q + "bt_" + proj] = lw[q + "bt_" + proj].to(dev, torch.bfloat16).contiguous()
+        self.tenant_steps = np.zeros(self.n_tenants, np.int64)
+        self._tick_tenants: list[int] = []
+
+    def _build_tenant_segments(self, offs: np.ndarray) -> None:
+        """Per tenant u, the AdamW segment table of its adapter rows: for every adapter tensor [R, width] the rows
+        [u * rank, (u + 1) * rank) -- one contiguous run of rank * width elements in the flat buffers and in the bf16
+        working copy."""
+        r = self.tcfg.lora_rank
+        self._tenant_seg = []
+        for u in range(self.n_tenants):
+            vstart, flat, wp = [0], [], []
+            for i, n in enumerate(self.sel):
+                k = r * self.lw[n].shape[1]
+                flat.append(int(offs[i]) + u * k)
+                wp.append(self.lw[n].data_ptr() + 2 * u * k)
+                vstart.append(vstart[-1] + k)
+            dev64 = lambda a: torch.tensor(a, dtype=torch.int64, device=self.dev)  # noqa: E731
+            self._tenant_seg.append((dev64(vstart), dev64(flat), dev64(wp), vstart[-1]))
+
     def _create_native(self):
         """mace_model_create: weight / gradient / KV pointers of the native tick executor (csrc/tick.cu)."""
         c = self.cfg
@@ -209,6 +281,20 @@ class HybridModel:
             dec_counters=self.dec_counters.data_ptr(), dec_work=self.dec_work.data_ptr(),
             decode_impl=int(self.decode_impl),
         )
+        if self.lora:
+            def lptr(l, n):
+                return self.lw[f"lora.{l}.{n}"].data_ptr()
+
+            def lgrad(l, n):
+                return self.gview[f"lora.{l}.{n}"].data_ptr()
+
+            self._lora_arr = (MaceLoraLayer * nsel)(*[MaceLoraLayer(
+                **{f"a_{p}": lptr(l, f"a_{p}") for p in LORA_PROJ},
+                bt_o=lptr(l, "bt_o"), bt_down=lptr(l, "bt_down"),
+                **{f"g_a_{p}": lgrad(l, f"a_{p}") for p in LORA_PROJ},
+                **{f"g_bt_{p}": lgrad(l, f"bt_{p}") for p in LORA_PROJ}) for l in self.sel_layers])
+            desc.lora_R, desc.lora_rank, desc.lora_scale = self.lora_R, self.tcfg.lora_rank, self.tcfg.lora_scale
+            desc.lora = self._lora_arr
         h = C.c_void_p()
         self.ctx.check(self.ctx.L.mace_model_create(self.ctx.h, C.byref(desc), C.byref(h)), "mace_model_create")
         return h
@@ -245,10 +331,15 @@ class HybridModel:
         c, dev = self.cfg, self.dev
         grew = False
         bf, f32 = dict(dtype=torch.bfloat16, device=dev), dict(dtype=torch.float32, device=dev)
+        LR = self.lora_R  # adapter columns (tenants x rank); R below is the tick's logit rows
+        ldh = c.d_model + LR  # LoRA layers: [h | Zm] rows
         if T > self._cap:
             cap = max(T, int(self._cap * 1.5), 256)
             self.x = torch.empty(cap, c.d_model, **f32)
-            self.h = torch.empty(cap, c.d_model, **bf)
+            self.h = torch.empty(cap, ldh, **bf)
+            if LR:
+                self.lz = torch.empty(cap, LR, **f32)
+                self.lzm = torch.empty(cap, LR, **bf)
             self.qkv = torch.empty(cap, c.qkv_dim, **bf)
             self.o = torch.empty(cap, c.n_heads * c.head_dim, **bf)
             self.lse = torch.empty(cap, c.n_heads, **f32)
@@ -262,25 +353,29 @@ class HybridModel:
             self.sav = {}
             for l in self.sel_layers:
                 self.sav[l] = dict(
-                    x_in=torch.empty(cap, c.d_model, **f32), h1=torch.empty(cap, c.d_model, **bf),
+                    x_in=torch.empty(cap, c.d_model, **f32), h1=torch.empty(cap, ldh, **bf),
                     qkv=torch.empty(cap, c.qkv_dim, **bf), o=torch.empty(cap, c.n_heads * c.head_dim, **bf),
                     lse=torch.empty(cap, c.n_heads, **f32), x_mid=torch.empty(cap, c.d_model, **f32),
-                    h2=torch.empty(cap, c.d_model, **bf), u=torch.empty(cap, c.up_dim, **bf),
+                    h2=torch.empty(cap, ldh, **bf), u=torch.empty(cap, c.up_dim, **bf),
                     a=torch.empty(cap, c.ffn, **bf),
                 )
+                if LR:
+                    self.sav[l].update(zm_o=torch.empty(cap, LR, **bf), zm_d=torch.empty(cap, LR, **bf))
             # ref-pass + backward scratch (FT rows only)
             self.rx = torch.empty(cap, c.d_model, **f32)
             self.rx2 = torch.empty(cap, c.d_model, **f32)
             self.x_lmin = torch.empty(cap, c.d_model, **f32)
             self.rlse = torch.empty(cap, c.n_heads, **f32)
-            self.rh = torch.empty(cap, c.d_model, **bf)
+            self.rh = torch.empty(cap, ldh, **bf)
             self.rqkv = torch.empty(cap, c.qkv_dim, **bf)
             self.ro = torch.empty(cap, c.n_heads * c.head_dim, **bf)
             self.ru = torch.empty(cap, c.up_dim, **bf)
             self.ra = torch.empty(cap, c.ffn, **bf)
             self.dx = torch.empty(cap, c.d_model, **f32)
-            self.dy16 = torch.empty(cap, c.d_model, **bf)
-            self.df = torch.empty(cap, max(c.ffn, c.up_dim, c.qkv_dim, c.n_heads * c.head_dim), **f32)
+            self.dy16 = torch.empty(cap, ldh, **bf)
+            self.df = torch.empty(cap, max(c.ffn, c.up_dim, c.qkv_dim, c.n_heads * c.head_dim, ldh), **f32)
+            if LR:
+                self.ldz = torch.empty(cap, LR, **bf)
             self.da16 = torch.empty(cap, c.ffn, **bf)
             self.du16 = torch.empty(cap, c.up_dim, **bf)
             self.do16 = torch.empty(cap, c.n_heads * c.head_dim, **bf)
@@ -324,6 +419,11 @@ class HybridModel:
         b = MaceTickBuffers()
         for n in ("x", "h", "qkv", "o", "lse", "hn", "u", "a"):
             setattr(b, n, getattr(self, n).data_ptr())
+        b.ld_h = self.cfg.d_model + self.lora_R
+        if self.lora:
+            b.lz, b.lzm = self.lz.data_ptr(), self.lzm.data_ptr()
+            if self._ft_cap:
+                b.ldz = self.ldz.data_ptr()
         if self._ft_cap:
             sav = [MaceSavedActs(**{k: t.data_ptr() for k, t in self.sav[l].items()}) for l in self.sel_layers]
             self._sav_arr = (MaceSavedActs * max(len(sav), 1))(*sav)
@@ -419,6 +519,11 @@ class HybridModel:
         d.n_copies = batch.page_copies.shape[0]
         d.ft_tc_items, d.n_ft_tc = v["ft_tc_items"], batch.ft_tc_items.shape[0]
         d.bwd_items, d.n_bwd = v["bwd_items"], batch.bwd_items.shape[0]
+        if self.lora:
+            if batch.row_tenant.shape[0] != T or (T and int(batch.row_tenant.max()) >= self.n_tenants):
+                raise ValueError(f"LoRA tick needs a tenant per row, each < {self.n_tenants}")
+            d.row_tenant = v["row_tenant"]
+            self._tick_tenants = sorted({p.tenant for p in batch.ft_pairs}) if has_ft else []
         events = None
         if self.instrument is not None and n_dec and T:
             events = [torch.cuda.Event(enable_timing=True) for _ in range(2 * self.cfg.n_layers)]
@@ -582,6 +687,8 @@ class HybridModel:
         L, s = self.ctx.L, self._s
         if not local_ft:
             self.grad.zero_()
+        if self.lora:
+            return self._apply_lora_update(local_ft)
         if self.pg is not None:
             if self.grad_allreduce == "bf16":
                 g16 = self._g16
@@ -611,3 +718,42 @@ class HybridModel:
                                        self.grad.data_ptr(), self.n_sel, self.seg_offsets.data_ptr(),
                                        self.seg_ptrs.data_ptr(), len(self.sel), t.lr, t.beta1, t.beta2, t.eps,
                                        t.weight_decay, self.adam_step, int(self.adam_vec4), s), "adamw")
+
+    def _apply_lora_update(self, local_ft: bool) -> None:
+        """Per-tenant AdamW of the adapters: each tenant with fine-tune rows this round (on any replica) takes one
+        step with its own step count over its own adapter rows only (mace_adamw_segments); the other tenants'
+        adapters and optimizer state stay untouched. Replicas all-reduce the gradient and the set of stepping
+        tenants, so every replica applies the same updates."""
+        L, s, t = self.ctx.L, self._s, self.tcfg
+        present = np.zeros(self.n_tenants, np.int32)
+        if local_ft:
+            present[self._tick_tenants] = 1
+        if self.pg is not None:
+            if self.grad_allreduce == "bf16":
+                g16 = self._g16
+                self._chk(L.mace_f32_to_bf16(self.ctx.h, self.grad.data_ptr(), self.n_sel, g16.data_ptr(), s),
+                          "grad to bf16")
+                torch.distributed.all_reduce(g16, group=self.pg)
+                self._chk(L.mace_bf16_to_f32(self.ctx.h, g16.data_ptr(), self.n_sel, self.grad.data_ptr(), s),
+                          "grad to f32")
+            else:
+                torch.distributed.all_reduce(self.grad, group=self.pg)
+            mask = torch.from_numpy(present).to(self.dev)
+            torch.distributed.all_reduce(mask, op=torch.distributed.ReduceOp.MAX, group=self.pg)
+            present = mask.cpu().numpy()
+        self.adam_step += 1
+        self.last_tenants = [int(u) for u in np.nonzero(present)[0]]
+        r, D, R = t.lora_rank, self.cfg.d_model, self.lora_R
+        for u in self.last_tenants:
+            self.tenant_steps[u] += 1
+            vstart, flat, wp, n = self._tenant_seg[u]
+            self._chk(L.mace_adamw_segments(self.ctx.h, self.master.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
+                                            self.grad.data_ptr(), len(self.sel), vstart.data_ptr(), flat.data_ptr(),
+                                            wp.data_ptr(), n, t.lr, t.beta1, t.beta2, t.eps, t.weight_decay,
+                                            int(self.tenant_steps[u]), int(self.adam_vec4), s), "adamw (tenant)")
+            for l in self.sel_layers:  # B of qkv / up: the updated rows back into the augmented weights
+                for proj in ("qkv", "up"):
+                    bt = self.lw[f"lora.{l}.bt_{proj}"]
+                    aug = self.w[f"layers.{l}.{proj}.w"]
+                    self._chk(L.mace_lora_bt_scatter(self.ctx.h, bt.data_ptr() + 2 * u * r * bt.shape[1], r,
+                                                     bt.shape[1], aug.data_ptr(), D + R, D + u * r, s), "lora scatter")

@@ -16,7 +16,7 @@ from macesim.distributions import parse_dist  # noqa: E402
 from macesim.engine import CacheConfig, EngineConfig  # noqa: E402
 from macesim.priority import PriorityParams  # noqa: E402
 from macesim.scheduler import Policy, SchedulerConfig  # noqa: E402
-from macesim.workload import TraceConfig, generate_trace  # noqa: E402
+from macesim.workload import TenantDriftSpec, TraceConfig, generate_trace  # noqa: E402
 
 
 @dataclass
@@ -34,12 +34,17 @@ class Workload:
     kv_tokens: int = 1 << 19  # prompt KV pool (tokens) the bench allocates for this trace
     decode_pages_per_head: int = 12  # decode ring pages per (slot, KV head) the bench allocates
     bench_skip: int = 150  # ticks the bench runs (untimed) before warm-up: the trace's steady state
+    tenant_params: dict | None = None  # multi-tenant env (config.py:212-239 [tenant.N] sections); None: one tenant
 
     def trace(self):
         return generate_trace(self.trace_cfg)
 
+    @property
+    def n_tenants(self) -> int:
+        return len(self.trace_cfg.tenants)
+
     def env(self):
-        return AlignmentEnv.create({0: TenantParams()}, seed=self.trace_cfg.seed)
+        return AlignmentEnv.create(self.tenant_params or {0: TenantParams()}, seed=self.trace_cfg.seed)
 
     def engine_args(self):
         """Positional args of Engine.__init__ (engine.py:186-196) with a fresh trace and env."""
@@ -106,3 +111,17 @@ def c4(seed: int = 100, arrival_rate: float = 40.0, duration: float = 30.0, capa
 
 
 WORKLOADS["c4"] = c4
+
+
+def with_tenants(wl: Workload, tenants: list[tuple[float, float]], lora_rank: int | None = None) -> Workload:
+    """The workload with several tenants (the reference's multi-tenant config, config.py:212-239 /
+    test_cli.py:238-256): tenants[i] = (mu0, drift_rate) of tenant i, used for both the trace's generation-time
+    drift spec (workload.py:110-128; generate_trace draws each request's tenant, workload.py:183-188) and the
+    env's TenantParams. With lora_rank, every tenant gets its own LoRA adapter (TrainConfig.lora_rank)."""
+    import dataclasses
+
+    specs = tuple(TenantDriftSpec(mu0=m, drift_rate=d) for m, d in tenants)
+    params = {i: TenantParams(mu0=m, drift_rate=d) for i, (m, d) in enumerate(tenants)}
+    train = dataclasses.replace(wl.train, lora_rank=lora_rank) if lora_rank else wl.train
+    return dataclasses.replace(wl, trace_cfg=dataclasses.replace(wl.trace_cfg, tenants=specs), tenant_params=params,
+                               train=train)
