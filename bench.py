@@ -124,7 +124,13 @@ def snapshot(model):
     if pool_bytes < 0.6 * torch.cuda.mem_get_info(model.dev)[0]:
         names = ["k_pool", "v_pool"] + names
     snap = {n: getattr(model, n).clone() for n in names}
-    snap["w"] = {n: model.w[n].clone() for n in model.sel}  # AdamW writes only the selected parameters
+    if model.lora:  # AdamW writes the tenants' adapters and the B columns of the augmented qkv / up weights
+        snap["lw"] = {n: t.clone() for n, t in model.lw.items()}
+        snap["w"] = {f"layers.{l}.{p}.w": model.w[f"layers.{l}.{p}.w"].clone() for l in model.sel_layers
+                     for p in ("qkv", "up")}
+        snap["tenant_steps"] = model.tenant_steps.copy()
+    else:
+        snap["w"] = {n: model.w[n].clone() for n in model.sel}  # AdamW writes only the selected parameters
     snap["adam_step"] = model.adam_step
     snap["kv_mirror"] = model.kv_mirror.state()
     return snap
@@ -132,9 +138,11 @@ def snapshot(model):
 
 def restore(model, snap):
     for n, t in snap.items():
-        if n == "w":
+        if n in ("w", "lw"):
             for k, v in t.items():
-                model.w[k].copy_(v)
+                getattr(model, n)[k].copy_(v)
+        elif n == "tenant_steps":
+            model.tenant_steps = t.copy()
         elif n == "adam_step":
             model.adam_step = t
         elif n == "kv_mirror":

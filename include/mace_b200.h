@@ -232,6 +232,12 @@ int mace_kv_decode_alloc(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots
 int mace_kv_status(mace_ctx* ctx, const MaceKvLayout* kv, int* out2);
 int mace_kv_trim(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, const int* kept, int n, void* stream);
 int mace_kv_release(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, int n, void* stream);
+/* compaction (after mace_kv_trim): items int32 [n][2] = (slot, kv head) whose retained window [dec_first, dec_end)
+ * (1 <= length <= max_w <= 64) fits in one page fewer when re-based -- the window's K/V rows move down to ring
+ * offset 0 in every layer of both pools, dec_base = dec_first, and the emptied last ring page is pushed. The host
+ * mirror (kvmanager.DecodePageMirror.compact) picks the items and counts the pages.                            */
+int mace_kv_compact(mace_ctx* ctx, const MaceKvLayout* kv, const int* items, int n, int max_w, int n_layers, int hd,
+                    long long pages_per_layer, void* k_pools, void* v_pools, void* stream);
 int mace_kv_page_copy(mace_ctx* ctx, const int* copies, int n, int n_kv_heads, int hd, long long pages_per_layer,
                       int n_layers, void* k_pools, void* v_pools, void* stream);
 int mace_kv_set_prompt_tables(mace_ctx* ctx, const MaceKvLayout* kv, const int* slots, const int* tables, int n,

@@ -187,6 +187,7 @@ SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_kv_status": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip]),
     "mace_kv_trim": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _ip, _i, _vp]),
     "mace_kv_release": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _i, _vp]),
+    "mace_kv_compact": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _i, _i, _i, _i, C.c_longlong, _vp, _vp, _vp]),
     "mace_kv_page_copy": (C.c_int, [_vp, _ip, _i, _i, _i, C.c_longlong, _i, _vp, _vp, _vp]),
     "mace_kv_set_prompt_tables": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _ip, _i, _i, _vp]),
     "mace_scatter_tokens": (C.c_int, [_vp, _ip, _ip, _i, _ip, _vp]),

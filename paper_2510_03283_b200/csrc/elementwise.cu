@@ -194,7 +194,7 @@ __global__ void norm_kernel(const float* __restrict__ x, int ldx, const int* __r
 // qkv row layout: [q heads | k heads | v heads] x hd (bf16). cos/sin tables [n_pos, hd/2] fp32.
 // Row kinds come from the tick's sequence table (MaceSeq). Paged destinations:
 //   prefill row (kind 0), prompt index t: head page = ptab[slot][t/16] * Hkv + h, row t % 16
-//   decode row  (kind 1), decode slot j:  head page = dtab[slot][h][(j - dec_base)/16],  row j % 16
+//   decode row  (kind 1), decode slot j:  head page = dtab[slot][h][(j - dec_base)/16],  row (j - dec_base) % 16
 //   fine-tune row (kind 2): attention reads K/V straight from the qkv rows (no write)
 // One CTA per row; every memory access is 16 bytes. Work items of a row:
 //   rotation items (q and k heads; only with RoPE): 8 consecutive pairs (i, i + hd/2) of one head -- two uint4
@@ -203,14 +203,16 @@ __global__ void norm_kernel(const float* __restrict__ x, int ldx, const int* __r
 //   copy items: the v heads' 16-byte chunks (and, without RoPE, the k heads' too) -> KV pages
 __device__ __forceinline__ long long kv_page_row(const MaceSeq& sq, const MaceKvLayout& kv, int Hkv, int h, int t,
                                                  int hd) {
-  int page;
+  int page, row;
   if (sq.kind == 0) {
     page = kv.ptab[(size_t)sq.slot * kv.max_prompt_pages + t / kPageTokens] * Hkv + h;
-  } else {
-    const int base = kv.dec_base[sq.slot * Hkv + h];
-    page = kv.dtab[((size_t)sq.slot * Hkv + h) * kv.max_dec_pages + (t - base) / kPageTokens];
+    row = t % kPageTokens;
+  } else {  // ring offset relative to dec_base (any value after a compaction re-base, mace_kv_compact)
+    const int rel = t - kv.dec_base[sq.slot * Hkv + h];
+    page = kv.dtab[((size_t)sq.slot * Hkv + h) * kv.max_dec_pages + rel / kPageTokens];
+    row = rel % kPageTokens;
   }
-  return ((long long)page * kPageTokens + (t % kPageTokens)) * hd;
+  return ((long long)page * kPageTokens + row) * hd;
 }
 
 __global__ void __launch_bounds__(128) rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int T, int Hq, int Hkv, int hd,

@@ -8,6 +8,9 @@
 //   trim          after a tick: the reference's post-tick kept[h] sets dec_first = dec_end - kept[h];
 //                 ring pages entirely below dec_first are pushed back and the ring is compacted
 //   release       a retiring request returns all its decode pages
+//   compact       re-base a head's ring at its retained window: the window [dec_first, dec_end) shifts down to
+//                 ring offset 0 inside the same pages, so a window that straddled a page boundary it does not
+//                 need (e.g. 4 tokens over 2 pages after a prune trim) frees its now-empty last page
 //   page_copy     copy-on-diverge of a partially shared prompt page (trie split at a non page-aligned
 //                 token, cache.py:79-105) across every layer of both pools
 // Pops and pushes never run in the same kernel, so the stack needs no ABA protection.
@@ -94,6 +97,50 @@ __global__ void release_kernel(const int* __restrict__ slots, int n, MaceKvLayou
     if (ring[r] != kv.sink_page) kv.free_stack[atomicAdd(kv.free_top, 1)] = ring[r];
   kv.dec_base[kvh] = 0;
   kv.dec_first[kvh] = 0;
+}
+
+// items int2 [n] = (slot, head), chosen by the host mirror (DecodePageMirror.compact_candidates): windows of at most
+// max_w tokens that one page fewer can hold. grid (n, L, 2 pools): the CTA stages the window's rows of one layer
+// and pool in shared memory (every read before any write: source and destination overlap), then writes them
+// back at ring offsets 0..w-1. dec_base / the free stack change only in the commit kernel after it.
+__global__ void kv_compact_move_kernel(const int2* __restrict__ items, MaceKvLayout kv, int hd,
+                                       long long pages_per_layer, __nv_bfloat16* __restrict__ kp,
+                                       __nv_bfloat16* __restrict__ vp) {
+  extern __shared__ uint4 stage[];
+  pdl_wait();
+  pdl_trigger();
+  const int2 it = items[blockIdx.x];
+  const int H = kv.n_kv_heads, kvh = it.x * H + it.y;
+  const int f = kv.dec_first[kvh], b = kv.dec_base[kvh], w = kv.dec_end[it.x] - f;
+  const int* ring = kv.dtab + (size_t)kvh * kv.max_dec_pages;
+  __nv_bfloat16* pool = (blockIdx.z ? vp : kp) + (size_t)blockIdx.y * pages_per_layer * kPageTokens * hd;
+  const int cpr = hd / 8;  // 16-byte chunks per token row
+  for (int i = threadIdx.x; i < w * cpr; i += blockDim.x) {
+    const int off = f - b + i / cpr;
+    stage[i] = *reinterpret_cast<const uint4*>(
+        pool + ((size_t)ring[off / kPageTokens] * kPageTokens + off % kPageTokens) * hd + (i % cpr) * 8);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < w * cpr; i += blockDim.x) {
+    const int off = i / cpr;
+    *reinterpret_cast<uint4*>(pool + ((size_t)ring[off / kPageTokens] * kPageTokens + off % kPageTokens) * hd +
+                              (i % cpr) * 8) = stage[i];
+  }
+}
+
+__global__ void kv_compact_commit_kernel(const int2* __restrict__ items, int n, MaceKvLayout kv) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int2 it = items[i];
+  const int kvh = it.x * kv.n_kv_heads + it.y;
+  const int f = kv.dec_first[kvh], b = kv.dec_base[kvh], e = kv.dec_end[it.x];
+  const int old_pages = (e - 1 - b) / kPageTokens + 1, new_pages = (e - 1 - f) / kPageTokens + 1;
+  const int* ring = kv.dtab + (size_t)kvh * kv.max_dec_pages;
+  for (int r = new_pages; r < old_pages; ++r)
+    if (ring[r] != kv.sink_page) kv.free_stack[atomicAdd(kv.free_top, 1)] = ring[r];
+  kv.dec_base[kvh] = f;
 }
 
 __global__ void reset_slot_kernel(const int* __restrict__ slots, int n, MaceKvLayout kv) {
@@ -207,4 +254,18 @@ extern "C" int mace_kv_status(mace_ctx* ctx, const MaceKvLayout* kv, int* out2) 
   if (cudaMemcpy(out2, kv->free_top, 2 * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
     return mace_fail(ctx, MACE_ERR_CUDA, "kv_status: copy failed");
   return MACE_OK;
+}
+
+extern "C" int mace_kv_compact(mace_ctx* ctx, const MaceKvLayout* kv, const int* items, int n, int max_w, int n_layers,
+                               int hd, long long pages_per_layer, void* k_pools, void* v_pools, void* stream) {
+  if (n <= 0) return 0;
+  if (hd % 8 || max_w <= 0 || max_w > 4 * kPageTokens)
+    return mace_fail(ctx, MACE_ERR_ARG, "kv_compact: hd % 8 == 0 and 0 < max_w <= 64");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t smem = (size_t)max_w * hd * 2;
+  launch_k(kv_compact_move_kernel, dim3(n, n_layers, 2), 128, smem, s, (const int2*)items, *kv, hd, pages_per_layer,
+           (__nv_bfloat16*)k_pools, (__nv_bfloat16*)v_pools);
+  launch_k(kv_compact_commit_kernel, (n + 127) / 128, 128, 0, s, (const int2*)items, n, *kv);
+  ctx->launches += 2;
+  return mace_check_launch(ctx, "kv_compact");
 }

@@ -39,7 +39,8 @@ class DecodePageMirror:
     without any device read and refuses a tick whose pops exceed the free pages (KvCapacityError):
       decode_alloc  (slot, head) pops one page when (dec_end - dec_base) % 16 == 0
       trim          dec_first = max(dec_first, dec_end - kept[h]); pages wholly below it are pushed
-      release       every live ring page of the slot is pushed"""
+      release       every live ring page of the slot is pushed
+      compact       a re-based window pushes its emptied last page"""
 
     def __init__(self, max_slots: int, n_heads: int, n_pages: int):
         self.end = np.zeros(max_slots, np.int64)
@@ -47,6 +48,8 @@ class DecodePageMirror:
         self.first = np.zeros((max_slots, n_heads), np.int64)
         self.free = int(n_pages)
         self.n_pages = int(n_pages)
+        self.compacted_heads = 0   # compaction statistics (C5 sweep)
+        self.compacted_tokens = 0
 
     def state(self):
         return (self.end.copy(), self.base.copy(), self.first.copy(), self.free)
@@ -76,6 +79,29 @@ class DecodePageMirror:
         drop = np.maximum(0, (first - self.base[slots]) // PAGE)
         self.free += int(drop.sum())
         self.base[slots] += drop * PAGE
+
+    def compact(self, slots: np.ndarray, max_w: int) -> np.ndarray:
+        """Compaction items (mace_kv_compact) among the given slots' heads: a retained window of 1..max_w tokens
+        whose ring, re-based at dec_first, needs one page fewer (a window straddling a page boundary it does not
+        need). Applies the re-base to the mirror (base = first, the emptied page freed); returns int32 [k, 2]
+        (slot, head)."""
+        if slots.size == 0 or max_w <= 0:
+            return np.zeros((0, 2), np.int32)
+        end = self.end[slots][:, None]
+        base, first = self.base[slots], self.first[slots]
+        w = end - first
+        old = np.where(end > base, (end - 1 - base) // PAGE + 1, 0)
+        new = np.where(w > 0, (end - 1 - first) // PAGE + 1, 0)
+        pick = (w >= 1) & (w <= max_w) & (new < old)
+        si, hi = np.nonzero(pick)
+        if si.size == 0:
+            return np.zeros((0, 2), np.int32)
+        sl = slots[si]
+        self.free += int((old - new)[si, hi].sum())
+        self.base[sl, hi] = self.first[sl, hi]
+        self.compacted_heads += int(si.size)
+        self.compacted_tokens += int(w[si, hi].sum())
+        return np.stack([sl, hi], 1).astype(np.int32)
 
     def release(self, slots: np.ndarray) -> None:
         end = self.end[slots][:, None]
@@ -157,6 +183,7 @@ class GpuPrefixTrie(PrefixTrie):
         self._memo: dict[int, tuple] = {}  # request id -> (epoch, stop kind, a, b, cached prefix length)
         self._epoch = 0                    # bumped by every split and every eviction
         self._bin_order = None             # prefill order of the executing bin (engine._dfs_order_hook)
+        self.groups_released_by_evict = 0  # page-group references the LRU offload dropped (C5 sweep)
 
     def cached_prefix_len(self, prompt_tokens):  # cache.py:164-184, same walk; label matches compared by slices
         return self._walk(prompt_tokens)[0]
@@ -244,6 +271,7 @@ class GpuPrefixTrie(PrefixTrie):
         for n in res.evicted:
             for g in self.node_pages.pop(n.node_id, {}).values():
                 self.pool.decref(g)
+                self.groups_released_by_evict += 1
         return res
 
 

@@ -158,6 +158,13 @@ class HybridModel:
         self.free_stack = torch.arange(prompt_groups * H, self.pages_per_layer - 1, **i32)
         self.free_top = torch.tensor([decode_pages, 0], **i32)  # {stack top, status}
         self.kv_mirror = DecodePageMirror(max_slots, H, decode_pages)  # host count of the same pops / pushes
+        # decode-window compaction (mace_kv_compact): on demand when a tick's page pops exceed the free pages, and
+        # after every prune trim for windows of <= compact_max_window tokens (0: off -- a window slides one slot per
+        # tick, so its straddled leading page empties by itself within < 16 ticks; re-basing it every tick would
+        # move the window each tick for at most one page); bytes moved / pages returned
+        self.compact_max_window = int(os.environ.get("MACE_KV_COMPACT_MAX", "0"))
+        self.compaction_bytes = 0
+        self.compaction_pages = 0
         self.last_token = torch.zeros(max_slots, **i32)
         self.dec_counters = torch.zeros(max_slots * H, **i32)  # decode chunk-merge counters (self-cleaning)
         # decode ticket counter: zero between launches -- the warp that draws a launch's terminal ticket resets
@@ -501,7 +508,10 @@ class HybridModel:
         P = len(batch.ft_pairs)
         self._ensure(max(T, 1), max(n_ft, 1), max(R, 1), max(n_dec, 1), max(P, 1))
         if n_dec:  # raises KvCapacityError before any launch if the decode pages cannot hold this tick
-            self.kv_mirror.alloc(batch.dec_slots.astype(np.int64))
+            ds = batch.dec_slots.astype(np.int64)
+            if self.kv_mirror.pops(ds) > self.kv_mirror.free:  # memory pressure: reclaim straddled pages first
+                self.compact_windows()
+            self.kv_mirror.alloc(ds)
         v = self._upload(batch)
         has_ft = n_ft > 0 and P > 0
         if self.instrument is not None and n_dec:
@@ -599,10 +609,33 @@ class HybridModel:
             return
         if self.tape is not None:
             self.tape.append(("trim", slots.copy(), kept.copy()))
-        self.kv_mirror.trim(np.asarray(slots, np.int64), np.asarray(kept, np.int64).reshape(n, -1))
+        sl = np.asarray(slots, np.int64)
+        self.kv_mirror.trim(sl, np.asarray(kept, np.int64).reshape(n, -1))
         dev = self._stage((np.ascontiguousarray(slots, np.int32).reshape(-1),
                            np.ascontiguousarray(kept, np.int32).reshape(-1)))
         self._chk(self.ctx.L.mace_kv_trim(self.ctx.h, C.byref(self.kv), dev, dev + 4 * n, n, self._s), "kv_trim")
+        if self.compact_max_window:
+            self.compact_windows(sl, self.compact_max_window)
+
+    def compact_windows(self, slots: np.ndarray | None = None, max_w: int = 64) -> int:
+        """Decode-window compaction (mace_kv_compact): every head of ``slots`` (default: every live slot) whose
+        retained window of <= max_w tokens fits one page fewer when re-based at dec_first moves its K/V rows down
+        inside its pages and returns the emptied page. Returns the pages reclaimed. Run on demand when a tick's
+        page pops exceed the free pages (step), or after every trim with compact_max_window > 0."""
+        if slots is None:
+            slots = np.nonzero(self.kv_mirror.end > 0)[0]
+        items = self.kv_mirror.compact(np.asarray(slots, np.int64), max_w)
+        if not items.shape[0]:
+            return 0
+        c = self.cfg
+        w = self.kv_mirror.end[items[:, 0]] - self.kv_mirror.first[items[:, 0], items[:, 1]]
+        self.compaction_bytes += int(w.sum()) * c.n_layers * 2 * c.head_dim * 2 * 2  # read + write, K and V
+        self.compaction_pages += int(items.shape[0])
+        di = self._stage((items.reshape(-1),))
+        self._chk(self.ctx.L.mace_kv_compact(self.ctx.h, C.byref(self.kv), di, items.shape[0], max_w, c.n_layers,
+                                             c.head_dim, self.pages_per_layer, self.k_pool.data_ptr(),
+                                             self.v_pool.data_ptr(), self._s), "kv_compact")
+        return int(items.shape[0])
 
     def release_slots(self, slots: list[int]) -> None:
         if not slots:

@@ -122,27 +122,29 @@ def test_masked_adamw_bit_exact(ctx, sizes, vec4):
     seg_ptr = torch.tensor([pool.data_ptr() + 2 * s for s in starts], dtype=torch.int64, device="cuda")
     hp = (1e-3, 0.9, 0.999, 1e-8, 0.01)
     P, M, Vv = master.cpu().numpy().copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
-    tp = torch.nn.Parameter(master.cpu().clone())
-    opt = torch.optim.AdamW([tp], lr=hp[0], betas=(hp[1], hp[2]), eps=hp[3], weight_decay=hp[4], foreach=False)
     for step in range(1, 6):
         g = torch.randn(n, device="cuda") * torch.logspace(-6, 0, n, device="cuda")
         ctx.check(ctx.L.mace_adamw_masked2(ctx.h, _p(master), _p(m), _p(v), _p(g), n, _p(seg_off), _p(seg_ptr),
                                            len(sizes), *map(C.c_double, hp), step, int(vec4), None), "adamw")
         gh = g.cpu().numpy()
-        P_prev = P
+        P_prev, M_prev, V_prev = P, M, Vv
         P, M, Vv = adamw_np(P, M, Vv, gh, *hp, step)
-        tp.grad = g.cpu().clone()
-        opt.step()
         torch.cuda.synchronize()
         assert np.array_equal(master.cpu().numpy().view(np.int32), P.view(np.int32)), f"master, step {step}"
         assert np.array_equal(m.cpu().numpy().view(np.int32), M.view(np.int32)), f"m, step {step}"
         assert np.array_equal(v.cpu().numpy().view(np.int32), Vv.view(np.int32)), f"v, step {step}"
-        # torch.optim.AdamW: within 8 ulp of the larger of the weight and the step. torch's CPU kernels may contract
-        # lerp / addcmul into FMAs and addcdiv rounds (value*m)/denom where the kernel rounds value*(m/denom): ulp-level
-        # differences in m, v and the update, visible when the update cancels p
+        # torch.optim.AdamW taking the same step from the same state: within 4 ulp of the larger of the weight and
+        # the step size. torch's CPU kernels may contract lerp / addcmul into FMAs (CPU-dependent vectorisation) and
+        # addcdiv rounds (value*m)/denom where the kernel rounds value*(m/denom): ulp-level differences per step
+        tp = torch.nn.Parameter(torch.from_numpy(P_prev.copy()))
+        opt = torch.optim.AdamW([tp], lr=hp[0], betas=(hp[1], hp[2]), eps=hp[3], weight_decay=hp[4], foreach=False)
+        opt.state[tp] = {"step": torch.tensor(float(step - 1)), "exp_avg": torch.from_numpy(M_prev.copy()),
+                         "exp_avg_sq": torch.from_numpy(V_prev.copy())}
+        tp.grad = g.cpu().clone()
+        opt.step()
         scale = np.maximum(np.maximum(np.abs(tp.detach().numpy()), np.abs(P_prev)), np.float32(hp[0]))
-        assert (np.abs(master.cpu().numpy() - tp.detach().numpy()) <= 8 * np.spacing(scale)).all(), \
-            f"torch AdamW, step {step}"
+        err = np.abs(P - tp.detach().numpy()) / np.spacing(scale)
+        assert err.max() <= 4, f"torch AdamW, step {step}: {err.max()} ulp at {int(err.argmax())}"
     mask = torch.zeros(pool.numel(), dtype=torch.bool, device="cuda")
     for s, k, o in zip(starts, sizes, offs[:-1]):
         assert torch.equal(pool[s: s + k], master[o: o + k].to(torch.bfloat16))

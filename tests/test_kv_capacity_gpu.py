@@ -28,6 +28,8 @@ def test_device_stack_matches_host_mirror(ctx):
         top, status = model.kv_status()
         assert status == 0
         assert top == model.kv_mirror.free
+    base = model.dec_base.cpu().numpy()
+    assert (base == model.kv_mirror.base[: base.shape[0]]).all()
 
 
 def test_exhausted_decode_pool_raises_before_launch(ctx):

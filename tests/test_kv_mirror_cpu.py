@@ -1,7 +1,9 @@
 """The host mirror of the decode-page allocator (kvmanager.DecodePageMirror) counts exactly the pops and
-pushes the device kernels make (csrc/kvpage.cu: decode_alloc / trim / release), restated here page by
-page with a real free stack, over random decode / prune-trim / retire sequences -- and it refuses the
-tick (KvCapacityError, nothing changed) exactly when the device stack would run dry."""
+pushes the device kernels make (csrc/kvpage.cu: decode_alloc / trim / compact / release), restated here page by
+page with a real free stack and real page contents, over random decode / prune-trim / compaction / retire
+sequences -- it refuses the tick (KvCapacityError, nothing changed) exactly when the device stack would run dry,
+and every retained decode slot stays readable at its ring address (rope_kv's write address = the attention
+kernels' read address) through compactions."""
 import numpy as np
 import pytest
 
@@ -20,6 +22,11 @@ class DeviceSim:
         self.first = [[0] * H for _ in range(S)]
         self.ring = [[[] for _ in range(H)] for _ in range(S)]
         self.H = H
+        self.data = {}  # page -> [16] decode slot index stored in each row (K/V stand-in)
+
+    def _addr(self, s, h, j):  # elementwise.cu kv_page_row, decode rows: ring offset relative to dec_base
+        rel = j - self.base[s][h]
+        return self.ring[s][h][rel // PAGE], rel % PAGE
 
     def alloc(self, slots):
         for s in slots:
@@ -29,8 +36,30 @@ class DeviceSim:
                         return False
                     self.ring[s][h].append(self.stack.pop())
         for s in slots:
+            for h in range(self.H):  # rope_kv writes the new slot's K/V
+                pg, row = self._addr(s, h, self.end[s])
+                self.data.setdefault(pg, [None] * PAGE)[row] = (s, h, self.end[s])
             self.end[s] += 1
         return True
+
+    def compact(self, items):
+        """kv_compact_move_kernel + kv_compact_commit_kernel: the window moves down to ring offset 0."""
+        for s, h in items:
+            f, b, e = self.first[s][h], self.base[s][h], self.end[s]
+            vals = [self.data[self.ring[s][h][(f - b + i) // PAGE]][(f - b + i) % PAGE] for i in range(e - f)]
+            for i, v in enumerate(vals):
+                self.data[self.ring[s][h][i // PAGE]][i % PAGE] = v
+            old, new = (e - 1 - b) // PAGE + 1, (e - 1 - f) // PAGE + 1
+            for _ in range(old - new):
+                self.stack.append(self.ring[s][h].pop())
+            self.base[s][h] = f
+
+    def check_windows(self, live):
+        for s in live:
+            for h in range(self.H):
+                for j in range(self.first[s][h], self.end[s]):
+                    pg, row = self._addr(s, h, j)
+                    assert self.data[pg][row] == (s, h, j), (s, h, j)
 
     def trim(self, slots, kept):
         for s, k in zip(slots, kept):
@@ -55,7 +84,7 @@ def test_mirror_counts_device_pops_and_pushes(seed):
     S, H, N = 24, 4, 110
     dev, mir = DeviceSim(S, H, N), DecodePageMirror(S, H, N)
     live = set()
-    refused = 0
+    refused = compacted = 0
     for step in range(3000):
         op = rng.random()
         if op < 0.7:
@@ -83,6 +112,10 @@ def test_mirror_counts_device_pops_and_pushes(seed):
             kept = rng.integers(1, 40, (slots.size, H))
             dev.trim(slots.tolist(), kept.tolist())
             mir.trim(slots, kept)
+            if rng.random() < 0.7:  # compaction after the trim (HybridModel.apply_trim)
+                items = mir.compact(slots, int(rng.integers(1, 48)))
+                dev.compact(items.tolist())
+                compacted += len(items)
         elif live:
             slots = np.array(sorted(rng.choice(sorted(live), min(len(live), 3), replace=False)), np.int64)
             dev.release(slots.tolist())
@@ -91,4 +124,8 @@ def test_mirror_counts_device_pops_and_pushes(seed):
         assert mir.free == len(dev.stack), step
         assert np.array_equal(mir.end, np.array(dev.end)), step
         assert np.array_equal(mir.base, np.array(dev.base)), step
+        if step % 50 == 0:
+            dev.check_windows(live)
+    dev.check_windows(live)
     assert refused > 0, "the sequence should exercise exhaustion"
+    assert compacted > 0, "the sequence should exercise compaction"

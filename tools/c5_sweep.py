@@ -5,8 +5,10 @@ fixed tick window; the reference's fine-tune memory charge is set from the devic
 HybridModel.ft_bytes_per_token() (the FT-row buffers the step really allocates), ft_mem_fixed = 0 (the
 selected-parameter optimizer state is resident, outside the budget). Reported per capacity: reference
 cache events (evict / prune, engine.py:364-372,520-529), rejections, KV pages freed on the device (trie
-evictions and prune trims), TPOT p50/p99 (reference clock), device tokens/s over the window.
-    python tools/c5_sweep.py [--ticks 48] [--caps 40960,61440,81920,122880,184320]
+evictions, prune trims and the decode-window compactions with the bytes they moved), TPOT p50/p99 (reference
+clock), device tokens/s over the window. The smallest capacities leave the reference's budget below the trie's
+residency, so its LRU offload (cache.py:217-238) evicts page groups on the device.
+    python tools/c5_sweep.py [--ticks 64] [--caps 20480,24576,32768,40960,81920,184320]
 """
 import argparse
 import gc
@@ -27,8 +29,8 @@ from paper_2510_03283_b200.weights import init_weights  # noqa: E402
 from paper_2510_03283_b200.workloads import c4  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--ticks", type=int, default=48)
-ap.add_argument("--caps", default="40960,61440,81920,122880,184320")
+ap.add_argument("--ticks", type=int, default=64)
+ap.add_argument("--caps", default="20480,24576,32768,40960,81920,184320")
 ap.add_argument("--pool-gb", type=float, default=112.0, help="prompt KV pool the B200 holds next to the 8B model")
 args = ap.parse_args()
 build()
@@ -77,6 +79,10 @@ for cap in caps:
         "device_tokens_per_s": sum(eng.tick_tokens) / (dev_ms / 1e3) if dev_ms else None,
         "e2e_tokens_per_s": sum(eng.tick_tokens) / wall,
         "tpot_p50_ms": lat["tbt_p50"], "tpot_p99_ms": lat["tbt_p99"], "error": err,
+        "kv_compaction_heads": model.compaction_pages, "kv_compaction_bytes": model.compaction_bytes,
+        "kv_compacted_tokens": model.kv_mirror.compacted_tokens,
+        "decode_pages_free": model.kv_mirror.free, "decode_pages": model.kv_mirror.n_pages,
+        "trie_groups_released_by_evict": getattr(eng.trie, "groups_released_by_evict", None),
     }
     rows.append(row)
     print(json.dumps(row), flush=True)
