@@ -236,7 +236,9 @@ def run_ours(args, rank, world, lock):
     from paper_2510_03283_b200.weights import init_weights
 
     build()
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MACE_ONE_GPU=1: every rank on cuda:0 (a multi-rank rehearsal of the N>1 path on a one-GPU box, with
+    # MACE_DIST_BACKEND=gloo for the gradient all-reduce: NCCL refuses two ranks on one device)
+    local = 0 if os.environ.get("MACE_ONE_GPU") == "1" else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     wl = make_workload(args.workload, rank, args.seed, args.lora_tenants, args.lora_rank)
     cfg = wl.model
@@ -507,7 +509,7 @@ def main():
         world = int(os.environ.get("WORLD_SIZE", "1"))
         run_reference(args, rank, world)
         return
-    rank, world, lock = init_from_env("nccl")
+    rank, world, lock = init_from_env(os.environ.get("MACE_DIST_BACKEND", "nccl"))
     run_ours(args, rank, world, lock)
 
 

@@ -27,11 +27,17 @@ from paper_2510_03283_b200.kvmanager import KvCapacityError  # noqa: E402
 from paper_2510_03283_b200.model import HybridModel  # noqa: E402
 from paper_2510_03283_b200.weights import init_weights  # noqa: E402
 from paper_2510_03283_b200.workloads import c4  # noqa: E402
+from macesim.distributions import parse_dist  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--ticks", type=int, default=64)
+ap.add_argument("--ticks", type=int, default=96)
 ap.add_argument("--caps", default="20480,24576,32768,40960,81920,184320")
 ap.add_argument("--pool-gb", type=float, default=112.0, help="prompt KV pool the B200 holds next to the 8B model")
+ap.add_argument("--output-mean", type=float, default=4.0,
+                help="geometric mean output length (C4: 32). The reference evicts only when the QUEUE HEAD does not fit "
+                     "(engine.py:375-389, every tick before planning): decode rows (priority 3) head the queue while any "
+                     "request decodes and their prefix nodes stay referenced, so short outputs are what let finished "
+                     "prefixes pile up in the trie and a prefill head trigger the LRU offload")
 args = ap.parse_args()
 build()
 caps = [float(x) for x in args.caps.split(",")]
@@ -43,6 +49,7 @@ pool_tokens = int(args.pool_gb * 1e9 / kv_tok_bytes) // 16 * 16
 rows = []
 for cap in caps:
     wl = c4(capacity_mb=cap)
+    wl = replace(wl, trace_cfg=replace(wl.trace_cfg, output_len_dist=parse_dist(f"geometric:mean={args.output_mean}")))
     model = HybridModel(cfg, wl.train, w, device=0, max_slots=1024, max_prompt_len=wl.max_prompt_len,
                         max_decode_steps=wl.sched.max_decode_steps,
                         prompt_groups=min(wl.kv_tokens, pool_tokens) // 16,
@@ -67,7 +74,7 @@ for cap in caps:
     ev = [e for e in eng.timeline if e.get("kind") == "cache_event"]
     lat = eng.metrics.latency_summary()
     row = {
-        "capacity_mb": cap, "ft_mem_per_token_mb": ft_mb, "ticks": done,
+        "capacity_mb": cap, "output_len_mean": args.output_mean, "ft_mem_per_token_mb": ft_mb, "ticks": done,
         "evict_events": sum(1 for e in ev if e.get("event") == "evict"),
         "evicted_nodes": sum(e.get("nodes", 0) for e in ev if e.get("event") == "evict"),
         "evicted_mb": -sum(e.get("bytes_mb", 0.0) for e in ev if e.get("event") == "evict"),
