@@ -96,7 +96,12 @@ typedef struct MaceSeq {
   int kind, q_start, q_len, slot; /* slot: KV-table slot of the request (paged kinds) */
   int n_pv;                       /* prompt tokens visible to this sequence            */
   int kv_len;                     /* FT / prefill: total causal KV length               */
-  int out_row, pad;               /* decode: row in the logits batch                    */
+  int hole0, hole_len;            /* FT: keys [hole0, hole0 + hole_len) are invisible to the rows at or after
+                                     hole0 + hole_len (causal otherwise). A preference pair is ONE sequence
+                                     [prompt | chosen | prompt[-1] | rejected]: hole0 = P - 1, hole_len = 1 +
+                                     n_chosen, so the rejected branch attends to prompt[:-1], its own copy of
+                                     the last prompt token and itself -- the prompt rows are computed once for
+                                     both responses. 0, 0 for every other kind.                              */
 } MaceSeq;
 
 /* Device-resident KV page tables (persist across ticks).  Pools are head-major pages:

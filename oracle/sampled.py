@@ -9,8 +9,8 @@ CPU path "on a sampled subset of ticks for C3-C5"; this module is that sample, r
   * the tick's bin is the UNMODIFIED reference scheduler's (macesim.engine.Engine, mode-P clock), captured by
     ``composition`` from the bin the reference hands to Engine._execute (engine.py:573-584): prefill rows = the
     uncached prompt suffix the reference charges (cache.py:164-184), decode rows = one per decode request,
-    fine-tune rows = [prompt | chosen] and [prompt | rejected] per FT request (the GPU path's rows, same
-    clipping to the model's positions);
+    fine-tune rows = [prompt | chosen | prompt[-1] | rejected] per FT request (the GPU path's rows: the prompt
+    once for both responses, same clipping to the model's positions);
   * ``SampledTickCPU.run`` executes ``rows`` of them, drawn proportionally from the three kinds (at least one
     of every kind present, evenly spaced inside each kind), through EVERY decoder layer of the fp32 oracle
     (OracleModel.layer: same norms / projections / RoPE / GQA / MLP as the oracle), each row attending over
@@ -55,9 +55,14 @@ def composition(engine, plan, max_pos: int) -> dict:
             n_dec += 1
         else:
             room = max(1, max_pos - P)
-            for n_resp in (min(r.pair.tokens_chosen, room), min(r.pair.tokens_rejected, room)):
-                for t in range(P + n_resp):
-                    rows.append((KIND_FT, t, t + 1, t >= P - 1 and t < P - 1 + n_resp))
+            n_c, n_r = min(r.pair.tokens_chosen, room), min(r.pair.tokens_rejected, room)
+            # the GPU path's pair layout [prompt | chosen | prompt[-1] | rejected] (engine.build_batch): prompt rows
+            # once, the chosen branch, then the rejected branch re-entering at position P-1 (keys: prompt[:-1] +
+            # its own rows)
+            for t in range(P + n_c):
+                rows.append((KIND_FT, t, t + 1, P - 1 <= t < P - 1 + n_c))
+            for i in range(n_r + 1):
+                rows.append((KIND_FT, P - 1 + i, P + i, i < n_r))
                 n_ft += P + n_resp
     return {"rows": rows, "n_prefill": n_pre, "n_decode": n_dec, "n_ft": n_ft}
 

@@ -139,7 +139,7 @@ class MaceTickDesc(C.Structure):
 
 
 # MaceSeq is 8 x int32 (see include/mace_b200.h); built as numpy/torch int32 [S, 8] arrays
-SEQ_FIELDS = ("kind", "q_start", "q_len", "slot", "n_pv", "kv_len", "out_row", "pad")
+SEQ_FIELDS = ("kind", "q_start", "q_len", "slot", "n_pv", "kv_len", "hole0", "hole_len")
 
 _vp, _i, _f, _ip = C.c_void_p, C.c_int, C.c_float, C.c_void_p
 

@@ -269,6 +269,9 @@ __global__ void __launch_bounds__(384, 1)
       const int qi = f.q0 + r;
       const bool q_ok = qi < f.sq.q_len;
       const int lim_row = min(f.sq.kv_len - 1, f.sq.kv_len - f.sq.q_len + qi);  // last visible key of this row
+      // FT preference pair (MaceSeq hole): the rejected branch's rows do not see the chosen branch's keys
+      const int h1 = f.sq.hole0 + f.sq.hole_len;
+      const bool in_hole_rows = f.sq.kind == 2 && f.sq.hole_len > 0 && qi >= h1;
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < f.n_tiles; ++j, ++g) {
         mbar_wait(s_full, g & 1);
@@ -283,10 +286,11 @@ __global__ void __launch_bounds__(384, 1)
         if (lane == 0) mbar_arrive(s_free);
         if (lane == 0) ATR(wg, 1, g);
         const int lim = lim_row - j * 128 - cb;
-        if (lim < 63) {  // causal diagonal / sequence end: masked scores -> -inf
+        const int hlo = in_hole_rows ? f.sq.hole0 - j * 128 - cb : 64, hhi = in_hole_rows ? h1 - j * 128 - cb : 0;
+        if (lim < 63 || (hlo < 64 && hhi > 0)) {  // causal diagonal / sequence end / pair hole: masked -> -inf
 #pragma unroll
           for (int c = 0; c < 64; ++c)
-            if (c > lim) sv[c] = __float_as_uint(-INFINITY);
+            if (c > lim || (c >= hlo && c < hhi)) sv[c] = __float_as_uint(-INFINITY);
         }
         float mx8[8];
 #pragma unroll

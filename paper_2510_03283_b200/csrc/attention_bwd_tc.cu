@@ -70,6 +70,8 @@ __global__ void __launch_bounds__(160, 1)
   const int W = (Hq + 2 * Hkv) * HD;
   const int n = sq.q_len;
   const int base = sq.q_start - row_offset;  // local row of token 0
+  // preference-pair hole (MaceSeq): rows at or after h1 do not see keys [hole0, h1); h1 = n + 1 when there is none
+  const int h1 = sq.hole_len > 0 ? sq.hole0 + sq.hole_len : n + 1;
   const int nqb = (n + 127) / 128;
   const int steps = G * (nqb - j);
   const float sl2 = scale * 1.4426950408889634f;
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(160, 1)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int q = q0 + c0 + c + e;
-            const bool ok = q < n && kg < n && kg <= q;
+            const bool ok = q < n && kg < n && kg <= q && !(q >= h1 && kg >= sq.hole0 && kg < h1);
             const float p = ok ? exp2f(__uint_as_float(sv[c + e]) * sl2 - l2_s[c0 + c + e]) : 0.f;
             p2[e] = p;
             d2[e] = p * (__uint_as_float(dv[c + e]) - d_s[c0 + c + e]);

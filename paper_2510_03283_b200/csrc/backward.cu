@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(256) attn_bwd_kernel(const __nv_bfloat16* __re
   const int W = (Hq + 2 * Hkv) * HD;
   const int n = sq.q_len;
   const int base = sq.q_start - row_offset;  // local row of token 0 in the FT activation block
+  const int h1 = sq.hole_len > 0 ? sq.hole0 + sq.hole_len : n + 1;  // preference-pair hole (MaceSeq)
   const int k0 = jb * B;
   const int tid = threadIdx.x;
   const int ty = tid / 16, tx = tid % 16;  // 16x16 threads, 4x4 micro tiles
@@ -342,7 +343,8 @@ __global__ void __launch_bounds__(256) attn_bwd_kernel(const __nv_bfloat16* __re
         for (int b = 0; b < 4; ++b) {
           const int kj = tx * 4 + b, kg = k0 + kj;
           float p = 0.f;
-          if (qg < n && kg < n && kg <= qg) p = __expf(s[a][b] * scale - ls[qi]);
+          if (qg < n && kg < n && kg <= qg && !(qg >= h1 && kg >= sq.hole0 && kg < h1))
+            p = __expf(s[a][b] * scale - ls[qi]);
           Ps[qi * (B + 1) + kj] = p;
           dSs[qi * (B + 1) + kj] = p * (dp[a][b] - Ds[qi]);
         }

@@ -368,37 +368,46 @@ class GpuEngine(Engine):
                 hit = self._pair_tokens[req.id] = (key, toks)
             chs, rjs = hit[1]
             pairs.append(FtPair(req.id, req.prompt_tokens, chs, rjs, self.ref_lp.get(req.id), req.tenant))
-            pr = []
-            for side, resp in enumerate((chs, rjs)):
-                n = P + len(resp)
-                si = n_seq + len(seqs)
-                q0 = n_rows
-                seqs.append((KIND_FT, q0, n, -1, 0, n, -1, 0))
-                tc_seg.append(tc_block(si, n, n))
-                fs = len(ft_seqs)
-                ft_seqs.append((KIND_FT, q0 - ft0, n, -1, 0, n, -1, 0))
-                ft_tc_seg.append(tc_block(fs, n, n))
-                kblk = 128 if c.head_dim >= 64 else 64  # key block of the backward kernel (csrc/backward.cu)
-                nkb = (n + kblk - 1) // kblk
-                bw = np.zeros((Hkv * nkb, 4), i32)
-                bw[:, 0] = fs
-                bw[:, 1] = np.repeat(np.arange(Hkv, dtype=i32), nkb)
-                bw[:, 2] = np.tile(np.arange(nkb, dtype=i32), Hkv)
-                bw[:, 3] = nkb - bw[:, 2]  # query blocks the key block walks (LPT key)
-                bwd_seg.append(bw)
-                tok_seg.append(np.asarray(list(req.prompt_tokens) + list(resp), i32))
-                ten_seg.append(np.full(n, req.tenant, i32))
-                pos_seg.append(np.arange(n, dtype=i32))
-                seq_seg.append(np.full(n, si, i32))
-                kvi_seg.append(np.full(n, -1, i32))
-                ft_seq_seg.append(np.full(n, fs, i32))
-                pr += [n_logit, len(resp)]
-                lr_seg.append(np.arange(q0 + P - 1, q0 + P - 1 + len(resp), dtype=i32))
-                tg_seg.append(np.asarray(resp, i32))
-                ps_seg.append(np.full(len(resp), 2 * p_i + side, i32))
-                n_logit += len(resp)
-                n_rows += n
-                n_ft += n
+            # ONE sequence per pair, [prompt | chosen | prompt[-1] | rejected]: the prompt rows are computed once for
+            # both responses. The rejected branch re-enters at position P-1 with its own copy of the last prompt
+            # token and, through the sequence's key hole [P-1, P + n_c), sees prompt[:-1], that copy and itself --
+            # exactly the keys of a separate [prompt | rejected] sequence (MaceSeq hole0 / hole_len).
+            n_c, n_r = len(chs), len(rjs)
+            n = P + n_c + 1 + n_r
+            h0, hl = P - 1, 1 + n_c
+            si = n_seq + len(seqs)
+            q0 = n_rows
+            seqs.append((KIND_FT, q0, n, -1, 0, n, h0, hl))
+            tc_seg.append(tc_block(si, n, n))
+            fs = len(ft_seqs)
+            ft_seqs.append((KIND_FT, q0 - ft0, n, -1, 0, n, h0, hl))
+            ft_tc_seg.append(tc_block(fs, n, n))
+            kblk = 128 if c.head_dim >= 64 else 64  # key block of the backward kernel (csrc/backward.cu)
+            nkb = (n + kblk - 1) // kblk
+            bw = np.zeros((Hkv * nkb, 4), i32)
+            bw[:, 0] = fs
+            bw[:, 1] = np.repeat(np.arange(Hkv, dtype=i32), nkb)
+            bw[:, 2] = np.tile(np.arange(nkb, dtype=i32), Hkv)
+            bw[:, 3] = nkb - bw[:, 2]  # query blocks the key block walks (LPT key)
+            bwd_seg.append(bw)
+            prompt = list(req.prompt_tokens)
+            tok_seg.append(np.asarray(prompt + list(chs) + prompt[-1:] + list(rjs), i32))
+            pos_seg.append(np.concatenate([np.arange(P + n_c, dtype=i32), np.arange(P - 1, P + n_r, dtype=i32)]))
+            seq_seg.append(np.full(n, si, i32))
+            kvi_seg.append(np.full(n, -1, i32))
+            ten_seg.append(np.full(n, req.tenant, i32))
+            ft_seq_seg.append(np.full(n, fs, i32))
+            # logit rows: chosen[i] is predicted at row P-1+i, rejected[i] at row P+n_c+i (the copy of prompt[-1] first)
+            pr = [n_logit, n_c, n_logit + n_c, n_r]
+            lr_seg.append(np.arange(q0 + P - 1, q0 + P - 1 + n_c, dtype=i32))
+            lr_seg.append(np.arange(q0 + P + n_c, q0 + P + n_c + n_r, dtype=i32))
+            tg_seg.append(np.asarray(chs, i32))
+            tg_seg.append(np.asarray(rjs, i32))
+            ps_seg.append(np.full(n_c, 2 * p_i, i32))
+            ps_seg.append(np.full(n_r, 2 * p_i + 1, i32))
+            n_logit += n_c + n_r
+            n_rows += n
+            n_ft += n
             pair_rows.append(pr)
 
         def cat(segs, tail=None):
