@@ -11,7 +11,8 @@ from the hybrid step itself:
             latency = the tick's device time; tokens = B new KV tokens; memory = B x KV bytes per token
   finetune  one DPO pair alone in a tick: tokens = chosen + rejected, latency = the tick's device time (pi_ref
             and policy passes, fused DPO, backward of the selected layers, masked AdamW); memory = the fine-tune
-            row buffers (HybridModel.ft_bytes_per_token) x (2 x prompt + chosen + rejected)
+            row buffers (HybridModel.ft_bytes_per_token) x (prompt + chosen + 1 + rejected): one sequence per
+            pair, the prompt rows shared by both responses (engine.build_batch)
 
 Every point runs through the unmodified reference scheduler (GpuEngine mode "M" on a hand-built trace), so the
 measured tick is exactly the bin the scheduler forms; memory is counted from the buffers the step allocates.
@@ -106,7 +107,7 @@ def measure_rows(model, wl, prefill_tokens=(128, 256, 512, 1024, 2048), decode_b
                                        prompt_tokens=_prompt(rng, ft_prompt, cfg.vocab), target_output_len=c,
                                        pair=PreferencePair(0.5, c, r))])
             ms = [t for t, (p, d, f) in out if f == 1 and p == 0 and d == 0]
-            rows.append(("finetune", 1, c + r, ms[0], model.ft_bytes_per_token() * (2 * ft_prompt + c + r) / MB))
+            rows.append(("finetune", 1, c + r, ms[0], model.ft_bytes_per_token() * (ft_prompt + c + 1 + r) / MB))
     return rows
 
 
