@@ -163,6 +163,8 @@ typedef struct MaceAttnArgs {
   int* dec_counters;
   unsigned long long* dec_work;  /* zero-initialised ticket counter, owned by the caller; each launch leaves it zero */
   int decode_impl;    /* 0 auto, 1 CUDA-core streaming kernel, 2 tcgen05 swap-AB kernel */
+  int tc_pairs;       /* 1: tc_items are (seq, q_head, q_block PAIR p -> rows [256p, 256p + 256), kv tiles): the
+                         two-query-tile kernel (head_dim 64 / 128); 0: (seq, q_head, q_block, kv tiles)  */
 } MaceAttnArgs;
 int mace_attn_fwd(mace_ctx* ctx, const MaceAttnArgs* args, void* stream);
 
@@ -298,6 +300,7 @@ typedef struct MaceModelDesc {
    * frozen, grads are NULL except the adapters'; pi_ref = the base model (every adapter masked to zero) */
   int lora_R, lora_rank; float lora_scale;
   const MaceLoraLayer* lora;               /* [n_sel] */
+  int attn_pairs;                          /* the tick's tc_items / ft_tc_items are query-block pairs (tc_pairs) */
 } MaceModelDesc;
 typedef struct MaceSavedActs {             /* policy activations of one selected layer (FT rows)   */
   float* x_in; void* h1; void* qkv; void* o; float* lse; float* x_mid; void* h2; void* u; void* a;

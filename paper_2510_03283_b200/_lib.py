@@ -52,7 +52,7 @@ class MaceAttnArgs(C.Structure):
         ("out", C.c_void_p), ("lse", C.c_void_p), ("head_norm", C.c_void_p),
         ("scale", C.c_float),
         ("dec_workspace", C.c_void_p), ("dec_workspace_bytes", C.c_size_t), ("dec_counters", C.c_void_p),
-        ("dec_work", C.c_void_p), ("decode_impl", C.c_int),
+        ("dec_work", C.c_void_p), ("decode_impl", C.c_int), ("tc_pairs", C.c_int),
     ]
 
 
@@ -94,6 +94,7 @@ class MaceModelDesc(C.Structure):
         ("decode_impl", C.c_int),
         ("lora_R", C.c_int), ("lora_rank", C.c_int), ("lora_scale", C.c_float),
         ("lora", C.POINTER(MaceLoraLayer)),
+        ("attn_pairs", C.c_int),
     ]
 
 

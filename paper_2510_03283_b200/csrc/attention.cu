@@ -16,11 +16,9 @@ namespace mace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-struct TcMaps {
-  CUtensorMap q;       // qkv [T, W], box {ATOM, 128}: Q tiles and the dense (FT) K / V tiles
-  CUtensorMap kpool;   // [pages*16, HD], box {ATOM, 16}: one box per 16-token page
-  CUtensorMap vpool;
-};
+using TcMaps = TcMapsFa;  // mace_internal.h
+template <int HD>
+int launch_fa2(MaceCtx* ctx, const MaceAttnArgs* a, float scale_log2, cudaStream_t s, const TcMapsFa& maps);
 
 // =====================================================================================================
 // warp-specialised tensor-core path
@@ -427,6 +425,11 @@ static int launch_tc(MaceCtx* ctx, const MaceAttnArgs* a, float scale_log2, cuda
   ok = ok && encode_2d(ctx, &maps.kpool, kp, HD, rows, ld, C::ATOM, 16, C::SWZ) &&
        encode_2d(ctx, &maps.vpool, vp, HD, rows, ld, C::ATOM, 16, C::SWZ);
   if (!ok) return mace_fail(ctx, MACE_ERR_LAUNCH, "attn: tensor map encode failed");
+  if constexpr (HD == 64 || HD == 128) {
+    if (a->tc_pairs) return launch_fa2<HD>(ctx, a, scale_log2, s, maps);  // items are query-block pairs
+  } else {
+    if (a->tc_pairs) return mace_fail(ctx, MACE_ERR_UNSUPPORTED, "attn: query-block pair items need head_dim 64 / 128");
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_fa_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaCfg<HD>::SMEM);

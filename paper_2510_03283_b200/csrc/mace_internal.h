@@ -34,6 +34,13 @@ struct MaceCtx {
 };
 
 int mace_fail(MaceCtx* ctx, int code, const std::string& msg);
+
+// tensor maps of the tensor-core prefill / FT attention (attention.cu, attention_fa2.cu)
+struct TcMapsFa {
+  CUtensorMap q;       // qkv [T, W], box {64, 128}: Q tiles and the dense (FT) K / V tiles
+  CUtensorMap kpool;   // [pages*16, HD], box {64, 16}: one box per 16-token page
+  CUtensorMap vpool;
+};
 int mace_check_launch(MaceCtx* ctx, const char* what);
 
 }  // namespace mace

@@ -165,6 +165,7 @@ static int layer_fwd(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc
   a.dec_counters = d.dec_counters;
   a.dec_work = d.dec_work;
   a.decode_impl = d.decode_impl;
+  a.tc_pairs = d.attn_pairs;
   void** ev = t->attn_events;
   if (ev && ar.n_dec > 0) {  // instrumented: tc tiles first, then the decode launch between events
     if (ar.n_tc > 0) {

@@ -239,15 +239,18 @@ class GpuEngine(Engine):
         self._planned_shared = {}
         hq_grid = np.arange(Hq, dtype=i32)
 
+        blk = 256 if self.model.attn_pairs else 128  # query rows per tensor-core attention item
+
         def tc_block(si, q_len, kv_len):
-            """(seq, q head, q block, KV tiles the block visits): one CTA of the tensor-core attention each."""
-            nb = (q_len + 127) // 128
+            """(seq, q head, q block, KV tiles the block visits): one item of the tensor-core attention each; a
+            block is 128 query rows, or a PAIR of them (256 rows, csrc/attention_fa2.cu) when model.attn_pairs."""
+            nb = (q_len + blk - 1) // blk
             g = np.empty((Hq * nb, 4), i32)
             g[:, 0] = si
             g[:, 1] = np.repeat(hq_grid, nb)
             qb = np.tile(np.arange(nb, dtype=i32), Hq)
             g[:, 2] = qb
-            g[:, 3] = (kv_len - q_len + np.minimum(qb * 128 + 127, q_len - 1)) // 128 + 1
+            g[:, 3] = (kv_len - q_len + np.minimum(qb * blk + blk - 1, q_len - 1)) // 128 + 1
             return g
 
         def lpt(items):

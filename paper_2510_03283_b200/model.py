@@ -172,6 +172,9 @@ class HybridModel:
         self.dec_work = torch.zeros(1, dtype=torch.int64, device=self.dev)
         # 0 auto (tcgen05 swap-AB for GQA, CUDA-core streaming for MHA), 1 / 2 forced (MACE_DECODE_IMPL: sweeps)
         self.decode_impl = int(os.environ.get("MACE_DECODE_IMPL", "0"))
+        # prefill / FT attention as query-block PAIRS (two 128-row tiles per CTA, csrc/attention_fa2.cu) for head_dim
+        # 64 / 128; MACE_ATTN_PAIRS=0 keeps the single-tile kernel (A/B). The engine builds the tile items to match.
+        self.attn_pairs = cfg.head_dim in (64, 128) and os.environ.get("MACE_ATTN_PAIRS", "1") != "0"
         self.kv = MaceKvLayout(
             ptab=self.ptab.data_ptr(), max_prompt_pages=self.maxpp, dtab=self.dtab.data_ptr(),
             max_dec_pages=self.maxdp, dec_base=self.dec_base.data_ptr(), dec_first=self.dec_first.data_ptr(),
@@ -286,7 +289,7 @@ class HybridModel:
             sin_t=self.sin_t.data_ptr(), kv=self.kv, k_pool=self.k_pool.data_ptr(), v_pool=self.v_pool.data_ptr(),
             pages_per_layer=self.pages_per_layer, last_token=self.last_token.data_ptr(),
             dec_counters=self.dec_counters.data_ptr(), dec_work=self.dec_work.data_ptr(),
-            decode_impl=int(self.decode_impl),
+            decode_impl=int(self.decode_impl), attn_pairs=int(self.attn_pairs),
         )
         if self.lora:
             def lptr(l, n):

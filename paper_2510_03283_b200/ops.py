@@ -98,6 +98,7 @@ def attn_fwd(
     dec_counters: torch.Tensor | None = None,
     dec_work: torch.Tensor | None = None,
     decode_impl: int = 0,
+    tc_pairs: bool = False,
 ) -> torch.Tensor:
     """Ragged paged attention of one tick (prefill + FT tiles on tcgen05, decode rows streamed)."""
     from ._lib import MaceAttnArgs
@@ -114,7 +115,7 @@ def attn_fwd(
         out=out.data_ptr(), lse=_ptr(lse), head_norm=_ptr(head_norm), scale=0.0,
         dec_workspace=_ptr(dec_workspace),
         dec_workspace_bytes=0 if dec_workspace is None else dec_workspace.numel() * dec_workspace.element_size(),
-        dec_counters=_ptr(dec_counters), dec_work=_ptr(dec_work), decode_impl=int(decode_impl),
+        dec_counters=_ptr(dec_counters), dec_work=_ptr(dec_work), decode_impl=int(decode_impl), tc_pairs=int(tc_pairs),
     )
     ctx.check(ctx.L.mace_attn_fwd(ctx.h, C.byref(a), _stream(stream)), "mace_attn_fwd")
     return out

@@ -9,7 +9,8 @@ are asserted where they sit above that floor and reported (stats) everywhere:
   decode logits      rel-L2(gpu, f32) <= max(1e-2, 1.5 * rel-L2(bf16 emulation, f32)) per tick
   decode token ids   bit-exact, except oracle near-ties (top-1/top-2 gap < 0.05): counted, <= 5% of tokens
   DPO margin / loss  EXACT (m = 0, L = ln 2) while pi_theta == pi_ref (a pair's first step: same kernels, rows);
-                     otherwise, over all later steps: rms(gpu - f32) <= 1.5 * rms(bf16 emulation - f32) + 1e-3.
+                     otherwise, over all n later-step pairs: rms(gpu - f32) <= r * rms(bf16 emulation - f32) + 1e-3,
+                     r = max(1.5, sqrt(F_0.995(n, n))) (the rms ratio of two equal-variance noise samples of n pairs).
                      (A margin is a difference of two log-prob sums of hundreds of nats computed under weights a
                      few bf16 ulps apart; its bf16 rounding noise, ~0.05-0.5 nat, is far above §8(c)'s 1e-2 and is
                      shown by the independent emulation as much as by the device.)
@@ -32,6 +33,7 @@ import math
 
 import numpy as np
 import torch
+from scipy.stats import f as f_dist
 
 
 def adamw_np(p, m, v, g, lr, b1, b2, eps, wd, step):
@@ -191,10 +193,15 @@ def check_records(eng, w, cfg, tcfg, device="cpu", max_tie_frac=0.05, label=""):
     if st["dw_bad_frac"] > 1.5 * st["dw_bad_frac_bf16emu"] + 1e-3:
         fails.append(f"mean fraction of updated weights outside the bound {st['dw_bad_frac']:.3e} vs bf16 emulation "
                      f"{st['dw_bad_frac_bf16emu']:.3e}")
-    if st["dL_rms"] > 1.5 * st["dL_rms_bf16emu"] + 1e-3:
-        fails.append(f"DPO loss rms error {st['dL_rms']:.3e} vs bf16 emulation {st['dL_rms_bf16emu']:.3e}")
-    if st["dm_rms"] > 1.5 * st["dm_rms_bf16emu"] + 1e-3:
-        fails.append(f"DPO margin rms error {st['dm_rms']:.3e} vs bf16 emulation {st['dm_rms_bf16emu']:.3e}")
+    # the per-pair loss / margin errors of both implementations are draws of bf16 noise: the ratio of their rms over
+    # n pairs is sqrt(F(n, n))-distributed, so few-pair samples get the 99.5% quantile instead of the flat 1.5
+    n_pairs = len(dm_g)
+    ratio = max(1.5, float(np.sqrt(f_dist.ppf(0.995, n_pairs, n_pairs)))) if n_pairs else 1.5
+    st["pair_rms_ratio_bound"] = ratio
+    if st["dL_rms"] > ratio * st["dL_rms_bf16emu"] + 1e-3:
+        fails.append(f"DPO loss rms error {st['dL_rms']:.3e} vs bf16 emulation {st['dL_rms_bf16emu']:.3e} (x{ratio:.2f})")
+    if st["dm_rms"] > ratio * st["dm_rms_bf16emu"] + 1e-3:
+        fails.append(f"DPO margin rms error {st['dm_rms']:.3e} vs bf16 emulation {st['dm_rms_bf16emu']:.3e} (x{ratio:.2f})")
     if st["tokens"] and st["ties"] > max_tie_frac * st["tokens"]:
         fails.append(f"{st['ties']} near-tie token exemptions of {st['tokens']}")
     st["kinds"] = sorted(st["kinds"])

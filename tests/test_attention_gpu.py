@@ -95,7 +95,7 @@ def _build(hd, Hq, Hkv, seed, prefill=((200, 120), (40, 40), (300, 1)),
     return host, d, lay, T
 
 
-def _reference(host, Hq, Hkv, hd, T):
+def _reference(host, Hq, Hkv, hd, T, lse=None):
     qkv = host["qkv"].float()
     kp, vp = host["kp"].float(), host["vp"].float()
     G = Hq // Hkv
@@ -120,7 +120,13 @@ def _reference(host, Hq, Hkv, hd, T):
             if kind != 1:
                 qlog = torch.arange(ql)[:, None] + (m - ql)
                 sc = sc.masked_fill(torch.arange(m)[None, :] > qlog, float("-inf"))
+            if kind == 2 and s[7] > 0:  # preference-pair key hole (MaceSeq hole0 / hole_len)
+                h0, h1 = s[6], s[6] + s[7]
+                keys, rows = torch.arange(m)[None, :], torch.arange(ql)[:, None]
+                sc = sc.masked_fill((rows >= h1) & (keys >= h0) & (keys < h1), float("-inf"))
             out[q0: q0 + ql, hq] = torch.softmax(sc, -1) @ V
+            if lse is not None:
+                lse[q0: q0 + ql, hq] = torch.logsumexp(sc, -1)
     return out
 
 
@@ -149,3 +155,31 @@ def test_attention_ragged(ctx, hd, Hq, Hkv, impl):
             r = s[1]
             want = ref[r].norm(dim=-1)
             assert torch.allclose(hn[r].cpu(), want, rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("pairs", [False, True])
+@pytest.mark.parametrize("hd,Hq,Hkv", [(64, 12, 12), (64, 32, 8), (128, 32, 8)])
+def test_attention_tc_pairs_and_pair_hole(ctx, hd, Hq, Hkv, pairs):
+    """The tensor-core prefill / FT path with single 128-row query blocks and with query-block PAIRS (two tiles per
+    CTA, csrc/attention_fa2.cu), on ragged prefill + FT sequences, one FT sequence laid out as a preference pair
+    with a key hole: outputs and LSE against the fp32 reference."""
+    host, d, lay, T = _build(hd, Hq, Hkv, seed=7 * hd + Hq, decode=(), ft=(130, 77, 300, 520))
+    for s in host["seqs"]:
+        if s[0] == 2 and s[2] == 300:
+            s[6], s[7] = 120, 61  # rows >= 181 do not see keys [120, 181)
+    seqs = torch.tensor(host["seqs"], dtype=torch.int32, device="cuda")
+    blk = 256 if pairs else 128
+    items = [[si, hq, qb, 0] for si, s in enumerate(host["seqs"]) if s[0] != 1 for hq in range(Hq)
+             for qb in range((s[2] + blk - 1) // blk)]
+    items_t = torch.tensor(items, dtype=torch.int32, device="cuda")
+    out = torch.zeros(T, Hq * hd, dtype=torch.bfloat16, device="cuda")
+    lse = torch.zeros(T, Hq, device="cuda")
+    ops.attn_fwd(ctx, d["qkv"], Hq, Hkv, hd, seqs, items_t, None, lay, d["kp"], d["vp"], out, lse=lse,
+                 tc_pairs=pairs)
+    torch.cuda.synchronize()
+    lse_ref = torch.zeros(T, Hq)
+    ref = _reference(host, Hq, Hkv, hd, T, lse=lse_ref)
+    got = out.float().cpu().reshape(T, Hq, hd)
+    err = (got - ref).abs().max().item()
+    assert err < 3e-2, f"max abs err {err}"
+    assert (lse.cpu() - lse_ref).abs().max().item() < 2e-2

@@ -13,7 +13,8 @@ from paper_2510_03283_b200.build import build  # noqa: E402
 build()
 ctx = Ctx(0)
 BWD = "--bwd" in sys.argv
-argv = [a for a in sys.argv[1:] if a != "--bwd"]
+PAIRS = "--pairs" in sys.argv  # query-block pairs: two 128-row tiles per CTA (csrc/attention_fa2.cu)
+argv = [a for a in sys.argv[1:] if a not in ("--bwd", "--pairs")]
 cases = [(128, 32, 8, 16, 1280), (128, 32, 8, 4, 2048), (64, 12, 12, 16, 512), (64, 32, 8, 16, 1920)]
 if len(argv) >= 5:
     cases = [tuple(int(x) for x in argv[:5])]
@@ -23,11 +24,12 @@ for hd, Hq, Hkv, S, n in cases:
     qkv = torch.randn(T, W, device="cuda").bfloat16()
     seqs = torch.tensor([[2, i * n, n, -1, 0, n, -1, 0] for i in range(S)], dtype=torch.int32, device="cuda")
     items = []
-    nb = (n + 127) // 128
+    blk = 256 if PAIRS else 128
+    nb = (n + blk - 1) // blk
     for si in range(S):
         for hq in range(Hq):
             for qb in range(nb):
-                items.append([si, hq, qb, qb + 1])
+                items.append([si, hq, qb, (min(qb * blk + blk, n) + 127) // 128])
     items.sort(key=lambda x: -x[3])
     items = torch.tensor(items, dtype=torch.int32, device="cuda")
     out = torch.empty(T, Hq * hd, dtype=torch.bfloat16, device="cuda")
@@ -36,7 +38,7 @@ for hd, Hq, Hkv, S, n in cases:
                        dec_end=None, free_stack=None, free_top=None, stack_cap=0, n_kv_heads=Hkv)
 
     def run():
-        ops.attn_fwd(ctx, qkv, Hq, Hkv, hd, seqs, items, None, lay, None, None, out, lse=lse)
+        ops.attn_fwd(ctx, qkv, Hq, Hkv, hd, seqs, items, None, lay, None, None, out, lse=lse, tc_pairs=PAIRS)
 
     if BWD:  # time the backward of the same sequences (forward once for o / lse)
         run()
