@@ -239,7 +239,7 @@ class GpuEngine(Engine):
         self._planned_shared = {}
         hq_grid = np.arange(Hq, dtype=i32)
 
-        blk = 256 if self.model.attn_pairs else 128  # query rows per tensor-core attention item
+        blk = 256 if getattr(self.model, "attn_pairs", False) else 128  # query rows per tensor-core attention item
 
         def tc_block(si, q_len, kv_len):
             """(seq, q head, q block, KV tiles the block visits): one item of the tensor-core attention each; a
