@@ -89,6 +89,13 @@ def measure_rows(model, wl, prefill_tokens=(128, 256, 512, 1024, 2048), decode_b
         rid += 1
         return Request(id=rid, tenant=0, arrival_time=0.0, **kw)
 
+    # one discarded warm-up of every tick kind: the first launches of a process pay one-time costs (tensor-map
+    # and function-attribute set-up, allocator growth) that are not the device time of the workload
+    _run(model, wl, [req(workload=WorkloadType.PREFILL, prompt_tokens=_prompt(rng, min(256, lim), cfg.vocab),
+                         target_output_len=3),
+                     req(workload=WorkloadType.FINETUNE, prompt_tokens=_prompt(rng, min(64, lim // 2), cfg.vocab),
+                         target_output_len=8, pair=PreferencePair(0.5, 8, 8))])
+
     for _ in range(repeats):
         for n in prefill_tokens:  # prefill alone in its tick
             out = _run(model, wl, [req(workload=WorkloadType.PREFILL, prompt_tokens=_prompt(rng, n, cfg.vocab),

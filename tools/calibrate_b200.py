@@ -52,6 +52,10 @@ def main():
     rep = calibrated(csv, wl.profile)
     prof_path = ROOT / "profiles" / f"r2_profile_{wl.name}.txt"
     write_profile(rep.profile, prof_path)
+    out_dir = ROOT / "gpurun_out"  # the GPU box returns only gpurun_out/
+    out_dir.mkdir(exist_ok=True)
+    write_csv(rows, out_dir / csv.name)
+    write_profile(rep.profile, out_dir / prof_path.name)
     t_cal = time.time() - t0
     # mode M on the workload's own trace: the measured clock decides admissions / bins
     eng = GpuEngine(*wl.engine_args(), model=model, mode="M")
