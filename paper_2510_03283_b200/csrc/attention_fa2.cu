@@ -25,6 +25,14 @@ namespace mace {
 
 constexpr float kLog2eFa2 = 1.4426950408889634f;
 constexpr float kRescaleLog2Fa2 = 8.f;  // lazy rescale threshold: p <= 2^8 between rescales (fp32-safe)
+#ifndef MACE_FA2_EMU
+#define MACE_FA2_EMU 0
+#endif
+constexpr int kEmuFa2 = MACE_FA2_EMU;
+#ifndef MACE_FA2_F2FP
+#define MACE_FA2_F2FP 0
+#endif
+constexpr bool kF2fpFa2 = MACE_FA2_F2FP;  // pack P with one F2FP (XU pipe) per pair instead of three ALU ops  // score pairs of every 8 exponentiated on the FMA pipe (A/B: tools/attn_bench.py)
 
 template <int HD>
 struct Fa2Cfg {
@@ -285,15 +293,16 @@ __global__ void __launch_bounds__(384, 1)
           for (int cc = 0; cc < 128; ++cc)
             if (cc > lim || (cc >= hlo && cc < hhi)) sv[cc] = __float_as_uint(-INFINITY);
         }
-        float mx8[8];
+        float mx8[8];  // row max: 8 independent chains of 3-input max (FMNMX3), 2 new scores per instruction
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx8[i] = __uint_as_float(sv[i]);
 #pragma unroll
-        for (int cc = 8; cc < 128; cc += 8)
+        for (int cc = 8; cc < 120; cc += 16)
 #pragma unroll
-          for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], __uint_as_float(sv[cc + i]));
-        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+          for (int i = 0; i < 8; ++i) mx8[i] = fmax3(mx8[i], __uint_as_float(sv[cc + i]), __uint_as_float(sv[cc + 8 + i]));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], __uint_as_float(sv[120 + i]));
+        const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
         const float mx_s = mx * scale_log2;
         const bool grow = mx_s > m_run + kRescaleLog2Fa2;
         const float m_new = grow ? mx_s : m_run;
@@ -301,13 +310,17 @@ __global__ void __launch_bounds__(384, 1)
         const float alpha = resc ? exp2f(m_run - m_new) : 1.f;
         const float m_sub = m_new == -INFINITY ? 0.f : m_new;
         const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_sub, -m_sub);
+        const bool masked = lim < 127 || (hlo < 128 && hhi > 0) || m_new == -INFINITY;  // -inf scores: MUFU only
         float2 ps[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int cc = 0; cc < 128; cc += 2) {
           const float2 x = ffma2(make_float2(__uint_as_float(sv[cc]), __uint_as_float(sv[cc + 1])), sc2, nm2);
-          const float2 pv = make_float2(ex2_fast(x.x), ex2_fast(x.y));
+          // of every 8 score pairs, MACE_FA2_EMU on the FMA pipe (exp2_poly2) instead of MUFU (valid rows only)
+          const float2 pv = (kEmuFa2 > 0 && !masked && ((cc >> 1) & 7) < kEmuFa2) ? exp2_poly2(x)
+                                                                                  : make_float2(ex2_fast(x.x), ex2_fast(x.y));
           ps[(cc >> 1) & 3] = fadd2(ps[(cc >> 1) & 3], pv);
-          sv[cc / 2] = pack_bf16_alu(pv.x, pv.y);  // in place: pair cc/2 only overwrites consumed scores
+          sv[cc / 2] = kF2fpFa2 ? pack_bf16_cvt(pv.x, pv.y) : pack_bf16_alu(pv.x, pv.y);  // in place: pair cc/2
+                                                                                         // overwrites consumed scores
         }
         const float2 pss = fadd2(fadd2(ps[0], ps[1]), fadd2(ps[2], ps[3]));
         l_run = l_run * alpha + (pss.x + pss.y);

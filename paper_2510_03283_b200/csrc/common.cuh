@@ -366,6 +366,18 @@ MACE_DEV float2 exp2_poly2(float2 x) {
 MACE_DEV uint32_t pack_bf16_alu(float a, float b) {
   return __byte_perm(__float_as_uint(a) + 0x8000u, __float_as_uint(b) + 0x8000u, 0x7632);
 }
+// two fp32 -> packed bf16x2 (round to nearest even) in one F2FP instruction
+MACE_DEV uint32_t pack_bf16_cvt(float a, float b) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));  // a -> low half, b -> high half
+  return d;
+}
+// 3-input max (FMNMX3)
+MACE_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 // GPT-2 "gelu_new" with the MUFU tanh (tanh.approx.f32, ~2^-11 relative error: below the bf16 rounding
 // of the output it feeds); used in the GEMM epilogue where a libm tanhf per element costs more than the MMA
 MACE_DEV float gelu_tanh_fast(float x) {
