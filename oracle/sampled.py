@@ -63,7 +63,7 @@ def composition(engine, plan, max_pos: int) -> dict:
                 rows.append((KIND_FT, t, t + 1, P - 1 <= t < P - 1 + n_c))
             for i in range(n_r + 1):
                 rows.append((KIND_FT, P - 1 + i, P + i, i < n_r))
-                n_ft += P + n_resp
+            n_ft += P + n_c + 1 + n_r
     return {"rows": rows, "n_prefill": n_pre, "n_decode": n_dec, "n_ft": n_ft}
 
 
