@@ -381,19 +381,24 @@ def run_ours(args, rank, world, lock):
     # the roofline line is the workload's dominant kernel class: decode attention for the decode-carrying C1-C3
     # ticks, the projection GEMMs for the prefill-heavy C4; the other one rides along
     dominant_gemm = wl.name == "c4"
-    cap = {"c2": "attn_decode", "c3": "attn_decode_tc", "c4": "gemm_pair"}.get(wl.name)
-    prof = ROOT / "profiles" / "r2_ncu_full_summary.json"
-    if not prof.exists():
-        prof = ROOT / "profiles" / "r1final_ncu_full_summary.json"
-    if cap and prof.exists():
-        rows = [r for r in json.loads(prof.read_text()).get(cap, []) if "dram_read" in r]
-        if rows:
-            tr = float(np.mean([r["dram_read"] + r["dram_write"] for r in rows]))
-            target = roof_gemm if dominant_gemm else roof_attn
-            target["traffic"] = tr
-            target["traffic_source"] = f"profiles/{prof.name}[{cap}] ({rows[0]['kernel']}; one ncu --set full capture)"
-            if rows[0].get("algorithmic_bytes"):
-                target["traffic_over_algorithmic_in_capture"] = tr / float(np.mean([r["algorithmic_bytes"] for r in rows]))
+    # dram traffic per launch of each roofline kernel from the committed ncu --set full captures (newest first)
+    caps = {"c2": ("attn_decode", None), "c3": ("attn_decode_tc", None), "c4": ("gemm_pair", "attn_decode_tc")}
+    cap_dom, cap_other = caps.get(wl.name, (None, None))
+    summaries = [ROOT / "profiles" / n for n in ("r2s3_ncu_full_summary.json", "r2_ncu_full_summary.json",
+                                                  "r1final_ncu_full_summary.json")]
+    for cap, target in ((cap_dom, roof_gemm if dominant_gemm else roof_attn),
+                        (cap_other, roof_attn if dominant_gemm else roof_gemm)):
+        for prof in summaries:
+            rows = [r for r in json.loads(prof.read_text()).get(cap, []) if "dram_read" in r] \
+                if cap and prof.exists() else []
+            if rows:
+                tr = float(np.mean([r["dram_read"] + r["dram_write"] for r in rows]))
+                target["traffic"] = tr
+                target["traffic_source"] = f"profiles/{prof.name}[{cap}] ({rows[0]['kernel']}; one ncu --set full capture)"
+                if rows[0].get("algorithmic_bytes"):
+                    target["traffic_over_algorithmic_in_capture"] = tr / float(np.mean([r["algorithmic_bytes"]
+                                                                                          for r in rows]))
+                break
     out["roofline"] = roof_gemm if dominant_gemm else roof_attn
     out["roofline_other"] = roof_attn if dominant_gemm else roof_gemm
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
