@@ -213,7 +213,7 @@ def bench_config(wl, args, skip, world):
     """The ``config`` object -- identical in both arms (the driver compares them)."""
     cfg = wl.model
     a, b = skip + args.warmup, skip + args.warmup + args.steps
-    return {"workload": f"{wl.name}: {cfg.name} hybrid serving + DPO fine-tune ({wl.name.upper()})", "model": cfg.name,
+    return {"workload": f"{wl.name}: {cfg.name} hybrid serving + DPO fine-tune ({wl.name.upper()})",
             "trace": {"arrival_rate": wl.trace_cfg.arrival_rate, "retrain_rate": wl.trace_cfg.retrain_rate,
                       "prompt_len": str(wl.trace_cfg.prompt_len_dist), "output_len": str(wl.trace_cfg.output_len_dist),
                       "seed_rank0": wl.seed, "seeds": "base + rank"},
