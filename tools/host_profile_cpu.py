@@ -22,7 +22,7 @@ class StubModel:
         self.h2d_bytes = 0
 
     def step(self, batch, ft_global=None):
-        return SimpleNamespace(dec_tokens=None, ref_lp=None)
+        return SimpleNamespace(dec_tokens=None, ref_lp=None, head_norm=None, ft_loss=None)
 
     def apply_trim(self, slots, kept):
         pass
