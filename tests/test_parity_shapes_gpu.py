@@ -30,19 +30,27 @@ def _wl(name):
     return dataclasses.replace(wl, trace_cfg=dataclasses.replace(wl.trace_cfg, retrain_rate=0.5))
 
 
-@pytest.mark.parametrize("name,oracle_dev", [("c2", "cpu"), ("c3", "cuda"), ("c4", "cuda")])
+@pytest.mark.parametrize("name,oracle_dev", [("c2", "cpu"), ("c3", "cuda"), ("c4", "cuda"), ("c4-lora", "cuda")])
 def test_full_shape_sampled_ticks(ctx, name, oracle_dev):
+    """c4-lora: the bench's LoRA line (4 tenants, rank 16, every adapter non-zero from the start) at the 8B shape."""
     from paper_2510_03283_b200.engine import GpuEngine
     from paper_2510_03283_b200.model import HybridModel
     from paper_2510_03283_b200.weights import init_weights
 
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
-    wl = _wl(name)
+    wl = _wl(name.split("-")[0])
+    lora = {}
+    if name.endswith("-lora"):
+        from paper_2510_03283_b200.weights import init_lora
+        from paper_2510_03283_b200.workloads import with_tenants
+
+        wl = with_tenants(wl, [(0.5, 0.01), (-0.5, 0.05), (0.2, 0.02), (0.0, 0.01)], lora_rank=16)
+        lora = dict(n_tenants=wl.n_tenants, lora_weights=init_lora(wl.model, wl.train, wl.n_tenants, seed=5, b_std=0.01))
     cfg = wl.model
     w = init_weights(cfg, seed=0, device="cpu" if name == "c2" else "cuda")
     model = HybridModel(cfg, wl.train, w, max_slots=64, max_prompt_len=wl.max_prompt_len,
-                        max_decode_steps=wl.sched.max_decode_steps, prompt_groups=64 * wl.max_prompt_len // 16)
+                        max_decode_steps=wl.sched.max_decode_steps, prompt_groups=64 * wl.max_prompt_len // 16, **lora)
     eng = GpuEngine(*wl.engine_args(), model=model, mode="P", record=True)
     for _ in range(12):  # until a tick carries decode and fine-tune rows together (or 12 ticks)
         if eng.run_ticks(1) == 0:
