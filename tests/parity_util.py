@@ -11,7 +11,8 @@ are asserted where they sit above that floor and reported (stats) everywhere:
   DPO margin / loss  EXACT (m = 0, L = ln 2) while pi_theta == pi_ref (a pair's first step: same kernels, rows);
                      otherwise, over all n later-step pairs: rms(gpu - f32) <= r * rms(bf16 emulation - f32) + 1e-3,
                      r = max(1.5, sqrt(F_0.995(n, n))) (the rms ratio of two equal-variance noise samples of n pairs,
-                     n >= 5); and for every pair |m - m_f32| <= 0.5 nat, |L - L_f32| <= beta * |m - m_f32|.
+                     n >= 5); every pair |m - m_f32| <= max(0.5 nat, 2 x the emulation's worst) and
+                     |L - L_f32| <= beta * |m - m_f32|.
                      (A margin is a difference of two log-prob sums of hundreds of nats computed under weights a
                      few bf16 ulps apart; its bf16 rounding noise, ~0.05-0.5 nat, is far above §8(c)'s 1e-2 and is
                      shown by the independent emulation as much as by the device.)
@@ -207,8 +208,10 @@ def check_records(eng, w, cfg, tcfg, device="cpu", max_tie_frac=0.05, label=""):
     # absolute backstop for every pair: the margin within 0.5 nat of the fp32 oracle, the loss (1-Lipschitz in the
     # margin at beta <= 1) within that pair's margin error
     st["worst_dm"] = max((abs(x) for x in dm_g), default=0.0)
-    if st["worst_dm"] > 0.5:
-        fails.append(f"a DPO margin is {st['worst_dm']:.3f} nat from the fp32 oracle")
+    st["worst_dm_bf16emu"] = max((abs(x) for x in dm_b), default=0.0)
+    if st["worst_dm"] > max(0.5, 2.0 * st["worst_dm_bf16emu"]):
+        fails.append(f"a DPO margin is {st['worst_dm']:.3f} nat from the fp32 oracle (bf16 emulation's worst "
+                     f"{st['worst_dm_bf16emu']:.3f})")
     if any(abs(a) > max(1.0, tcfg.dpo_beta) * abs(b_) + 1e-3 for a, b_ in zip(dL_g, dm_g)):
         fails.append("a DPO loss error exceeds its margin error (the loss is beta-Lipschitz in the margin)")
     if st["tokens"] and st["ties"] > max_tie_frac * st["tokens"]:
