@@ -32,7 +32,11 @@ constexpr int kEmuFa2 = MACE_FA2_EMU;
 #ifndef MACE_FA2_F2FP
 #define MACE_FA2_F2FP 0
 #endif
-constexpr bool kF2fpFa2 = MACE_FA2_F2FP;  // pack P with one F2FP (XU pipe) per pair instead of three ALU ops  // score pairs of every 8 exponentiated on the FMA pipe (A/B: tools/attn_bench.py)
+constexpr bool kF2fpFa2 = MACE_FA2_F2FP;
+#ifndef MACE_FA2_INORDER
+#define MACE_FA2_INORDER 0
+#endif
+constexpr bool kInorderFa2 = MACE_FA2_INORDER;  // pack P with one F2FP (XU pipe) per pair instead of three ALU ops  // score pairs of every 8 exponentiated on the FMA pipe (A/B: tools/attn_bench.py)
 
 template <int HD>
 struct Fa2Cfg {
@@ -182,7 +186,9 @@ __global__ void __launch_bounds__(384, 1)
     int u[2] = {0, 0};   // items that used O of each block (phase of o_free)
     int g0 = 0;          // CTA-global KV tile index of the item's tile 0
     auto issue_s = [&](int b, int st) {  // S_b = Q_b K^T into TMEM (P_b.V of the previous tile is done)
-      if (c[b] > 0) mbar_wait(&pv_done[b], (c[b] - 1) & 1);
+      // MACE_FA2_INORDER: rely on the single issuing thread's tcgen05.mma executing in issue order (P_b.V reads
+      // the P columns before the next S_b writes them) instead of waiting for P_b.V's completion
+      if (!kInorderFa2 && c[b] > 0) mbar_wait(&pv_done[b], (c[b] - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t qa = smem_u32(smem + C::Q_OFF + b * C::TILE);
