@@ -230,6 +230,13 @@ int mace_bf16_to_f32(mace_ctx* ctx, const void* x, long long n, float* y, void* 
 int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, const void* dout, const float* lse, int n_rows, int Hq,
                   int Hkv, int hd, const MaceSeq* seqs, const int* items, int n_items, int row_offset, float* Dbuf,
                   float* dqkv, void* stream);
+/* the same with a deterministic dQ: dq_order int32 [n_rows * Hq] zeroed once by the caller (left zeroed by every
+ * call) orders the key blocks' dQ contributions of each (query block, query head) by ascending key block (an
+ * acquire / release counter per block) instead of fp32 atomics, so dQ -- and the whole FT step -- is bitwise
+ * reproducible. Items must be ordered by ascending key block within each (sequence, kv head) (LPT order is).   */
+int mace_attn_bwd2(mace_ctx* ctx, const void* qkv, const void* o, const void* dout, const float* lse, int n_rows, int Hq,
+                   int Hkv, int hd, const MaceSeq* seqs, const int* items, int n_items, int row_offset, float* Dbuf,
+                   float* dqkv, int* dq_order, void* stream);
 
 /* ---------------------------------------------------------------- (4) KV pages */
 /* pages are popped per (slot, head) whose ring is full; the host mirrors the count and refuses a tick that
@@ -320,6 +327,7 @@ typedef struct MaceTickBuffers {           /* device scratch sized by the caller
   float* ws; size_t ws_bytes;              /* split-K / reduction scratch                          */
   int ld_h;                                /* row stride of h and the saved h1 / h2 (d_model + lora_R; 0 = d)   */
   float* lz; void *lzm, *ldz;              /* LoRA scratch: Z fp32 [rows, R], Zm / dZ bf16 [rows, R]            */
+  int* dq_order;                           /* [n_ft * Hq] zeroed int32: deterministic dQ order (mace_attn_bwd2)  */
 } MaceTickBuffers;
 typedef struct MaceTickDesc {              /* device row tables of one tick (see TickBatch)        */
   int T, ft0, n_dec, R, n_pairs, need_ref; /* need_ref 0: ref_cached holds pi_ref log-probs       */

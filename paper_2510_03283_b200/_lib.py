@@ -116,6 +116,7 @@ class MaceTickBuffers(C.Structure):
         ("ws_bytes", C.c_size_t),
         ("ld_h", C.c_int),
         *[(n, C.c_void_p) for n in ("lz", "lzm", "ldz")],
+        ("dq_order", C.c_void_p),
     ]
 
 
@@ -184,6 +185,7 @@ SIGNATURES: dict[str, tuple[type, list]] = {
     "mace_f32_to_bf16": (C.c_int, [_vp, _vp, C.c_longlong, _vp, _vp]),
     "mace_bf16_to_f32": (C.c_int, [_vp, _vp, C.c_longlong, _vp, _vp]),
     "mace_attn_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _ip, _i, _i, _vp, _vp, _vp]),
+    "mace_attn_bwd2": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _ip, _i, _i, _vp, _vp, _vp, _vp]),
     "mace_kv_decode_alloc": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _i, _vp]),
     "mace_kv_status": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip]),
     "mace_kv_trim": (C.c_int, [_vp, C.POINTER(MaceKvLayout), _ip, _ip, _i, _vp]),

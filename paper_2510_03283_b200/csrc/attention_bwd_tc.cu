@@ -50,7 +50,8 @@ template <int HD>
 __global__ void __launch_bounds__(160, 1)
     attn_bwd_tc_kernel(const __grid_constant__ BwdMaps maps, const float* __restrict__ lse,
                        const float* __restrict__ Dv, const MaceSeq* __restrict__ seqs, const int4* __restrict__ items,
-                       int Hq, int Hkv, float scale, float* __restrict__ dqkv, int row_offset) {
+                       int Hq, int Hkv, float scale, float* __restrict__ dqkv, int row_offset,
+                       int* __restrict__ dq_order) {
   using C = BwdCfg<HD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -94,9 +95,12 @@ __global__ void __launch_bounds__(160, 1)
   pdl_wait();
   pdl_trigger();
 
+  // steps: query blocks DESCENDING (outer), the GQA group's query heads (inner). Every key block's CTA reaches a
+  // given (query block, head) at the same step index, so the ordered dQ accumulation (key block j waits for j - 1)
+  // costs one hand-off per level instead of a lag that grows with the head index
   auto step_q = [&](int s, int& hq, int& qb) {
-    hq = h * G + s / (nqb - j);
-    qb = j + s % (nqb - j);
+    hq = h * G + s % G;
+    qb = nqb - 1 - s / G;
   };
 
   if (warp == 4) {
@@ -234,9 +238,16 @@ __global__ void __launch_bounds__(160, 1)
       if (lane == 0) mbar_arrive(ds_ready);
       mbar_wait(mm_done, s & 1);
       tc_fence_after();
-      // ---- dQ rows (thread = query row) -> fp32 atomics
+      // ---- dQ rows (thread = query row). Key blocks j = 0..qb contribute to query block qb: with dq_order the
+      // contributions are added in ascending j (a per-(query block, head) counter: wait for j, add, publish j + 1;
+      // the last contributor resets it), so dQ is bitwise reproducible; without it, fp32 atomics
       const int qg = q0 + r;
       float* dq_row = dqkv + (size_t)(base + qg) * W + hq * HD;
+      int* ctr = dq_order ? dq_order + (size_t)(base + q0) * Hq + hq : nullptr;
+      if (ctr) {
+        if (r == 0) order_wait(ctr, j);
+        named_bar_sync(1, 128);
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < HD; c0 += 32) {
         uint32_t v[32];
@@ -244,10 +255,26 @@ __global__ void __launch_bounds__(160, 1)
         tmem_ld_wait();
         if (qg < n) {
 #pragma unroll
-          for (int c = 0; c < 32; c += 4)
-            red_add_v4(dq_row + c0 + c, __uint_as_float(v[c]) * scale, __uint_as_float(v[c + 1]) * scale,
-                       __uint_as_float(v[c + 2]) * scale, __uint_as_float(v[c + 3]) * scale);
+          for (int c = 0; c < 32; c += 4) {
+            if (ctr) {
+              float4* p4 = reinterpret_cast<float4*>(dq_row + c0 + c);
+              float4 x = __ldcg(p4);
+              x.x += __uint_as_float(v[c]) * scale;
+              x.y += __uint_as_float(v[c + 1]) * scale;
+              x.z += __uint_as_float(v[c + 2]) * scale;
+              x.w += __uint_as_float(v[c + 3]) * scale;
+              __stcg(p4, x);
+            } else {
+              red_add_v4(dq_row + c0 + c, __uint_as_float(v[c]) * scale, __uint_as_float(v[c + 1]) * scale,
+                         __uint_as_float(v[c + 2]) * scale, __uint_as_float(v[c + 3]) * scale);
+            }
+          }
         }
+      }
+      if (ctr) {
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (r == 0) order_release(ctr, j == qb ? 0 : j + 1);
       }
       tc_fence_before();
       __syncwarp();
@@ -297,7 +324,7 @@ static bool bwd_map(MaceCtx* ctx, CUtensorMap* m, const void* ptr, uint64_t inne
 template <int HD>
 static int launch_bwd_tc(MaceCtx* ctx, const void* qkv, const void* dout, const float* lse, int n_rows, int Hq, int Hkv,
                          const MaceSeq* seqs, const int* items, int n_items, int row_offset, const float* Dbuf,
-                         float* dqkv, cudaStream_t s) {
+                         float* dqkv, int* dq_order, cudaStream_t s) {
   using C = BwdCfg<HD>;
   BwdMaps maps;
   const int W = (Hq + 2 * Hkv) * HD;
@@ -309,17 +336,19 @@ static int launch_bwd_tc(MaceCtx* ctx, const void* qkv, const void* dout, const 
     attr = true;
   }
   launch_k(attn_bwd_tc_kernel<HD>, n_items, 160, C::SMEM, s, maps, lse, Dbuf, seqs,
-           reinterpret_cast<const int4*>(items), Hq, Hkv, 1.f / sqrtf((float)HD), dqkv, row_offset);
+           reinterpret_cast<const int4*>(items), Hq, Hkv, 1.f / sqrtf((float)HD), dqkv, row_offset, dq_order);
   ctx->launches++;
   return 0;
 }
 
 int attn_bwd_tc(MaceCtx* ctx, const void* qkv, const void* dout, const float* lse, int n_rows, int Hq, int Hkv, int hd,
                 const MaceSeq* seqs, const int* items, int n_items, int row_offset, const float* Dbuf, float* dqkv,
-                cudaStream_t s) {
+                int* dq_order, cudaStream_t s) {
   if (hd == 64)
-    return launch_bwd_tc<64>(ctx, qkv, dout, lse, n_rows, Hq, Hkv, seqs, items, n_items, row_offset, Dbuf, dqkv, s);
-  return launch_bwd_tc<128>(ctx, qkv, dout, lse, n_rows, Hq, Hkv, seqs, items, n_items, row_offset, Dbuf, dqkv, s);
+    return launch_bwd_tc<64>(ctx, qkv, dout, lse, n_rows, Hq, Hkv, seqs, items, n_items, row_offset, Dbuf, dqkv,
+                             dq_order, s);
+  return launch_bwd_tc<128>(ctx, qkv, dout, lse, n_rows, Hq, Hkv, seqs, items, n_items, row_offset, Dbuf, dqkv,
+                            dq_order, s);
 }
 
 }  // namespace mace

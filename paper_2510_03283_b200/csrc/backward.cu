@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256) attn_bwd_kernel(const __nv_bfloat16* __re
                                                        const float* __restrict__ lse, const float* __restrict__ Dv,
                                                        const MaceSeq* __restrict__ seqs, const int4* __restrict__ items,
                                                        int Hq, int Hkv, float scale, float* __restrict__ dqkv,
-                                                       int row_offset) {
+                                                       int row_offset, int* __restrict__ dq_order) {
   pdl_wait();
   pdl_trigger();
   constexpr int B = 64;
@@ -297,9 +297,13 @@ __global__ void __launch_bounds__(256) attn_bwd_kernel(const __nv_bfloat16* __re
 #pragma unroll
     for (int b = 0; b < DC; ++b) dK[a][b] = dV[a][b] = 0.f;
 
+  // query chunks at or after the key block, LAST chunk first (outer), the GQA group's heads inner: every key block
+  // reaches a given (query chunk, head) at the same iteration, so the ordered dQ hand-off does not accumulate lag
+  const int q_last = (n - 1) / B * B;
+  for (int q0 = q_last; q0 >= k0; q0 -= B)
   for (int g = 0; g < G; ++g) {
     const int hq = h * G + g;
-    for (int q0 = k0; q0 < n; q0 += B) {  // causal: query chunks at or after the key block
+    {
       __syncthreads();
       for (int i = tid; i < B * HD; i += 256) {
         const int r = i / HD, c = i % HD;
@@ -386,13 +390,30 @@ __global__ void __launch_bounds__(256) attn_bwd_kernel(const __nv_bfloat16* __re
           for (int a = 0; a < 4; ++a) dq[a][b] = fmaf(sa[a], k_, dq[a][b]);
         }
       }
+      // key blocks jb = 0..q0/B contribute to this query chunk: with dq_order in ascending jb (bitwise reproducible)
+      int* ctr = dq_order ? dq_order + (size_t)(base + q0) * Hq + hq : nullptr;
+      if (ctr) {
+        if (tid == 0) order_wait(ctr, jb);
+        __syncthreads();
+      }
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int qg = q0 + ty * 4 + a;
         if (qg < n) {
 #pragma unroll
-          for (int b = 0; b < DC; ++b) atomicAdd(&dqkv[(size_t)(base + qg) * W + hq * HD + tx * DC + b], dq[a][b] * scale);
+          for (int b = 0; b < DC; ++b) {
+            float* p = &dqkv[(size_t)(base + qg) * W + hq * HD + tx * DC + b];
+            if (ctr)
+              __stcg(p, __ldcg(p) + dq[a][b] * scale);
+            else
+              atomicAdd(p, dq[a][b] * scale);
+          }
         }
+      }
+      if (ctr) {
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) order_release(ctr, jb == q0 / B ? 0 : jb + 1);
       }
     }
   }
@@ -497,22 +518,23 @@ extern "C" int mace_bf16_to_f32(mace_ctx* ctx, const void* x, long long n, float
 namespace mace {
 int attn_bwd_tc(MaceCtx* ctx, const void* qkv, const void* dout, const float* lse, int n_rows, int Hq, int Hkv, int hd,
                 const MaceSeq* seqs, const int* items, int n_items, int row_offset, const float* Dbuf, float* dqkv,
-                cudaStream_t s);  // attention_bwd_tc.cu
+                int* dq_order, cudaStream_t s);  // attention_bwd_tc.cu
 }  // namespace mace
 
 // items int4 [n_items] = (seq, kv_head, key_block, steps); key blocks of 128 keys (head_dim 64 / 128: the tcgen05
 // kernel of attention_bwd_tc.cu) or 64 keys (head_dim 32: the CUDA-core kernel below). Rows of qkv/dout/lse/dqkv
 // are local to the FT
 // block starting at global row `row_offset`. dqkv must be zeroed by the caller (dq accumulates).
-extern "C" int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, const void* dout, const float* lse, int n_rows,
-                             int Hq, int Hkv, int hd, const MaceSeq* seqs, const int* items, int n_items, int row_offset,
-                             float* Dbuf, float* dqkv, void* stream) {
+extern "C" int mace_attn_bwd2(mace_ctx* ctx, const void* qkv, const void* o, const void* dout, const float* lse,
+                              int n_rows, int Hq, int Hkv, int hd, const MaceSeq* seqs, const int* items, int n_items,
+                              int row_offset, float* Dbuf, float* dqkv, int* dq_order, void* stream) {
   if (n_items <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   launch_k(attn_bwd_prep_kernel, (n_rows * Hq + 7) / 8, 256, 0, s, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, n_rows,
                                                              Hq, hd, Dbuf);
   if (hd == 64 || hd == 128) {  // tcgen05 path (128-key blocks)
-    const int rc = attn_bwd_tc(ctx, qkv, dout, lse, n_rows, Hq, Hkv, hd, seqs, items, n_items, row_offset, Dbuf, dqkv, s);
+    const int rc = attn_bwd_tc(ctx, qkv, dout, lse, n_rows, Hq, Hkv, hd, seqs, items, n_items, row_offset, Dbuf, dqkv,
+                               dq_order, s);
     if (rc) return rc;
     ctx->launches++;  // the prep kernel
     return mace_check_launch(ctx, "attn_bwd");
@@ -522,7 +544,7 @@ extern "C" int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, cons
     const size_t sh = (4 * 64 * (HD + 1) + 2 * 64 * 65 + 128) * sizeof(float);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
     launch_k(kern, n_items, 256, sh, s, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse, Dbuf, seqs,
-                                  reinterpret_cast<const int4*>(items), Hq, Hkv, scale, dqkv, row_offset);
+                                  reinterpret_cast<const int4*>(items), Hq, Hkv, scale, dqkv, row_offset, dq_order);
   };
   switch (hd) {
     case 32: go(attn_bwd_kernel<32>, 32); break;
@@ -532,4 +554,11 @@ extern "C" int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, cons
   }
   ctx->launches += 2;
   return mace_check_launch(ctx, "attn_bwd");
+}
+
+extern "C" int mace_attn_bwd(mace_ctx* ctx, const void* qkv, const void* o, const void* dout, const float* lse, int n_rows,
+                             int Hq, int Hkv, int hd, const MaceSeq* seqs, const int* items, int n_items, int row_offset,
+                             float* Dbuf, float* dqkv, void* stream) {
+  return mace_attn_bwd2(ctx, qkv, o, dout, lse, n_rows, Hq, Hkv, hd, seqs, items, n_items, row_offset, Dbuf, dqkv,
+                        nullptr, stream);
 }

@@ -78,6 +78,20 @@ MACE_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
 #endif
 }
 
+// ordered accumulation (deterministic dQ of the attention backward): spin until *ctr == want (acquire), and
+// publish the next value (release) once this block's contribution is written
+MACE_DEV void order_wait(const int* ctr, int want) {
+  int v;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v == want) break;
+    __nanosleep(64);
+  }
+}
+MACE_DEV void order_release(int* ctr, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
+}
+
 // named barrier among `count` threads (id 1..15; 0 is __syncthreads)
 MACE_DEV void named_bar_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

@@ -307,8 +307,8 @@ static int layer_bwd_lora(ModelState& m, const MaceTickBuffers* b, const MaceTic
   MACE_TRY(gemm(m, b, s, b->dy16, ldy, false, W.o_w, HO, true, n, HO, D + R, b->do16, HO, MACE_EPI_BF16, nullptr));
   // attention core (dense causal FT sequences)
   MACE_TRY(zero(m, b->dqkv, (size_t)n * QKV * 4, s));
-  MACE_TRY(mace_attn_bwd(m.ctx, sv.qkv, sv.o, b->do16, sv.lse, n, d.n_heads, d.n_kv_heads, d.head_dim, t->ft_seqs,
-                         t->bwd_items, t->n_bwd, 0, b->Dbuf, b->dqkv, s));
+  MACE_TRY(mace_attn_bwd2(m.ctx, sv.qkv, sv.o, b->do16, sv.lse, n, d.n_heads, d.n_kv_heads, d.head_dim, t->ft_seqs,
+                          t->bwd_items, t->n_bwd, 0, b->Dbuf, b->dqkv, b->dq_order, s));
   if (d.family == 0)
     MACE_TRY(mace_rope_bwd(m.ctx, b->dqkv, n, d.n_heads, d.n_kv_heads, d.head_dim, t->pos + t->ft0, d.cos_t, d.sin_t, s));
   MACE_TRY(mace_f32_to_bf16(m.ctx, b->dqkv, (long long)n * QKV, b->dqkv16, s));
@@ -354,8 +354,8 @@ static int layer_bwd(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc
   MACE_TRY(gemm(m, b, s, b->dy16, D, false, W.o_w, HO, true, n, HO, D, b->do16, HO, MACE_EPI_BF16, nullptr));
   // attention core (dense causal FT sequences)
   MACE_TRY(zero(m, b->dqkv, (size_t)n * QKV * 4, s));
-  MACE_TRY(mace_attn_bwd(m.ctx, sv.qkv, sv.o, b->do16, sv.lse, n, d.n_heads, d.n_kv_heads, d.head_dim, t->ft_seqs,
-                         t->bwd_items, t->n_bwd, 0, b->Dbuf, b->dqkv, s));
+  MACE_TRY(mace_attn_bwd2(m.ctx, sv.qkv, sv.o, b->do16, sv.lse, n, d.n_heads, d.n_kv_heads, d.head_dim, t->ft_seqs,
+                          t->bwd_items, t->n_bwd, 0, b->Dbuf, b->dqkv, b->dq_order, s));
   if (d.family == 0)
     MACE_TRY(mace_rope_bwd(m.ctx, b->dqkv, n, d.n_heads, d.n_kv_heads, d.head_dim, t->pos + t->ft0, d.cos_t, d.sin_t, s));
   MACE_TRY(mace_f32_to_bf16(m.ctx, b->dqkv, (long long)n * QKV, b->dqkv16, s));

@@ -134,13 +134,19 @@ def attn_bwd(
     items: torch.Tensor,
     dqkv: torch.Tensor | None = None,
     stream: torch.cuda.Stream | None = None,
+    ordered: bool = True,
 ) -> torch.Tensor:
     """Attention backward of dense causal sequences: dqkv fp32 [T, (Hq+2Hkv)*hd] (dQ, dK, dV in the qkv layout).
+    ordered: deterministic dQ accumulation (mace_attn_bwd2) instead of fp32 atomics.
     ``items`` int32 [n, 4] = (seq, kv_head, key_block, steps) with 128-key blocks (hd 64/128) or 64 (hd 32)."""
     T = qkv.shape[0]
     if dqkv is None:
         dqkv = torch.zeros(T, qkv.shape[1], dtype=torch.float32, device=qkv.device)
     Dbuf = torch.empty(T, Hq, dtype=torch.float32, device=qkv.device)
-    ctx.check(ctx.L.mace_attn_bwd(ctx.h, _ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), T, Hq, Hkv, hd, _ptr(seqs),
-                                  _ptr(items), items.shape[0], 0, _ptr(Dbuf), _ptr(dqkv), _stream(stream)), "attn_bwd")
+    order = torch.zeros(T * Hq, dtype=torch.int32, device=qkv.device) if ordered else None
+    ctx.check(ctx.L.mace_attn_bwd2(ctx.h, _ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), T, Hq, Hkv, hd, _ptr(seqs),
+                                   _ptr(items), items.shape[0], 0, _ptr(Dbuf), _ptr(dqkv), _ptr(order),
+                                   _stream(stream)), "attn_bwd")
+    if ordered:  # every counter is left at zero by its last contributor
+        assert int(order.abs().sum()) == 0
     return dqkv

@@ -14,7 +14,8 @@ build()
 ctx = Ctx(0)
 BWD = "--bwd" in sys.argv
 PAIRS = "--pairs" in sys.argv  # query-block pairs: two 128-row tiles per CTA (csrc/attention_fa2.cu)
-argv = [a for a in sys.argv[1:] if a not in ("--bwd", "--pairs")]
+ATOMIC = "--atomic" in sys.argv  # backward dQ by fp32 atomics instead of the ordered (deterministic) accumulation
+argv = [a for a in sys.argv[1:] if a not in ("--bwd", "--pairs", "--atomic")]
 cases = [(128, 32, 8, 16, 1280), (128, 32, 8, 4, 2048), (64, 12, 12, 16, 512), (64, 32, 8, 16, 1920)]
 if len(argv) >= 5:
     cases = [tuple(int(x) for x in argv[:5])]
@@ -52,7 +53,7 @@ for hd, Hq, Hkv, S, n in cases:
 
         def run():  # noqa: F811
             dqkv.zero_()
-            ops.attn_bwd(ctx, qkv, out, dout, lse, Hq, Hkv, hd, seqs, bitems, dqkv=dqkv)
+            ops.attn_bwd(ctx, qkv, out, dout, lse, Hq, Hkv, hd, seqs, bitems, dqkv=dqkv, ordered=not ATOMIC)
 
     for _ in range(3):
         run()
