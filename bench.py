@@ -336,6 +336,28 @@ def run_ours(args, rank, world, lock):
                  "peak_source": peak_src, "traffic": None, "share_of_step": g_ms / dev_ms if dev_ms else None,
                  "flops_per_launch_mean": g_flops / max(g_n, 1), "launches": g_n,
                  "share_note": "per-launch events break the PDL overlap of the value replay: shares are upper bounds"}
+    # ---- whole-tick roofline: measured GEMM FLOPs + tensor-core attention FLOPs at the tensor peak,
+    # measured decode-attention bytes + row-kernel bytes at the HBM peak, against the device time of the same ticks
+    from paper_2510_03283_b200.roofline import tick_extras
+
+    n_sel_l = wl.train.n_selected_layers
+    steps_ops = [op for op in tape if op[0] == "step"]
+    attn_f = row_b = 0.0
+    for op in steps_ops:
+        b_ = op[1]
+        n_upd = model.n_sel if not model.lora else \
+            model.n_sel // model.n_tenants * len({p_.tenant for p_ in b_.ft_pairs})
+        e_ = tick_extras(b_, cfg, n_sel_l, n_upd, model.lora)
+        attn_f += e_["attn_flops"]
+        row_b += e_["row_bytes"]
+    roof_ms = 1e3 * ((g_flops + attn_f) / (tc_peak * 1e12) + (sum(byts) + row_b) / (hbm_peak * 1e9))
+    dev_ms_rank = ev0.elapsed_time(ev1)
+    tick_roof = {"roofline_ms": roof_ms, "measured_ms": dev_ms_rank, "frac": roof_ms / dev_ms_rank if dev_ms_rank else None,
+                 "tensor_tflop": (g_flops + attn_f) / 1e12, "gemm_tflop": g_flops / 1e12, "attention_tflop": attn_f / 1e12,
+                 "hbm_gb": (sum(byts) + row_b) / 1e9, "decode_attention_gb": sum(byts) / 1e9, "row_kernels_gb": row_b / 1e9,
+                 "peaks": {"tensor_tflops": tc_peak, "hbm_gbs": hbm_peak, "source": peak_src},
+                 "note": "roofline time = tensor FLOPs / tensor peak + HBM bytes / HBM peak over the timed ticks "
+                         "(paper_2510_03283_b200/roofline.py); rank 0's ticks"}
     value = n_tokens / (dev_ms / 1e3)
     e2e = n_tokens / e2e_s
     n_ft_ticks = sum(1 for op in tape if op[0] == "step" and op[1].ft_pairs)
@@ -363,6 +385,7 @@ def run_ours(args, rank, world, lock):
                     "clock": "measured: device end-of-tick events of the e2e run (reference TBT, engine.py:130-143, "
                              "on the B200 clock; rank 0)"},
         "finetune_samples_per_s": lock.sum_over_ranks(n_pairs) / (dev_ms / 1e3),
+        "tick_roofline": tick_roof,
         "ft_ticks_in_timed_region": n_ft_ticks,
         "ft_pairs_in_timed_region": n_pairs,
         "per_gpu_tokens_per_s": value / world,
