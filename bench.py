@@ -401,19 +401,20 @@ def run_ours(args, rank, world, lock):
                  "share_of_step": attn_ms_total / dev_ms if dev_ms else None,
                  "bytes_per_launch_mean": float(np.mean(byts)) if byts else 0.0,
                  "launches": len(durs)}
-    # the roofline line is the workload's dominant kernel class: decode attention for the decode-carrying C1-C3
-    # ticks, the projection GEMMs for the prefill-heavy C4; the other one rides along
-    dominant_gemm = wl.name == "c4"
-    # dram traffic per launch of each roofline kernel from the committed ncu --set full captures (newest first)
-    caps = {"c2": ("attn_decode", None), "c3": ("attn_decode_tc", None), "c4": ("gemm_pair", "attn_decode_tc")}
-    cap_dom, cap_other = caps.get(wl.name, (None, None))
+    # the roofline line is the workload's dominant kernel class (larger measured share of the step: the projection
+    # GEMMs or the paged decode attention); the other one rides along
+    dominant_gemm = (roof_gemm["share_of_step"] or 0.0) >= (roof_attn["share_of_step"] or 0.0)
+    # dram traffic per launch of each roofline kernel from the committed ncu --set full captures (newest first);
+    # a capture is attached only when it profiled this workload's shape (same kernel template)
+    cap_gemm, cap_attn = {"c2": (None, "attn_decode"), "c4": ("gemm_pair", "attn_decode_tc")}.get(wl.name, (None, None))
     summaries = [ROOT / "profiles" / n for n in ("r2s3_ncu_full_summary.json", "r2_ncu_full_summary.json",
                                                   "r1final_ncu_full_summary.json")]
-    for cap, target in ((cap_dom, roof_gemm if dominant_gemm else roof_attn),
-                        (cap_other, roof_attn if dominant_gemm else roof_gemm)):
+    for cap, target in ((cap_gemm, roof_gemm), (cap_attn, roof_attn)):
         for prof in summaries:
             rows = [r for r in json.loads(prof.read_text()).get(cap, []) if "dram_read" in r] \
                 if cap and prof.exists() else []
+            if cap and cap.startswith("attn_decode"):
+                rows = [r for r in rows if f"<{cfg.head_dim}," in r.get("kernel", "")]
             if rows:
                 tr = float(np.mean([r["dram_read"] + r["dram_write"] for r in rows]))
                 target["traffic"] = tr

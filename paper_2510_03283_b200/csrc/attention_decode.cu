@@ -27,8 +27,9 @@ struct Dec2 {
   static constexpr int STAGES = HD >= 128 ? 3 : 4;
   static constexpr int PAGE = kPageTokens * HD * 2;
   static constexpr int STAGE = 2 * PAGE;                      // K page | V page
-  static constexpr int Q_OFF = STAGES * STAGE;                // fp32 [G][HD]
-  static constexpr int P_OFF = Q_OFF + G * HD * 4;            // fp32 [16][G]
+  static constexpr int QH = HD / 2 + 4;                       // padded half row of q (bank spread)
+  static constexpr int Q_OFF = STAGES * STAGE;                // fp32 [G][2][QH]
+  static constexpr int P_OFF = Q_OFF + G * 2 * QH * 4;        // fp32 [16][G]
   static constexpr int BAR_OFF = P_OFF + 16 * G * 4;          // STAGES mbarriers
   static constexpr int WARP_BYTES = ((BAR_OFF + STAGES * 8) + 127) / 128 * 128;
   static constexpr int SMEM = WARPS * WARP_BYTES;
@@ -57,7 +58,9 @@ __global__ void __launch_bounds__(Dec2<HD, G>::WARPS * 32) attn_decode2_kernel(
   pdl_wait();
   pdl_trigger();
   const int W = (Hq + 2 * Hkv) * HD;
-  const int t = lane & 15, half = lane >> 4;
+  // lane (t, half) = (lane >> 1, lane & 1): each 8-lane phase of a 16-byte shared load covers 4 tokens x 2 halves,
+  // and with the per-token chunk rotation below those are 8 distinct 4-bank groups (conflict-free K reads)
+  const int t = lane >> 1, half = lane & 1;
   uint32_t ring_count = 0;  // pages issued by this warp so far (mbarrier phase bookkeeping across items)
 
   while (true) {
@@ -81,7 +84,10 @@ __global__ void __launch_bounds__(Dec2<HD, G>::WARPS * 32) attn_decode2_kernel(
 #endif
     // ---- q of the G query heads of this kv group -> fp32 smem
     const __nv_bfloat16* qrow = qkv + (size_t)sq.q_start * W + (size_t)h * G * HD;
-    for (int i = lane; i < G * HD; i += 32) qs[i] = __bfloat162float(qrow[i]);
+    for (int i = lane; i < G * HD; i += 32) {
+      const int g = i / HD, d = i % HD;
+      qs[(g * 2 + d / (HD / 2)) * C::QH + d % (HD / 2)] = __bfloat162float(qrow[i]);
+    }
     // ---- this chunk's pages: prompt pages split evenly, the last chunk adds the decode window
     const int n_pv = sq.n_pv;
     const int npp = (n_pv + 15) / 16;
@@ -163,14 +169,16 @@ __global__ void __launch_bounds__(Dec2<HD, G>::WARPS * 32) attn_decode2_kernel(
         constexpr int NC = HD / 16;  // 16-byte chunks per half row
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          const int cc = (c + t) % NC;  // rotate chunks across lanes: spread smem banks
+          // rotate chunks across lanes so the 8 lanes of a load phase hit 8 distinct 4-bank groups (hd 128: the
+          // two halves of a row are 32 words apart, i.e. the same banks, so they rotate apart too)
+          const int cc = (HD >= 128 ? c + 2 * t + half : c + t) % NC;
           const uint4 u = *reinterpret_cast<const uint4*>(krow + cc * 8);
           const float2 k0 = bf2_to_f2(u.x), k1 = bf2_to_f2(u.y), k2 = bf2_to_f2(u.z), k3 = bf2_to_f2(u.w);
-          const float* qh = qs + half * (HD / 2) + cc * 8;
+          const float* qh = qs + half * C::QH + cc * 8;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
-            const float4 qa = *reinterpret_cast<const float4*>(qh + g * HD);
-            const float4 qb = *reinterpret_cast<const float4*>(qh + g * HD + 4);
+            const float4 qa = *reinterpret_cast<const float4*>(qh + g * 2 * C::QH);
+            const float4 qb = *reinterpret_cast<const float4*>(qh + g * 2 * C::QH + 4);
             sacc[g] = ffma2(make_float2(qa.x, qa.y), k0, sacc[g]);
             sacc[g] = ffma2(make_float2(qa.z, qa.w), k1, sacc[g]);
             sacc[g] = ffma2(make_float2(qb.x, qb.y), k2, sacc[g]);
@@ -183,16 +191,16 @@ __global__ void __launch_bounds__(Dec2<HD, G>::WARPS * 32) attn_decode2_kernel(
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         float sv = sacc[g].x + sacc[g].y;
-        sv += __shfl_xor_sync(0xffffffffu, sv, 16);
+        sv += __shfl_xor_sync(0xffffffffu, sv, 1);
         sv = valid ? sv * scale_log2 : -INFINITY;
         float mx = sv;
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (int o = 16; o > 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         const float mn = fmaxf(m[g], mx);
         const float p = valid ? exp2f(sv - mn) : 0.f;
         float sum = p;
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        for (int o = 16; o > 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         alpha[g] = (m[g] == -INFINITY) ? (mn == -INFINITY ? 1.f : 0.f) : exp2f(m[g] - mn);
         l[g] = l[g] * alpha[g] + sum;
         m[g] = mn;
@@ -205,6 +213,22 @@ __global__ void __launch_bounds__(Dec2<HD, G>::WARPS * 32) attn_decode2_kernel(
 #pragma unroll
         for (int d = 0; d < C::DPL; ++d) acc[g][d] *= alpha[g];
       const __nv_bfloat16* vpage = reinterpret_cast<const __nv_bfloat16*>(stage + C::PAGE);
+      if (G == 1 && C::DPL == 2 && lo == 0 && hi == 16) {
+        // full page (the common case): fully unrolled, two accumulator chains (even / odd tokens), p as float4
+        float2 e = make_float2(acc[0][0], acc[0][1]), o = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 pw = *reinterpret_cast<const float4*>(ps + q4 * 4);
+          const uint32_t* vr = reinterpret_cast<const uint32_t*>(vpage + (q4 * 4) * HD + lane * 2);
+          const uint32_t w0 = vr[0], w1 = vr[HD / 2], w2 = vr[HD], w3 = vr[3 * HD / 2];
+          e = ffma2(make_float2(pw.x, pw.x), bf2_to_f2(w0), e);
+          o = ffma2(make_float2(pw.y, pw.y), bf2_to_f2(w1), o);
+          e = ffma2(make_float2(pw.z, pw.z), bf2_to_f2(w2), e);
+          o = ffma2(make_float2(pw.w, pw.w), bf2_to_f2(w3), o);
+        }
+        acc[0][0] = e.x + o.x;
+        acc[0][C::DPL > 1 ? 1 : 0] = e.y + o.y;
+      } else
 #pragma unroll 4
       for (int tt = lo; tt < hi; ++tt) {
         float vv[C::DPL];
