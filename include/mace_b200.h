@@ -66,6 +66,11 @@ enum mace_epilogue {
   MACE_EPI_BF16_GELU = 4,  /* out bf16 = gelu_tanh(result) (fused GPT-2 MLP activation) */
   MACE_EPI_BF16_SWIGLU = 5,/* out bf16 [M, N] = silu(A.Bg^T) * (A.Bu^T) with B = [gate rows 0..N-1; up rows
                               N..2N-1] (K-major, no bias): the fused Llama MLP activation */
+  MACE_EPI_ARGMAX = 6,     /* greedy decode head: out = uint64 keys [M], ZEROED before the call; every row's key is
+                              atomically max-reduced to (orderable fp32 bits of its largest result << 32) |
+                              (0xffffffff - first column holding it), i.e. the argmax over N with the lowest index on
+                              ties, without materialising the [M, N] logits (ldo, bias unused; no split-K).
+                              mace_argmax_keys turns the keys into token ids and re-zeroes them. */
 };
 typedef struct MaceGemmArgs {
   const void* a; int lda; int a_mn_major;
@@ -135,6 +140,9 @@ int mace_rope_kv(mace_ctx* ctx, void* qkv, int T, int Hq, int Hkv, int hd, const
                  const MaceKvLayout* kv, void* k_pool, void* v_pool, void* stream);
 int mace_act(mace_ctx* ctx, const void* u, int T, int F, int swiglu, void* out, void* stream);
 int mace_argmax(mace_ctx* ctx, const float* logits, int n, int V, int ld, int* out, void* stream);
+/* keys of a MACE_EPI_ARGMAX GEMM -> out[i] = argmax column of row i; keys[0..n) are reset to 0 (ready for the
+ * next call). Same result as mace_argmax over the materialised fp32 logits (first index on ties). */
+int mace_argmax_keys(mace_ctx* ctx, unsigned long long* keys, int n, int* out, void* stream);
 
 /* ---------------------------------------------------------------- (1) ragged paged attention fwd
  * Prefill and fine-tune sequences run as tcgen05 tiles (128 query rows x one query head; S = QK^T
@@ -328,6 +336,8 @@ typedef struct MaceTickBuffers {           /* device scratch sized by the caller
   int ld_h;                                /* row stride of h and the saved h1 / h2 (d_model + lora_R; 0 = d)   */
   float* lz; void *lzm, *ldz;              /* LoRA scratch: Z fp32 [rows, R], Zm / dZ bf16 [rows, R]            */
   int* dq_order;                           /* [n_ft * Hq] zeroed int32: deterministic dQ order (mace_attn_bwd2)  */
+  unsigned long long* dec_keys;            /* [n_dec] zeroed: fused lm_head + argmax (MACE_EPI_ARGMAX); NULL = write
+                                              dec_logits [n_dec, ld_vocab] and take the argmax over them          */
 } MaceTickBuffers;
 typedef struct MaceTickDesc {              /* device row tables of one tick (see TickBatch)        */
   int T, ft0, n_dec, R, n_pairs, need_ref; /* need_ref 0: ref_cached holds pi_ref log-probs       */

@@ -117,6 +117,7 @@ class MaceTickBuffers(C.Structure):
         ("ld_h", C.c_int),
         *[(n, C.c_void_p) for n in ("lz", "lzm", "ldz")],
         ("dq_order", C.c_void_p),
+        ("dec_keys", C.c_void_p),
     ]
 
 
@@ -165,6 +166,7 @@ SIGNATURES: dict[str, tuple[type, list]] = {
                                C.POINTER(MaceKvLayout), _vp, _vp, _vp]),
     "mace_act": (C.c_int, [_vp, _vp, _i, _i, _i, _vp, _vp]),
     "mace_argmax": (C.c_int, [_vp, _vp, _i, _i, _i, _ip, _vp]),
+    "mace_argmax_keys": (C.c_int, [_vp, _vp, _i, _ip, _vp]),
     "mace_attn_fwd": (C.c_int, [_vp, C.POINTER(MaceAttnArgs), _vp]),
     "mace_dpo_fused": (C.c_int, [_vp, _vp, _i, _i, _i, _ip, _ip, _i, _ip, _vp, _f, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _i, _vp]),

@@ -311,6 +311,17 @@ __global__ void act_kernel(const __nv_bfloat16* __restrict__ u, int T, int F, in
   }
 }
 
+// ------------------------------------------------------------------ keys of the fused lm_head argmax -> token ids
+__global__ void argmax_keys_kernel(unsigned long long* __restrict__ keys, int n, int* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    out[i] = (int)(0xffffffffu - (uint32_t)(keys[i] & 0xffffffffull));
+    keys[i] = 0ull;  // ready for the next MACE_EPI_ARGMAX GEMM
+  }
+}
+
 // ------------------------------------------------------------------ argmax over fp32 logits rows
 __global__ void argmax_kernel(const float* __restrict__ logits, int V, int ld, int* __restrict__ out) {
   pdl_wait();
@@ -431,6 +442,14 @@ extern "C" int mace_act(mace_ctx* ctx, const void* u, int T, int F, int swiglu, 
   launch_k(act_kernel, grid, 256, 0, (cudaStream_t)stream, (const __nv_bfloat16*)u, T, F, swiglu, (__nv_bfloat16*)out);
   ctx->launches++;
   return mace_check_launch(ctx, "act");
+}
+
+extern "C" int mace_argmax_keys(mace_ctx* ctx, unsigned long long* keys, int n, int* out, void* stream) {
+  if (!ctx || (n > 0 && (!keys || !out))) return MACE_ERR_ARG;
+  if (n <= 0) return 0;
+  launch_k(argmax_keys_kernel, (n + 255) / 256, 256, 0, (cudaStream_t)stream, keys, n, out);
+  ctx->launches++;
+  return mace_check_launch(ctx, "argmax_keys");
 }
 
 extern "C" int mace_argmax(mace_ctx* ctx, const float* logits, int n, int V, int ld, int* out, void* stream) {

@@ -105,6 +105,38 @@ MACE_DEV void swiglu_epilogue(const CUtensorMap* map_c, uint8_t* smem_c, uint32_
   }
 }
 
+// fused greedy decode head (EPI_ARGMAX): this thread's accumulator row over the tile's columns -> (largest value,
+// first column holding it), in ascending column order; tcgen05.ld is warp-collective, the loop bound is warp-uniform
+template <int BN>
+MACE_DEV void argmax_row(uint32_t t_row, int col_base, int N, float alpha, float& best, int& bi) {
+  best = -INFINITY;
+  bi = 0x7fffffff;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    if (col_base + c0 >= N) break;
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(t_row + c0, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float v = __uint_as_float(r[j]) * alpha;
+      if (col_base + c0 + j < N && v > best) {
+        best = v;
+        bi = col_base + c0 + j;
+      }
+    }
+  }
+}
+
+// the row's key: orderable fp32 bits in the high word, the complemented column in the low word, so atomicMax picks
+// the largest value and, among equal values, the lowest column (order-independent: deterministic)
+MACE_DEV void argmax_publish(unsigned long long* keys, int row, int M, float best, int bi) {
+  if (row >= M || bi == 0x7fffffff) return;
+  uint32_t b = __float_as_uint(best);
+  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  atomicMax(keys + row, ((unsigned long long)b << 32) | (unsigned long long)(0xffffffffu - (uint32_t)bi));
+}
+
 #ifdef MACE_GEMM_TRACE
 // phase timestamps (%globaltimer ns) per CTA, tools/gemm_trace.py: [cta][32]
 __device__ unsigned long long* g_gemm_trace = nullptr;
@@ -326,6 +358,20 @@ __global__ void __launch_bounds__(256, 1)
       const int ti_ = (t - (int)blockIdx.x) / (int)gridDim.x;
       if (warp == 4 && lane == 0 && ti_ < 5) TRACE(8 + ti_ * 4 + 1);
 #endif
+      if (ep.mode == EPI_ARGMAX) {
+        float best;
+        int bi;
+        argmax_row<BN>(tmem_base + ((quarter * 32u) << 16) + acc * BN, n_blk * BN, p.N, ep.alpha, best, bi);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        argmax_publish(reinterpret_cast<unsigned long long*>(ep.out), m_blk * kBM + quarter * 32 + lane, p.M, best, bi);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
       if constexpr (TMA_EPI) {
         if (p.swiglu) {
           swiglu_epilogue<BN>(&map_c, smem_c, tmem_base + ((quarter * 32u) << 16) + acc * BN, quarter, lane,
@@ -688,6 +734,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row0 = m_blk * 256 + rank * 128 + quarter * 32;
+      if (ep.mode == EPI_ARGMAX) {
+        float best;
+        int bi;
+        argmax_row<BN>(tmem_base + ((quarter * 32u) << 16) + acc * BN, n_blk * BN, p.N, ep.alpha, best, bi);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+        argmax_publish(reinterpret_cast<unsigned long long*>(ep.out), row0 + lane, p.M, best, bi);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
       if (p.swiglu) {
         swiglu_epilogue<BN>(&map_c, smem_c, tmem_base + ((quarter * 32u) << 16) + acc * BN, quarter, lane, row0,
                             n_blk * (BN / 2), p.N, nullptr, true, tempty0 + acc * 8);
@@ -921,7 +981,10 @@ static int launch_gemm2(MaceCtx* ctx, const MaceGemmArgs* g, cudaStream_t stream
   p.c_reduce = ep.mode == EPI_F32_ADD || ep.mode == EPI_F32_ATOMIC;
   p.b_static = (g->flags & MACE_GEMM_B_STATIC) ? 1 : 0;
   p.dbg = 0;
-  if (make_map_c(ctx, &mc, ep, g->M, g->N, 1)) return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm2: tensor map C encode failed");
+  if (ep.mode == EPI_ARGMAX)
+    mc = ma;  // unused: the argmax epilogue publishes keys with atomics
+  else if (make_map_c(ctx, &mc, ep, g->M, g->N, 1))
+    return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm2: tensor map C encode failed");
   auto kern = gemm_tc2_kernel<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -947,7 +1010,7 @@ static int dispatch_major_t(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cud
 template <int BN>
 static int dispatch_major(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStream_t s, const GemmEpilogue& ep) {
   static const bool no_tma_epi = getenv("MACE_GEMM_NO_TMA_EPI") != nullptr;  // A/B comparisons only
-  if (tma_epi_ok(ep) && !no_tma_epi) return dispatch_major_t<BN, true>(ctx, g, splits, s, ep);
+  if (ep.mode != EPI_ARGMAX && tma_epi_ok(ep) && !no_tma_epi) return dispatch_major_t<BN, true>(ctx, g, splits, s, ep);
   return dispatch_major_t<BN, false>(ctx, g, splits, s, ep);
 }
 
@@ -969,7 +1032,10 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 0;  // empty ragged batch: nothing to do
   if ((g->lda & 7) || (g->ldb & 7) || ((uintptr_t)g->a & 15) || ((uintptr_t)g->b & 15))
     return mace_fail(ctx, MACE_ERR_ARG, "gemm: operands need 16-byte aligned rows (ld % 8 == 0)");
-  if (g->mode < EPI_BF16 || g->mode > EPI_BF16_SWIGLU) return mace_fail(ctx, MACE_ERR_ARG, "gemm: bad epilogue mode");
+  if (g->mode < EPI_BF16 || g->mode > EPI_ARGMAX) return mace_fail(ctx, MACE_ERR_ARG, "gemm: bad epilogue mode");
+  const bool argmax = g->mode == EPI_ARGMAX;
+  if (argmax && (g->bias || g->split_k > 1 || ((uintptr_t)g->out & 7)))
+    return mace_fail(ctx, MACE_ERR_ARG, "gemm: the argmax epilogue takes 8-byte aligned keys, no bias, no split-K");
   const bool swiglu = g->mode == EPI_BF16_SWIGLU;
   if (swiglu && (g->a_mn_major || g->b_mn_major || g->bias || g->split_k > 1))
     return mace_fail(ctx, MACE_ERR_UNSUPPORTED, "gemm: SwiGLU epilogue needs K-major operands, no bias, no split-K");
@@ -986,8 +1052,8 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   const int num_m2 = (g->M + 255) / 256;
   const int kb_total = (g->K + kBK - 1) / kBK;
   const bool pair_ok = !g->a_mn_major && !g->b_mn_major && g->split_k <= 0 && g->mode != EPI_F32_ATOMIC &&
-                       ((uintptr_t)g->out & 15) == 0 &&
-                       ((size_t)g->ldo * ((g->mode == EPI_BF16 || g->mode == EPI_BF16_GELU || swiglu) ? 2 : 4)) % 16 == 0;
+                       (argmax || (((uintptr_t)g->out & 15) == 0 &&
+                        ((size_t)g->ldo * ((g->mode == EPI_BF16 || g->mode == EPI_BF16_GELU || swiglu) ? 2 : 4)) % 16 == 0));
   const long sms = ctx->num_sms, pairs = ctx->num_sms / 2;
   int bn = 128, pair_bn = 0;
   if (swiglu) {  // 256-wide accumulator tiles = 128 gate + 128 up columns of the same 128 outputs
@@ -1016,7 +1082,7 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     }
   }
   int splits = g->split_k > 0 ? g->split_k : 1;
-  if (g->split_k <= 0 && !swiglu && kb_total >= 96 && (long)num_m * ((g->N + 127) / 128) < pairs) {
+  if (g->split_k <= 0 && !swiglu && !argmax && kb_total >= 96 && (long)num_m * ((g->N + 127) / 128) < pairs) {
     // long K over few tiles (decode-sized down projections, FT dW): split K across the idle SMs (BN 128)
     bn = 128;
     pair_bn = 0;
@@ -1027,7 +1093,7 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     if (splits < 1) splits = 1;
   }
   // tuning override (tools/gemm_sweep.py): MACE_GEMM_FORCE="<bn>,<splits>" | "pair,<bn>" | "single"
-  if (const char* f = getenv("MACE_GEMM_FORCE"); f && !swiglu) {
+  if (const char* f = getenv("MACE_GEMM_FORCE"); f && !swiglu && !argmax) {
     int fb = 0, fs = 0;
     if (sscanf(f, "%d,%d", &fb, &fs) == 2) {
       if (fb == 64 || fb == 128 || fb == 192 || fb == 256) bn = fb;

@@ -14,7 +14,7 @@ namespace mace {
 
 constexpr int kPageTokens = MACE_PAGE_TOKENS;
 
-enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ADD = 2, EPI_F32_ATOMIC = 3, EPI_BF16_GELU = 4, EPI_BF16_SWIGLU = 5 };
+enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ADD = 2, EPI_F32_ATOMIC = 3, EPI_BF16_GELU = 4, EPI_BF16_SWIGLU = 5, EPI_ARGMAX = 6 };
 
 struct GemmEpilogue {
   void* out;

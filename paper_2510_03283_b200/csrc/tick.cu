@@ -435,9 +435,15 @@ static int tick_run(ModelState& m, const MaceTickBuffers* b, const MaceTickDesc*
   if (t->n_dec > 0) {
     MACE_TRY(mace_norm(ctx, b->x, D, t->dec_rows, t->n_dec, D, d.final_norm_w, d.final_norm_b, d.family == 1, d.norm_eps,
                        b->dec_h, D, nullptr, s));
-    MACE_TRY(gemm(m, b, s, b->dec_h, D, false, d.embed, D, false, t->n_dec, d.vocab, D, b->dec_logits, b->ld_vocab,
-                  MACE_EPI_F32, nullptr));
-    MACE_TRY(mace_argmax(ctx, b->dec_logits, t->n_dec, d.vocab, b->ld_vocab, b->dec_tok, s));
+    if (b->dec_keys) {  // fused: the lm_head epilogue reduces every row to its argmax key, no [n_dec, V] logits
+      MACE_TRY(gemm(m, b, s, b->dec_h, D, false, d.embed, D, false, t->n_dec, d.vocab, D, b->dec_keys, 0,
+                    MACE_EPI_ARGMAX, nullptr));
+      MACE_TRY(mace_argmax_keys(ctx, b->dec_keys, t->n_dec, b->dec_tok, s));
+    } else {            // logits kept for the caller (oracle replays read them)
+      MACE_TRY(gemm(m, b, s, b->dec_h, D, false, d.embed, D, false, t->n_dec, d.vocab, D, b->dec_logits, b->ld_vocab,
+                    MACE_EPI_F32, nullptr));
+      MACE_TRY(mace_argmax(ctx, b->dec_logits, t->n_dec, d.vocab, b->ld_vocab, b->dec_tok, s));
+    }
     MACE_TRY(mace_scatter_tokens(ctx, b->dec_tok, t->dec_slots, t->n_dec, d.last_token, s));
   }
   if (has_ft) MACE_TRY(ft_step(m, b, t, s));

@@ -156,6 +156,8 @@ class GpuEngine(Engine):
         self.ref_lp: dict[int, tuple[float, float]] = {}
         self._pending_ref: list = []
         self.record = record
+        if record:  # the oracle replay compares the decode logits
+            model.keep_dec_logits = True
         self.records: list[dict] = []
         self.tick_tokens: list[int] = []
         self.tick_device_ms: list = []      # (start, end) CUDA events per tick (mode M / time_ticks)

@@ -199,6 +199,9 @@ class HybridModel:
         self._attn_bytes = 0
         self.idx = torch.empty(1 << 16, dtype=torch.int32, device=self.dev)
         self._bufs = MaceTickBuffers()
+        # True: the decode head writes the fp32 logits [n_dec, V] and takes the argmax over them (recorded oracle
+        # replays read the logits); False: the lm_head GEMM's epilogue reduces each row to its argmax directly
+        self.keep_dec_logits = False
         self.mh = self._create_native()
 
     def _build_lora(self, lw: dict[str, torch.Tensor]) -> None:
@@ -413,6 +416,7 @@ class HybridModel:
             self.dec_h = torch.empty(cap, c.d_model, **bf)
             self.dec_logits = torch.empty(cap, self.vpad, **f32)
             self.dec_tok = torch.empty(cap, dtype=torch.int32, device=dev)
+            self.dec_keys = torch.zeros(cap, dtype=torch.int64, device=dev)  # fused argmax keys (self-cleaning)
             self.dec_ws = torch.empty(cap * c.n_kv_heads * 4 * (2 * c.group + c.group * c.head_dim), **f32)
             self._ndec_cap = cap
             grew = True
@@ -457,6 +461,7 @@ class HybridModel:
             for n in ("dec_h", "dec_logits", "dec_tok", "dec_ws"):
                 setattr(b, n, getattr(self, n).data_ptr())
             b.dec_ws_bytes = self.dec_ws.numel() * 4
+            b.dec_keys = self.dec_keys.data_ptr()
         if self._P_cap:
             b.lp, b.ref_lp, b.loss = self.dpo_lp.data_ptr(), self.dpo_ref_lp.data_ptr(), self.dpo_loss.data_ptr()
             b.margin, b.coef = self.dpo_margin.data_ptr(), self.dpo_coef.data_ptr()
@@ -563,6 +568,8 @@ class HybridModel:
             gcount = np.zeros(1, np.int32)
             d.gemm_events, d.gemm_events_cap = C.cast(self._gev_arr, C.c_void_p), cap
             d.gemm_flops, d.gemm_count = self._gflops.ctypes.data, gcount.ctypes.data
+        if self._ndec_cap:  # fused lm_head argmax unless the caller reads the decode logits (oracle replays)
+            self._bufs.dec_keys = None if self.keep_dec_logits else self.dec_keys.data_ptr()
         self.ctx.check(self.ctx.L.mace_tick_run(self.mh, C.byref(self._bufs), C.byref(d), self._s), "mace_tick_run")
         if gcount is not None:
             torch.cuda.synchronize(self.dev)

@@ -11,7 +11,7 @@ import torch
 
 from ._lib import Ctx, MaceGemmArgs
 
-EPI = {"bf16": 0, "f32": 1, "f32_add": 2, "f32_atomic": 3, "bf16_gelu": 4, "bf16_swiglu": 5}
+EPI = {"bf16": 0, "f32": 1, "f32_add": 2, "f32_atomic": 3, "bf16_gelu": 4, "bf16_swiglu": 5, "argmax": 6}
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -58,23 +58,39 @@ def gemm(
     if mode == "bf16_swiglu":  # b = [gate; up] stacked: 2N rows, N outputs
         assert N % 2 == 0 and not b_mn
         N //= 2
-    if out is None:
-        assert mode in ("bf16", "f32", "bf16_gelu", "bf16_swiglu")
-        out = torch.empty(M, N, device=a.device, dtype=torch.float32 if mode == "f32" else torch.bfloat16)
-    assert out.shape[0] >= M and out.shape[1] >= N and out.stride(1) == 1
-    assert out.dtype == (torch.bfloat16 if mode in ("bf16", "bf16_gelu", "bf16_swiglu") else torch.float32)
+    if mode == "argmax":  # out: int64 keys [M], zeroed (see argmax_keys)
+        if out is None:
+            out = torch.zeros(M, device=a.device, dtype=torch.int64)
+        assert out.dtype == torch.int64 and out.numel() >= M and out.is_contiguous()
+    else:
+        if out is None:
+            assert mode in ("bf16", "f32", "bf16_gelu", "bf16_swiglu")
+            out = torch.empty(M, N, device=a.device, dtype=torch.float32 if mode == "f32" else torch.bfloat16)
+        assert out.shape[0] >= M and out.shape[1] >= N and out.stride(1) == 1
+        assert out.dtype == (torch.bfloat16 if mode in ("bf16", "bf16_gelu", "bf16_swiglu") else torch.float32)
     if bias is not None:
         assert bias.dtype == torch.bfloat16 and bias.numel() == N
     g = MaceGemmArgs(
         a=_ptr(a), lda=a.stride(0), a_mn_major=int(a_mn),
         b=_ptr(b), ldb=b.stride(0), b_mn_major=int(b_mn),
         M=M, N=N, K=K,
-        out=_ptr(out), ldo=out.stride(0), mode=EPI[mode],
+        out=_ptr(out), ldo=0 if mode == "argmax" else out.stride(0), mode=EPI[mode],
         bias=_ptr(bias), alpha=float(alpha), split_k=int(split_k),
         workspace=_ptr(workspace), workspace_bytes=0 if workspace is None else workspace.numel() * workspace.element_size(),
         flags=1 if b_static else 0,
     )
     ctx.check(ctx.L.mace_gemm_bf16(ctx.h, C.byref(g), _stream(stream)), "mace_gemm_bf16")
+    return out
+
+
+def argmax_keys(ctx: Ctx, keys: torch.Tensor, n: int | None = None, out: torch.Tensor | None = None,
+                stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Token ids from the keys of an ``argmax`` GEMM (first index on ties); resets the keys to zero."""
+    n = keys.numel() if n is None else n
+    assert keys.dtype == torch.int64 and keys.is_contiguous()
+    if out is None:
+        out = torch.empty(n, device=keys.device, dtype=torch.int32)
+    ctx.check(ctx.L.mace_argmax_keys(ctx.h, _ptr(keys), n, _ptr(out), _stream(stream)), "mace_argmax_keys")
     return out
 
 

@@ -10,7 +10,7 @@ the kernels happen to move:
                 dV, dK, dQ) for the FT backward of the selected layers;
   HBM bytes     paged decode attention (every visible K / V row once + q / o rows; measured per launch from the
                 device tables), and the row kernels: embedding, the two norms and RoPE / KV scatter of every layer
-                pass, the decode head's fp32 logits and argmax, the DPO logit passes, the FT backward's row kernels
+                pass, the decode head (norm; its argmax is fused into the lm_head GEMM), the DPO logit passes, the FT backward's row kernels
                 and the masked AdamW (30 B per updated parameter).
 
 roofline_ms = tensor_flops / tensor_peak + hbm_bytes / hbm_peak (each class is bound by one resource).
@@ -60,7 +60,7 @@ def tick_extras(batch, cfg, n_sel: int, n_updated_params: int, lora: bool = Fals
     layer_rows = (T * l_min + ft0 * n_sel) if has_ft else T * L
     byts = row(T, D * (2 + 4))                                   # embedding
     byts += layer_rows * (2 * norm_b + rope_b)
-    byts += row(n_dec, norm_b + V * 4 * 2)                       # decode head: norm, fp32 logits write + argmax read
+    byts += row(n_dec, norm_b + 8)                               # decode head: norm + argmax key (fused lm_head)
     if has_ft:
         sub_rows = 2 * n_sel * n_ft                              # pi_ref + policy sub-passes
         byts += sub_rows * (2 * norm_b + QKV * 2 * 2 + UP * 2 + F * 2 + 2 * 4 * D)  # + unfused act, saved copies
