@@ -201,7 +201,7 @@ class HybridModel:
         self._bufs = MaceTickBuffers()
         # True: the decode head writes the fp32 logits [n_dec, V] and takes the argmax over them (recorded oracle
         # replays read the logits); False: the lm_head GEMM's epilogue reduces each row to its argmax directly
-        self.keep_dec_logits = False
+        self.keep_dec_logits = os.environ.get("MACE_DEC_LOGITS") == "1"  # A/B switch
         self.mh = self._create_native()
 
     def _build_lora(self, lw: dict[str, torch.Tensor]) -> None:

@@ -49,7 +49,8 @@ torch.cuda.synchronize()
 # host issue cost with an idle device: one tick at a time, synchronized between ticks
 issue = []
 for op in tape:
-    if op[0] != "step":
+    if op[0] != "step":  # trims / releases / idle updates keep the device page state consistent: replay, untimed
+        model.replay([op])
         continue
     torch.cuda.synchronize()
     t0 = time.perf_counter()
