@@ -21,10 +21,16 @@ namespace mace {
 #ifdef MACE_DEC_TRACE
 __device__ unsigned long long* g_dec_trace = nullptr;  // [item][4]: start ns, end ns, pages, smid
 #endif
+#ifndef MACE_DEC2_WARPS64
+#define MACE_DEC2_WARPS64 12  // sweep overrides (-D) for hd <= 64
+#endif
+#ifndef MACE_DEC2_STAGES64
+#define MACE_DEC2_STAGES64 4
+#endif
 template <int HD, int G>
 struct Dec2 {
-  static constexpr int WARPS = HD >= 128 ? 8 : 12;
-  static constexpr int STAGES = HD >= 128 ? 3 : 4;
+  static constexpr int WARPS = HD >= 128 ? 8 : MACE_DEC2_WARPS64;
+  static constexpr int STAGES = HD >= 128 ? 3 : MACE_DEC2_STAGES64;
   static constexpr int PAGE = kPageTokens * HD * 2;
   static constexpr int STAGE = 2 * PAGE;                      // K page | V page
   static constexpr int QH = HD / 2 + 4;                       // padded half row of q (bank spread)
