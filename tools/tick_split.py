@@ -39,13 +39,28 @@ for op in tape:
     elif ticks:
         ticks[-1].append(op)
 evs = []
+dec_only = []  # (event pair, algorithmic HBM bytes) of ticks with decode rows only
+KIND_PREFILL = 0
 for ops in ticks:
+    bt = ops[0][1]
+    pure = bt.n_dec > 0 and not bt.ft_pairs and not (bt.seqs[:, 0] == KIND_PREFILL).any()
+    byts = model.decode_attn_bytes(bt) * cfg.n_layers if pure else 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     model.replay(ops)
     e1.record()
-    evs.append((e0, e1, bool(ops[0][1].ft_pairs), ops[0][1]))
+    evs.append((e0, e1, bool(bt.ft_pairs), bt))
+    if pure:
+        dec_only.append((e0, e1, byts, bt.n_dec))
 torch.cuda.synchronize()
+if dec_only:
+    import json as _json
+    hbm = _json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
+    wbytes = 2 * sum(v.numel() for k, v in model.w.items() if k != "pos_emb")  # every weight streamed once
+    ms = np.array([a.elapsed_time(b) for a, b, _, _ in dec_only])
+    roof = np.array([(wbytes + kv) / (hbm * 1e9) * 1e3 for _, _, kv, _ in dec_only])
+    print(f"decode-only ticks {len(dec_only)}: mean {ms.mean():.3f} ms, rows {np.mean([r for *_, r in dec_only]):.0f}, "
+          f"HBM roofline (weights + KV once) {roof.mean():.3f} ms -> frac {float((roof / ms).mean()):.3f}")
 ft = [a.elapsed_time(b) for a, b, f, _ in evs if f]
 nf = [a.elapsed_time(b) for a, b, f, _ in evs if not f]
 print(f"{name}: {len(evs)} ticks; FT ticks {len(ft)} mean {np.mean(ft) if ft else 0:.3f} ms; "
