@@ -582,7 +582,10 @@ struct Gemm2Cfg {
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
   static constexpr int kSmemBytes = kStages * kStageBytes + kCBytes + 1024 + 256;
 };
-constexpr int kGroupM = 16;
+#ifndef MACE_GEMM_GROUP_M
+#define MACE_GEMM_GROUP_M 16  // sweep override (-D)
+#endif
+constexpr int kGroupM = MACE_GEMM_GROUP_M;
 
 MACE_DEV void tile2_coords(int t, int num_m, int num_n, int& m_blk, int& n_blk) {
   const int group = t / (kGroupM * num_n);
