@@ -596,7 +596,7 @@ MACE_DEV void tile2_coords(int t, int num_m, int num_n, int& m_blk, int& n_blk) 
   n_blk = r / gm;
 }
 
-template <int BN>
+template <int BN, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c, const GemmParams p) {
@@ -644,7 +644,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     auto load_b = [&](int stage, int kb, int n_blk, uint32_t bar) {
       // swiglu: the leader holds the gate rows, the peer the up rows of the same BN/2 outputs
       const int row = p.swiglu ? (rank ? p.N : 0) + n_blk * (BN / 2) : n_blk * BN + rank * (BN / 2);
-      tma_load_2d_pair(smem_b + stage * Cfg::kBBytes, &map_b, bar, kb * kBK, row);
+      if constexpr (B_MN) {  // [K, N] storage: this CTA's BN/2 columns as 64-wide MN blocks
+#pragma unroll
+        for (int j = 0; j < BN / 128; ++j)
+          tma_load_2d_pair(smem_b + stage * Cfg::kBBytes + j * (64 * kBK * 2), &map_b, bar, row + j * 64, kb * kBK);
+      } else {
+        tma_load_2d_pair(smem_b + stage * Cfg::kBBytes, &map_b, bar, kb * kBK, row);
+      }
+    };
+    auto load_a = [&](int stage, int kb, int m_blk, uint32_t bar) {
+      const int row = m_blk * 256 + rank * 128;
+      if constexpr (A_MN) {  // [K, M] storage: this CTA's 128 rows as two 64-wide MN blocks
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          tma_load_2d_pair(smem_a + stage * Cfg::kABytes + j * (64 * kBK * 2), &map_a, bar, row + j * 64, kb * kBK);
+      } else {
+        tma_load_2d_pair(smem_a + stage * Cfg::kABytes, &map_a, bar, kb * kBK, row);
+      }
     };
     const uint32_t full0 = mapa_shared(smem_u32(&full_bar[0]), 0);  // leader's full barriers
     int pre = 0;
@@ -673,7 +689,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         if (elect_one()) {
           const uint32_t bar = full0 + stage * 8;
           if (rank == 0 && !b_done) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
-          tma_load_2d_pair(smem_a + stage * Cfg::kABytes, &map_a, bar, kb * kBK, m_blk * 256 + rank * 128);
+          load_a(stage, kb, m_blk, bar);
           if (!b_done) load_b(stage, kb, n_blk, bar);
         }
         __syncwarp();
@@ -685,7 +701,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
   } else if (warp == 1 && rank == 0) {
     // ------------------------------------------------ MMA issuer (leader only)
-    constexpr uint32_t idesc = idesc_bf16_f32(256, BN, false, false);
+    constexpr uint32_t idesc = idesc_bf16_f32(256, BN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -702,9 +718,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const uint32_t b_addr = b_base + stage * Cfg::kBBytes;
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            umma_bf16_pair(d_tmem, smem_desc_sw128(a_addr + k * 32, 16, 1024),
-                           smem_desc_sw128(b_addr + k * 32, 16, 1024), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < kBK / 16; ++k) {
+            // K-major: 16 K-elements = 32 B inside the swizzle atom; MN-major: 16 K-rows = 2048 B, LBO = one
+            // 64-wide MN block (as in the single-CTA kernel)
+            const uint64_t ad = A_MN ? smem_desc_sw128(a_addr + k * 2048, 64 * kBK * 2, 1024)
+                                     : smem_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
+                                     : smem_desc_sw128(b_addr + k * 32, 16, 1024);
+            umma_bf16_pair(d_tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          }
           umma_commit_pair(&empty_bar[stage], 0x3);
         }
         __syncwarp();
@@ -960,14 +982,15 @@ static int launch_gemm(MaceCtx* ctx, const MaceGemmArgs* g, int splits, cudaStre
   return 0;
 }
 
-template <int BN>
+template <int BN, bool A_MN, bool B_MN>
 static int launch_gemm2(MaceCtx* ctx, const MaceGemmArgs* g, cudaStream_t stream, const GemmEpilogue& ep) {
   using Cfg = Gemm2Cfg<BN>;
   CUtensorMap ma, mb, mc;
-  if (make_map(ctx, &ma, g->a, g->K, g->M, g->lda, kBK, 128))
+  if (A_MN ? make_map(ctx, &ma, g->a, g->M, g->K, g->lda, 64, kBK) : make_map(ctx, &ma, g->a, g->K, g->M, g->lda, kBK, 128))
     return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm2: tensor map A encode failed");
   const bool swiglu = ep.mode == EPI_BF16_SWIGLU;
-  if (make_map(ctx, &mb, g->b, g->K, swiglu ? 2 * g->N : g->N, g->ldb, kBK, BN / 2))
+  if (B_MN ? make_map(ctx, &mb, g->b, g->N, g->K, g->ldb, 64, kBK)
+           : make_map(ctx, &mb, g->b, g->K, swiglu ? 2 * g->N : g->N, g->ldb, kBK, BN / 2))
     return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm2: tensor map B encode failed");
   GemmParams p{};
   p.M = g->M;
@@ -988,7 +1011,7 @@ static int launch_gemm2(MaceCtx* ctx, const MaceGemmArgs* g, cudaStream_t stream
     mc = ma;  // unused: the argmax epilogue publishes keys with atomics
   else if (make_map_c(ctx, &mc, ep, g->M, g->N, 1))
     return mace_fail(ctx, MACE_ERR_LAUNCH, "gemm2: tensor map C encode failed");
-  auto kern = gemm_tc2_kernel<BN>;
+  auto kern = gemm_tc2_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -1000,6 +1023,14 @@ static int launch_gemm2(MaceCtx* ctx, const MaceGemmArgs* g, cudaStream_t stream
   launch_k(kern, grid, 256, Cfg::kSmemBytes, stream, ma, mb, mc, p);
   ctx->launches++;
   return 0;
+}
+
+template <int BN>
+static int dispatch_pair(MaceCtx* ctx, const MaceGemmArgs* g, cudaStream_t s, const GemmEpilogue& ep) {
+  if (!g->a_mn_major && !g->b_mn_major) return launch_gemm2<BN, false, false>(ctx, g, s, ep);
+  if (!g->a_mn_major && g->b_mn_major) return launch_gemm2<BN, false, true>(ctx, g, s, ep);
+  if (g->a_mn_major && !g->b_mn_major) return launch_gemm2<BN, true, false>(ctx, g, s, ep);
+  return launch_gemm2<BN, true, true>(ctx, g, s, ep);
 }
 
 template <int BN, bool T>
@@ -1054,7 +1085,7 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   const int num_m = (g->M + kBM - 1) / kBM;
   const int num_m2 = (g->M + 255) / 256;
   const int kb_total = (g->K + kBK - 1) / kBK;
-  const bool pair_ok = !g->a_mn_major && !g->b_mn_major && g->split_k <= 0 && g->mode != EPI_F32_ATOMIC &&
+  const bool pair_ok = g->split_k <= 0 && g->mode != EPI_F32_ATOMIC &&
                        (argmax || (((uintptr_t)g->out & 15) == 0 &&
                         ((size_t)g->ldo * ((g->mode == EPI_BF16 || g->mode == EPI_BF16_GELU || swiglu) ? 2 : 4)) % 16 == 0));
   const long sms = ctx->num_sms, pairs = ctx->num_sms / 2;
@@ -1117,7 +1148,7 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   ep.split_stride = 0;
   {
     if (pair_bn) {
-      const int rc2 = pair_bn == 256 ? launch_gemm2<256>(ctx, g, stream, ep) : launch_gemm2<128>(ctx, g, stream, ep);
+      const int rc2 = pair_bn == 256 ? dispatch_pair<256>(ctx, g, stream, ep) : dispatch_pair<128>(ctx, g, stream, ep);
       if (rc2) return rc2;
       return mace_check_launch(ctx, "gemm2");
     }

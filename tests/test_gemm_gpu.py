@@ -125,3 +125,32 @@ def test_gemm_swiglu(ctx, M, F, K):
     ref = torch.nn.functional.silu(g) * u
     err = (out.float() - ref).abs().max().item()
     assert err <= 2e-2 * ref.abs().max().item() + 1e-3, err
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 2048, 1024), (777, 1000, 520), (3000, 4096, 2304)])
+@pytest.mark.parametrize("a_mn,b_mn", [(False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("force", ["pair,128", "pair,256"])
+def test_gemm_cta_pair_mn_major(ctx, M, N, K, a_mn, b_mn, force, monkeypatch):
+    """CTA-pair kernel with MN-major operands (the fine-tune backward's dX = dY.W and dW = dY^T.X): against the
+    fp32 reference, and bit-identical to the single-CTA kernel (same K order of fp32 accumulation)."""
+    monkeypatch.setenv("MACE_GEMM_FORCE", force)
+    torch.manual_seed(M + N + K + 2 * a_mn + b_mn)
+    a = torch.randn((K, M) if a_mn else (M, K), device="cuda").bfloat16()
+    b = torch.randn((K, N) if b_mn else (N, K), device="cuda").bfloat16()
+    if a_mn and M % 8:
+        a = torch.nn.functional.pad(a, (0, 8 - M % 8))[:, :M]
+    if b_mn and N % 8:
+        b = torch.nn.functional.pad(b, (0, 8 - N % 8))[:, :N]
+    if not a_mn and K % 8:
+        pytest.skip("K-major rows need K % 8 == 0")
+    ref = _ref(a, b, a_mn, b_mn)
+    out = ops.gemm(ctx, a, b, mode="f32", a_mn=a_mn, b_mn=b_mn)
+    assert (out - ref).abs().max().item() <= 1e-3 * K ** 0.5 + 1e-2
+    acc0 = torch.randn(M, N, device="cuda")
+    acc = acc0.clone()
+    ops.gemm(ctx, a, b, acc, mode="f32_add", a_mn=a_mn, b_mn=b_mn)
+    assert torch.allclose(acc, acc0 + ref, atol=2e-2, rtol=1e-3)
+    y = ops.gemm(ctx, a, b, mode="bf16", a_mn=a_mn, b_mn=b_mn)
+    assert torch.allclose(y.float(), ref, atol=0.1, rtol=1e-2)
+    monkeypatch.setenv("MACE_GEMM_FORCE", "single")
+    assert torch.equal(out, ops.gemm(ctx, a, b, mode="f32", a_mn=a_mn, b_mn=b_mn))
