@@ -14,6 +14,7 @@
 //    form is what the fine-tune backward needs (dX = dY.W and dW = dY^T.X) without transposes.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "mace_internal.h"
@@ -1093,7 +1094,9 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   if (swiglu) {  // 256-wide accumulator tiles = 128 gate + 128 up columns of the same 128 outputs
     if (!pair_ok) return mace_fail(ctx, MACE_ERR_ARG, "gemm: SwiGLU output needs 16-byte aligned rows");
     bn = 256;
-    if ((long)num_m2 * ((g->N + 127) / 128) >= sms) pair_bn = 256;
+    // pair tiles from one wave on, and for decode-sized M (one 256-row pair tile holds all rows: same CTA count
+    // as two single-CTA m-tiles, half the weight bytes per SM)
+    if ((long)num_m2 * ((g->N + 127) / 128) >= sms || (num_m2 == 1 && g->M > 128)) pair_bn = 256;
   } else if (pair_ok && (long)num_m2 * ((g->N + 255) / 256) >= sms) {
     pair_bn = 256;
   } else if (!pair_ok && (long)num_m * ((g->N + 255) / 256) >= sms) {
@@ -1127,7 +1130,10 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     if (splits < 1) splits = 1;
   }
   // tuning override (tools/gemm_sweep.py): MACE_GEMM_FORCE="<bn>,<splits>" | "pair,<bn>" | "single"
-  if (const char* f = getenv("MACE_GEMM_FORCE"); f && !swiglu && !argmax) {
+  if (const char* f = getenv("MACE_GEMM_FORCE"); f && swiglu && !argmax) {  // SwiGLU: BN 256, pair or single only
+    if (!strcmp(f, "pair,256") && pair_ok) pair_bn = 256;
+    else if (!strcmp(f, "single")) pair_bn = 0;
+  } else if (f && !argmax) {
     int fb = 0, fs = 0;
     if (sscanf(f, "%d,%d", &fb, &fs) == 2) {
       if (fb == 64 || fb == 128 || fb == 192 || fb == 256) bn = fb;

@@ -16,8 +16,13 @@ SHAPES = [(1215, 2304, 768, "bf16"), (1215, 768, 768, "f32_add"), (1215, 3072, 7
           (256, 3072, 2048, "bf16"), (256, 2048, 2048, "f32_add"), (256, 16384, 2048, "bf16"),
           (256, 2048, 8192, "f32_add"), (256, 128256, 2048, "f32"), (2000, 3072, 2048, "bf16"),
           (2000, 2048, 8192, "f32_add")]
-if len(sys.argv) > 2 and sys.argv[1] == "--shapes":
-    SHAPES = [(int(a), int(b), int(c), d) for a, b, c, d in (x.split(",") for x in sys.argv[2:])]
+COLD = 1  # --cold N: cycle N copies of the weight operand (N x |B| > L2: weights stream from HBM, as in a tick)
+argv = sys.argv[1:]
+if len(argv) > 1 and argv[0] == "--cold":
+    COLD = int(argv[1])
+    argv = argv[2:]
+if len(argv) > 1 and argv[0] == "--shapes":
+    SHAPES = [(int(a), int(b), int(c), d) for a, b, c, d in (x.split(",") for x in argv[1:])]
 ctx = Ctx(0)
 ws = torch.empty(64 << 20, device="cuda")
 
@@ -28,16 +33,16 @@ def timed(M, N, K, mode, cfg, n=30):
     else:
         os.environ["MACE_GEMM_FORCE"] = cfg
     a = torch.randn(M, K, device="cuda").bfloat16()
-    b = torch.randn(N, K, device="cuda").bfloat16()
+    bs = [torch.randn(2 * N if mode == "bf16_swiglu" else N, K, device="cuda").bfloat16() for _ in range(COLD)]
     out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if mode.startswith("f32") else torch.bfloat16)
     s = torch.cuda.Stream()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
-        ops.gemm(ctx, a, b, out, mode=mode, workspace=ws, b_static=True)
+        ops.gemm(ctx, a, bs[0], out, mode=mode, workspace=ws, b_static=True)
         s.synchronize()
         with torch.cuda.graph(g, stream=s):
-            for _ in range(n):
-                ops.gemm(ctx, a, b, out, mode=mode, workspace=ws, b_static=True)
+            for i in range(n):
+                ops.gemm(ctx, a, bs[i % COLD], out, mode=mode, workspace=ws, b_static=True)
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -52,8 +57,9 @@ def timed(M, N, K, mode, cfg, n=30):
 
 
 for M, N, K, mode in SHAPES:
-    row = [(c, timed(M, N, K, mode, c)) for c in ["auto", "pair,128", "pair,256"] +
-           [f"{bn},{sp}" for bn in (64, 128, 192, 256) for sp in (1, 2, 3)]]
+    cfgs = ["auto", "pair,256", "single"] if mode == "bf16_swiglu" else \
+        ["auto", "pair,128", "pair,256"] + [f"{bn},{sp}" for bn in (64, 128, 192, 256) for sp in (1, 2, 3)]
+    row = [(c, timed(M, N, K, mode, c)) for c in cfgs]
     best = min((t, c) for c, t in row)
     print(f"M={M} N={N} K={K} {mode}: auto {row[0][1]:.2f} | best {best[1]} {best[0]:.2f} | "
           + " ".join(f"{c}:{t:.1f}" for c, t in row[1:]), flush=True)
