@@ -407,7 +407,8 @@ def run_ours(args, rank, world, lock):
     # dram traffic per launch of each roofline kernel from the committed ncu --set full captures (newest first);
     # a capture is attached only when it profiled this workload's shape (same kernel template)
     cap_gemm, cap_attn = {"c2": (None, "attn_decode"), "c4": ("gemm_pair", "attn_decode_tc")}.get(wl.name, (None, None))
-    summaries = [ROOT / "profiles" / n for n in ("r2s3_ncu_full_summary.json", "r2_ncu_full_summary.json",
+    summaries = [ROOT / "profiles" / n for n in ("r2f_ncu_full_summary.json", "r2s3_ncu_full_summary.json",
+                                                  "r2_ncu_full_summary.json",
                                                   "r1final_ncu_full_summary.json")]
     for cap, target in ((cap_gemm, roof_gemm), (cap_attn, roof_attn)):
         for prof in summaries:
