@@ -19,6 +19,7 @@
 // cores do tile t's softmax. Multi-chunk items write (m, l, o) partials merged in chunk order by the
 // last finishing CTA (deterministic).
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "mace_internal.h"
@@ -52,8 +53,12 @@ struct DecItem {  // page-slot range of one item, computed identically by every 
   int seq, h, chunk, nch, pbase, slot, n_pv, npp, kvh, d0, db, de, r0, s0, s1;
 };
 
-template <int HD, int G>
-__global__ void __launch_bounds__(192, 1) attn_decode_tc_kernel(
+// SPLIT = 1: the S = K.Q^T MMAs and the O = V^T.P MMAs are issued by two threads in different warps (warp 5 and
+// warp 6), so P.V(t) -- and with it the release of tile t's K / V stage -- goes out the moment the softmax publishes
+// P(t), instead of queueing behind the arrival of tile t+1 for S(t+1) in a single issuer's program order. Each
+// issuer's tcgen05.commit tracks only its own MMAs; the two streams touch disjoint TMEM columns.
+template <int HD, int G, int SPLIT>
+__global__ void __launch_bounds__(SPLIT ? 224 : 192, 1) attn_decode_tc_kernel(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
     const __grid_constant__ CUtensorMap qmap, const MaceSeq* __restrict__ seqs, const int4* __restrict__ items,
     int n_items, const MaceKvLayout kv, int Hq, int Hkv, float scale_log2, __nv_bfloat16* __restrict__ out,
@@ -74,12 +79,13 @@ __global__ void __launch_bounds__(192, 1) attn_decode_tc_kernel(
   uint64_t* ofull = pfull + 2;              // [2]  (pempty == ofull: P(t) is free once P.V(t) completed)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::N_BARS);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NT = SPLIT ? 224 : 192;
 
   // ---- setup: zero V stages, Q and P (skipped page slots / padded heads multiply as finite zeros)
   for (int s = 0; s < C::STAGES; ++s)
-    for (int i = tid * 16; i < C::TILE; i += 192 * 16)
+    for (int i = tid * 16; i < C::TILE; i += NT * 16)
       *reinterpret_cast<uint4*>(smem + (2 * s + 1) * C::TILE + i) = make_uint4(0, 0, 0, 0);
-  for (int i = C::Q_OFF + tid * 16; i < C::RED_OFF; i += 192 * 16)
+  for (int i = C::Q_OFF + tid * 16; i < C::RED_OFF; i += NT * 16)
     *reinterpret_cast<uint4*>(smem + i) = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -148,39 +154,42 @@ __global__ void __launch_bounds__(192, 1) attn_decode_tc_kernel(
 
   if (warp == 4) {
     // ================================================================ producer (TMA)
-    if (lane == 0) {
-      uint32_t t = 0, it_local = 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++it_local) {
-        const DecItem d = item_info(idx);
-        const int qb = it_local & 1;
+    // The whole warp: lane q < 8 resolves page slot q of a tile (page-table loads of the 8 slots in parallel,
+    // one tile ahead, so their L2 round trip overlaps the ring wait and the previous tile's TMA issue), lane 0
+    // arms the stage barrier, every lane with a live page issues its own K / V boxes. (ncu, one lane resolving
+    // 8 slots in sequence: 8 dependent L2 round trips per 128-token tile bounded the kernel.)
+    uint32_t t = 0, it_local = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++it_local) {
+      const DecItem d = item_info(idx);
+      const int qb = it_local & 1;
+      if (lane == 0) {
         mbar_wait(&qempty[qb], ((it_local >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&qfull[qb], C::KATOMS * G * C::SWZ);
         const int qrow = seqs[d.seq].q_start * (Hq + 2 * Hkv) + d.h * G;
 #pragma unroll
         for (int a = 0; a < C::KATOMS; ++a)
           tma_load_2d(smem + C::Q_OFF + qb * C::Q_BYTES + a * 16 * C::SWZ, &qmap, &qfull[qb], a * C::ATOM, qrow);
-        const int n_tiles = (d.s1 - d.s0 + 7) / 8;
-        for (int j = 0; j < n_tiles; ++j, ++t) {
-          const int st = t % C::STAGES;
+      }
+      const int n_tiles = (d.s1 - d.s0 + 7) / 8;
+      int pg_next = -1, lo, hi;
+      if (lane < 8) slot_info(d, lane, pg_next, lo, hi);
+      for (int j = 0; j < n_tiles; ++j, ++t) {
+        const int st = t % C::STAGES;
+        const int pg = pg_next;
+        if (lane < 8 && j + 1 < n_tiles) slot_info(d, 8 * (j + 1) + lane, pg_next, lo, hi);
+        const uint32_t live = __ballot_sync(0xffffffffu, lane < 8 && pg >= 0);
+        if (lane == 0) {
           mbar_wait(&empty[st], ((t / C::STAGES) & 1) ^ 1);
-          int pages[8], nbox = 0;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            int lo, hi;
-            slot_info(d, 8 * j + q, pages[q], lo, hi);
-            nbox += pages[q] >= 0;
-          }
-          mbar_arrive_expect_tx(&full[st], nbox * 2 * C::KATOMS * 16 * C::SWZ);
+          mbar_arrive_expect_tx(&full[st], __popc(live) * 2 * C::KATOMS * 16 * C::SWZ);
+        }
+        __syncwarp();
+        if (lane < 8 && pg >= 0) {
           uint8_t* ks = smem + 2 * st * C::TILE;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            if (pages[q] < 0) continue;
-#pragma unroll
-            for (int a = 0; a < C::KATOMS; ++a) {
-              tma_load_2d(ks + a * C::ATOM_BYTES + q * 16 * C::SWZ, &kmap, &full[st], a * C::ATOM, pages[q] * 16);
-              tma_load_2d(ks + C::TILE + a * C::ATOM_BYTES + q * 16 * C::SWZ, &vmap, &full[st], a * C::ATOM,
-                          pages[q] * 16);
-            }
+          for (int a = 0; a < C::KATOMS; ++a) {
+            tma_load_2d(ks + a * C::ATOM_BYTES + lane * 16 * C::SWZ, &kmap, &full[st], a * C::ATOM, pg * 16);
+            tma_load_2d(ks + C::TILE + a * C::ATOM_BYTES + lane * 16 * C::SWZ, &vmap, &full[st], a * C::ATOM,
+                        pg * 16);
           }
         }
       }
@@ -229,10 +238,36 @@ __global__ void __launch_bounds__(192, 1) attn_decode_tc_kernel(
           }
           umma_commit(&sfull[sb]);
           if (j == n_tiles - 1) umma_commit(&qempty[qb]);
-          if (t > 0) issue_pv(t - 1);
+          if (!SPLIT && t > 0) issue_pv(t - 1);
         }
       }
-      if (t > 0) issue_pv(t - 1);
+      if (!SPLIT && t > 0) issue_pv(t - 1);
+    }
+  } else if (warp == 6) {
+    // ================================================================ P.V issuer (SPLIT only)
+    if (SPLIT && lane == 0) {
+      constexpr uint32_t idesc_o = idesc_bf16_f32(128, 16, true, false);
+      constexpr uint32_t lbo_v = C::KATOMS > 1 ? C::ATOM_BYTES : 0;
+      uint32_t tp = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const DecItem d = item_info(idx);
+        const int n_tiles = (d.s1 - d.s0 + 7) / 8;
+        for (int j = 0; j < n_tiles; ++j, ++tp) {
+          const int pb = tp & 1;
+          mbar_wait(&pfull[pb], (tp >> 1) & 1);  // P(tp) published => S(tp) done => stage tp's K / V landed
+          tc_fence_after();
+          const uint32_t va = smem_u32(smem + (2 * (tp % C::STAGES) + 1) * C::TILE);
+          const uint32_t pa = smem_u32(smem + C::P_OFF + pb * C::P_BYTES);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t ad = smem_desc(va + k * 16 * C::SWZ, lbo_v, 8 * C::SWZ, C::LAYOUT);
+            const uint64_t bd = smem_desc(pa + (k / 4) * (16 * 128) + (k % 4) * 32, 16, 1024, 2u);
+            umma_bf16(tmem + 32 + pb * 16, ad, bd, idesc_o, k > 0 ? 1u : 0u);
+          }
+          umma_commit(&ofull[pb]);
+          umma_commit(&empty[tp % C::STAGES]);
+        }
+      }
     }
   } else {
     // ================================================================ softmax + epilogue (warps 0-3)
@@ -408,7 +443,7 @@ static bool encode_rows(MaceCtx* ctx, CUtensorMap* m, const void* base, long lon
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int HD, int G>
+template <int HD, int G, int SPLIT>
 int launch_decode_tc(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStream_t s) {
   using C = DecTc<HD>;
   CUtensorMap km, vm, qm;
@@ -422,13 +457,13 @@ int launch_decode_tc(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStream_
     return mace_fail(ctx, MACE_ERR_ARG, "attn decode: workspace/counters too small");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_tc_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(attn_decode_tc_kernel<HD, G, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
   const int per_sm = (227 * 1024) / C::SMEM;
   int grid = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
   if (grid > a->n_dec) grid = a->n_dec;
-  launch_k(attn_decode_tc_kernel<HD, G>, grid, 192, C::SMEM, s, km, vm, qm, a->seqs,
+  launch_k(attn_decode_tc_kernel<HD, G, SPLIT>, grid, SPLIT ? 224 : 192, C::SMEM, s, km, vm, qm, a->seqs,
            reinterpret_cast<const int4*>(a->dec_items), a->n_dec, a->kv, a->Hq, a->Hkv, sl2, (__nv_bfloat16*)a->out,
            a->head_norm, (float*)a->dec_workspace, a->dec_counters);
   ctx->launches++;
@@ -437,12 +472,19 @@ int launch_decode_tc(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStream_
 
 int dispatch_decode_tc(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStream_t s) {
   const int G = a->Hq / a->Hkv;
+  // MACE_DTC_ISSUE=1: one MMA issuer (S and P.V in one thread's program order); default 2 (split issuers)
+  static const int split = [] {
+    const char* e = getenv("MACE_DTC_ISSUE");
+    return (e && atoi(e) == 1) ? 0 : 1;
+  }();
+#define MACE_DTC_G(HD_, G_) \
+  return split ? launch_decode_tc<HD_, G_, 1>(ctx, a, sl2, s) : launch_decode_tc<HD_, G_, 0>(ctx, a, sl2, s);
 #define MACE_DTC(HD_)                                                 \
   switch (G) {                                                        \
-    case 1: return launch_decode_tc<HD_, 1>(ctx, a, sl2, s);          \
-    case 2: return launch_decode_tc<HD_, 2>(ctx, a, sl2, s);          \
-    case 4: return launch_decode_tc<HD_, 4>(ctx, a, sl2, s);          \
-    case 8: return launch_decode_tc<HD_, 8>(ctx, a, sl2, s);          \
+    case 1: MACE_DTC_G(HD_, 1)                                        \
+    case 2: MACE_DTC_G(HD_, 2)                                        \
+    case 4: MACE_DTC_G(HD_, 4)                                        \
+    case 8: MACE_DTC_G(HD_, 8)                                        \
     default: return mace_fail(ctx, MACE_ERR_UNSUPPORTED, "attn decode: GQA group must be 1, 2, 4 or 8"); \
   }
   switch (a->hd) {
@@ -452,6 +494,7 @@ int dispatch_decode_tc(MaceCtx* ctx, const MaceAttnArgs* a, float sl2, cudaStrea
     default: return mace_fail(ctx, MACE_ERR_UNSUPPORTED, "attn decode: head_dim must be 32, 64 or 128");
   }
 #undef MACE_DTC
+#undef MACE_DTC_G
 }
 
 }  // namespace mace
