@@ -418,8 +418,10 @@ def run_ours(args, rank, world, lock):
     dominant_gemm = (roof_gemm["share_of_step"] or 0.0) >= (roof_attn["share_of_step"] or 0.0)
     # dram traffic per launch of each roofline kernel from the committed ncu --set full captures (newest first);
     # a capture is attached only when it profiled this workload's shape (same kernel template)
-    cap_gemm, cap_attn = {"c2": (None, "attn_decode"), "c4": ("gemm_pair", "attn_decode_tc")}.get(wl.name, (None, None))
-    summaries = [ROOT / "profiles" / n for n in ("r2f_ncu_full_summary.json", "r2s3_ncu_full_summary.json",
+    cap_gemm, cap_attn = {"c2": (None, "attn_decode"), "c3": (None, "r2s5f_dtc_c3"),
+                          "c4": ("gemm_pair", "r2s5f_dtc_c4")}.get(wl.name, (None, None))
+    summaries = [ROOT / "profiles" / n for n in ("r2s5f_ncu_full_summary.json", "r2f_ncu_full_summary.json",
+                                                  "r2s3_ncu_full_summary.json",
                                                   "r2_ncu_full_summary.json",
                                                   "r1final_ncu_full_summary.json")]
     for cap, target in ((cap_gemm, roof_gemm), (cap_attn, roof_attn)):
