@@ -77,20 +77,35 @@ class ClockSampler:
         self.gpu = gpu
         self.samples: list[tuple[int, int]] = []
         self.max_mhz = None
+        self.h = None
+        self.error = None
         self._stop = threading.Event()
+
+    def _read(self, h):
+        import pynvml
+
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        try:
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        return sm, r
 
     def _run(self):
         import pynvml
 
-        h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        try:
+            h = self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.error = repr(e)
+            return
         while not self._stop.is_set():
-            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
             try:
-                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            except Exception:
-                r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-            self.samples.append((time.perf_counter(), sm, r))
+                sm, r = self._read(h)
+                self.samples.append((time.perf_counter(), sm, r))
+            except Exception as e:  # noqa: BLE001  (one failed poll must not end the sampling)
+                self.error = repr(e)
             time.sleep(0.002)
 
     def __enter__(self):
@@ -114,8 +129,14 @@ class ClockSampler:
         smp = [(s, r) for t, s, r in self.samples if (t0 is None or t >= t0) and (t1 is None or t <= t1)]
         if not smp:  # window shorter than one NVML poll: take the nearest samples around it
             smp = [(s, r) for t, s, r in self.samples][-3:]
+        if not smp and self.h is not None:  # the poller recorded nothing: one direct reading right after the window
+            try:
+                smp = [self._read(self.h)]
+            except Exception as e:  # noqa: BLE001
+                self.error = repr(e)
         if not smp:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0,
+                    "error": self.error}
         reasons = sorted({n for _, r in smp for bit, n in self.REASONS.items() if r & bit})
         return {"sm_mhz": statistics.median(s for s, _ in smp), "sm_max_mhz": self.max_mhz,
                 "reasons": reasons, "samples": len(smp)}

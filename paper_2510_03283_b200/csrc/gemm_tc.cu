@@ -549,7 +549,9 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   }
-  if (TMA_EPI && warp >= 4 && lane == 0) bulk_wait<0>();  // staged stores complete before exit
+  // the staging smem must outlive the stores' reads; their global writes complete with the grid (the dependent
+  // kernel's griddepcontrol.wait orders after them), so the CTA does not wait for the write round trip
+  if (TMA_EPI && warp >= 4 && lane == 0) bulk_wait_read<0>();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -845,7 +847,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         acc_phase ^= 1;
       }
     }
-    if (lane == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait_read<0>();  // smem reads of the stores done (writes complete with the grid)
   }
   tc_fence_before();
   cluster_sync();  // the peer's epilogue arrivals and the leader's MMAs are done before TMEM is released
