@@ -491,7 +491,15 @@ def cpu_baseline(args, wl, skip, model, budget_s=20.0):
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
     _, timed = _window_compositions(wl, skip, args.warmup, args.steps, wl.model.max_pos)
-    w = {n: t.float().cpu() for n, t in model.w.items()}
+    # base weights at their model shapes (with per-tenant LoRA the selected layers' device tensors carry the adapter
+    # columns [W | B] next to W: the CPU arm runs the base projections, ~0.4% fewer FLOPs than the adapted ones)
+    shapes = wl.model.param_shapes()
+    w = {}
+    for n, t in model.w.items():
+        sh = shapes.get(n)
+        if sh is not None and t.dim() == 2 and tuple(t.shape) != sh:
+            t = t[: sh[0], : sh[1]]
+        w[n] = t.float().cpu()
     ex = SampledTickCPU(wl.model, w)
     ex.run(sample_rows(timed[0], min(16, args.cpu_rows)))  # warm (threads, allocator)
     secs = rows = ticks = 0
