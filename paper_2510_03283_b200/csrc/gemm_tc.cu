@@ -1120,7 +1120,18 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
     }
     if (pair_ok && kb_total >= 32) {  // the pair kernel's longer fill (~0.6 us) only pays off over long K loops
       const long t2 = (long)num_m2 * ((g->N + 127) / 128);
-      if ((double)((t2 + pairs - 1) / pairs) * kb_total * 0.155 + 0.6 < best) pair_bn = 128;
+      const double c128 = (double)((t2 + pairs - 1) / pairs) * kb_total * 0.155 + 0.6;
+      if (c128 < best) {
+        pair_bn = 128;
+        best = c128;
+      }
+      // pair BN 64 (each CTA stages 32 weight rows per k-block): sub-wave M <= ~1.2k projections with long K, e.g.
+      // M=256 N=2048 K=2048 9.4 -> 8.2 us, M=600 N=768 K=3072 11.9 -> 10.3 us (profiles/r2s5_pair64_sweep.log);
+      // K-major B only (the MN-major B loader moves 64-wide blocks of BN/2 >= 64 columns)
+      if (!g->b_mn_major && g->M > 128) {  // M <= 128 would leave the peer CTA's rows empty
+        const long t64 = (long)num_m2 * ((g->N + 63) / 64);
+        if ((double)((t64 + pairs - 1) / pairs) * kb_total * 0.13 + 0.6 < best) pair_bn = 64;
+      }
     }
   }
   int splits = g->split_k > 0 ? g->split_k : 1;
@@ -1144,7 +1155,7 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
       if (fb == 64 || fb == 128 || fb == 192 || fb == 256) bn = fb;
       if (fs >= 1) splits = fs;
       pair_bn = 0;
-    } else if (sscanf(f, "pair,%d", &fb) == 1 && (fb == 128 || fb == 256) && pair_ok) {
+    } else if (sscanf(f, "pair,%d", &fb) == 1 && (fb == 64 || fb == 128 || fb == 256) && pair_ok) {
       pair_bn = fb;
     } else {
       pair_bn = 0;
@@ -1159,7 +1170,9 @@ extern "C" int mace_gemm_bf16(mace_ctx* ctx_, const MaceGemmArgs* g, void* strea
   ep.split_stride = 0;
   {
     if (pair_bn) {
-      const int rc2 = pair_bn == 256 ? dispatch_pair<256>(ctx, g, stream, ep) : dispatch_pair<128>(ctx, g, stream, ep);
+      const int rc2 = pair_bn == 256   ? dispatch_pair<256>(ctx, g, stream, ep)
+                      : pair_bn == 128 ? dispatch_pair<128>(ctx, g, stream, ep)
+                                       : dispatch_pair<64>(ctx, g, stream, ep);
       if (rc2) return rc2;
       return mace_check_launch(ctx, "gemm2");
     }

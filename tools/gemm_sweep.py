@@ -58,7 +58,7 @@ def timed(M, N, K, mode, cfg, n=30):
 
 for M, N, K, mode in SHAPES:
     cfgs = ["auto", "pair,256", "single"] if mode == "bf16_swiglu" else \
-        ["auto", "pair,128", "pair,256"] + [f"{bn},{sp}" for bn in (64, 128, 192, 256) for sp in (1, 2, 3)]
+        ["auto", "pair,64", "pair,128", "pair,256"] + [f"{bn},{sp}" for bn in (64, 128, 192, 256) for sp in (1, 2, 3)]
     row = [(c, timed(M, N, K, mode, c)) for c in cfgs]
     best = min((t, c) for c, t in row)
     print(f"M={M} N={N} K={K} {mode}: auto {row[0][1]:.2f} | best {best[1]} {best[0]:.2f} | "
