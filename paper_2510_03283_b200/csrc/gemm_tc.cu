@@ -584,7 +584,10 @@ struct Gemm2Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kCBytes = 4 * 2 * 4096;
   static constexpr int kBudget = 227 * 1024 - kCBytes - 1024 - 256;
-  static constexpr int kStages = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
+#ifndef MACE_GEMM2_MAX_STAGES
+#define MACE_GEMM2_MAX_STAGES 8
+#endif
+  static constexpr int kStages = kBudget / kStageBytes > MACE_GEMM2_MAX_STAGES ? MACE_GEMM2_MAX_STAGES : kBudget / kStageBytes;
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
   static constexpr int kSmemBytes = kStages * kStageBytes + kCBytes + 1024 + 256;
 };
